@@ -1,0 +1,269 @@
+/*
+ * patchdyn_b200.h — C-ABI of the B200-native gap-tooth hot path.
+ *
+ * This is the drop-in boundary between the reference's C++ operator
+ * interfaces and the sm_100a kernels.  Plain pointers and sizes only; every
+ * pointer argument named *_host is host memory, *_dev is device memory.
+ * Citations are /root/reference/<path>:<line>.
+ *
+ * Entry point                      replaces (reference)
+ * -------------------------------  -------------------------------------------------
+ * pd_engine_create                 GapToothEngine ctor: patch list + PatchIntegrator
+ *                                  coefficient sampling  proj/src/gaptooth.cpp:200-282,
+ *                                  proj/src/microsim.cpp:204-263
+ * pd_gaptooth_step                 GapToothEngine::step_direct  proj/src/gaptooth.cpp:360-375
+ *                                  (proj/include/patchdyn/gaptooth.hpp:100)
+ * pd_projective_step               cpi::projective_step  proj/src/cpi.cpp:58-77
+ *                                  (proj/include/patchdyn/cpi.hpp:19-20)
+ * pd_run                           cpi::run macro loop + blow-up guard
+ *                                  proj/src/cpi.cpp:175-213 (cpi.hpp:45)
+ * pd_integrate_batch               PatchIntegrator::integrate, batched over patches
+ *                                  proj/src/microsim.cpp:509-552 (microsim.hpp:93-94)
+ * pd_lift_batch                    build_stencil + neumann_edge_slopes /
+ *                                  dirichlet_edge_values + lift
+ *                                  proj/src/gaptooth.cpp:74-168
+ * pd_restrict_batch                restrict_average  proj/src/gaptooth.cpp:170-194
+ * pd_last_error / pd_status        typed exceptions proj/include/patchdyn/errors.hpp:9-61
+ *
+ * Host-side problem builder (mesh/metric setup, stays on the host as in the
+ * reference; proj/src/geometry.cpp:93-125, microsim.cpp:226-263):
+ * pd_problem_create / pd_problem_engine_desc / pd_problem_initial_field /
+ * pd_problem_boundary / pd_problem_destroy.
+ *
+ * Threading: an engine owns one CUDA stream and is not thread-safe, matching
+ * the reference engine (gaptooth.hpp:121-122 mutable caches).
+ */
+#ifndef PATCHDYN_B200_H
+#define PATCHDYN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PD_ABI_VERSION 1
+
+/* Status codes map 1:1 onto the reference exception types
+ * (proj/include/patchdyn/errors.hpp:9-61). */
+typedef enum pd_status {
+    PD_OK = 0,
+    PD_NON_POSITIVE_JACOBIAN = 1,  /* NonPositiveJacobian  errors.hpp:13 */
+    PD_DERIVATIVE_MISMATCH = 2,    /* DerivativeMismatch   errors.hpp:16 */
+    PD_MIXED_TERM_UNSUPPORTED = 3, /* MixedTermUnsupported errors.hpp:19 */
+    PD_STABILITY_VIOLATION = 4,    /* StabilityViolation   errors.hpp:22 */
+    PD_INSUFFICIENT_STENCIL = 5,   /* InsufficientStencil  errors.hpp:25 */
+    PD_INDEX_OUT_OF_RANGE = 6,     /* IndexOutOfRange      errors.hpp:28 */
+    PD_SHAPE_MISMATCH = 7,         /* ShapeMismatch        errors.hpp:31 */
+    PD_INVALID_STRETCH = 8,        /* InvalidStretch       errors.hpp:34 */
+    PD_DOMAIN_ERROR = 9,           /* DomainError          errors.hpp:37 */
+    PD_MACRO_INSTABILITY = 12,     /* MacroInstability     errors.hpp:46 */
+    PD_MACRO_PATCH_ERROR = 13,     /* MacroPatchError      errors.hpp:50 */
+    PD_VALIDATION_ERROR = 15,      /* ValidationError      errors.hpp:56 */
+    PD_CUDA_ERROR = 100,           /* device failure (no reference analogue) */
+    PD_UNSUPPORTED = 101           /* feature outside the device path (ADI, general source) */
+} pd_status;
+
+/* SchemeConfig::BCType  proj/include/patchdyn/scheme_config.hpp:21-23 */
+enum { PD_BC_NEUMANN = 0, PD_BC_DIRICHLET = 1, PD_BC_ROBIN = 2 };
+/* microsim::EdgeKind  proj/include/patchdyn/microsim.hpp:23 */
+enum { PD_EDGE_DIRICHLET = 0, PD_EDGE_NEUMANN = 1, PD_EDGE_ROBIN = 2 };
+/* microsim::Edge order  microsim.hpp:26 */
+enum { PD_EDGE_E = 0, PD_EDGE_W = 1, PD_EDGE_N = 2, PD_EDGE_S = 3 };
+/* SchemeConfig::Quadrature  scheme_config.hpp:25-26 */
+enum { PD_QUAD_TRAPEZOID = 0, PD_QUAD_SIMPSON = 1 };
+/* source structure  microsim.hpp:58-64 */
+enum { PD_SOURCE_ZERO = 0, PD_SOURCE_SEPARABLE = 1 };
+/* Kernel family.  EXACT replays the reference's operation order (IEEE, no FMA
+ * contraction) and is bit-identical to the reference for b = 0; FAST is the
+ * register-blocked folded-weight kernel (FMA), within 1e-11 of it. */
+enum { PD_MODE_FAST = 0, PD_MODE_EXACT = 1 };
+
+/* Solver-form coefficient slots per micro node (microsim.hpp:101-102, plus the
+ * mixed term B = -b/l that the reference rejects at microsim.cpp:239-244). */
+enum { PD_COEF_A = 0, PD_COEF_B = 1, PD_COEF_C = 2, PD_COEF_VX = 3, PD_COEF_VY = 4,
+       PD_COEF_W = 5, PD_NCOEF = 6 };
+
+/* Everything the engine needs; the library copies all tables to the device
+ * and the caller keeps ownership of the host buffers. */
+typedef struct pd_engine_desc {
+    /* CoarseGrid  gaptooth.hpp:18-25 */
+    double a, b, c, d;
+    int32_t Nxi, Neta;
+    int32_t periodic_xi;
+    /* SchemeConfig subset  scheme_config.hpp:9-37 */
+    int32_t nx, ny, nt, k;
+    double tau;      /* gap-tooth horizon */
+    double dt_macro; /* projective step  SchemeConfig::dt() = T/Nt */
+    double h_xi, h_eta;
+    int32_t bc_type;
+    double robin_w1, robin_w2;
+    int32_t quadrature;
+    /* patch table in the reference's order (gaptooth.cpp:259-280): j outer,
+     * i inner.  NULL = build it in that order. */
+    int32_t npatches;
+    const int32_t* patch_ij; /* [npatches][2] */
+    /* solver-form coefficients, [ncoeff_sets][PD_NCOEF][nx+1][ny+1], node
+     * (i,j) at i*(ny+1)+j (field.hpp:20-27); coeff_set[p] selects the set of
+     * patch p (row sharing, gaptooth.cpp:254-266).  NULL coeff_set = identity. */
+    int32_t ncoeff_sets;
+    const int32_t* coeff_set;
+    const double* coeffs;
+    /* separable source g = spatial(xi,eta) * time(t) / l  (microsim.cpp:272-277) */
+    int32_t source_kind;
+    const double* source_spatial; /* [ncoeff_sets][nx+1][ny+1] or NULL */
+    double l;
+    int32_t mode;
+} pd_engine_desc;
+
+typedef struct pd_engine pd_engine;
+
+/* Run statistics of pd_run (cpi::RunResult subset, cpi.hpp:28-35). */
+typedef struct pd_run_stats {
+    int32_t steps_done;      /* macro steps completed without tripping the guard */
+    int32_t failed_step;     /* 1-based step that tripped the guard, 0 if none */
+    int32_t failed_nonfinite;/* 1 if the failure was a non-finite value */
+    double umax_last;        /* max |U| after the last completed step */
+    double blowup_threshold; /* 10 * max(max|U0|, 1e-12)  cpi.cpp:142-144 */
+    double device_ms;        /* device time of the macro loop (CUDA events) */
+    int64_t kernel_launches; /* kernels launched by this call */
+} pd_run_stats;
+
+int32_t pd_abi_version(void);
+const char* pd_status_name(int32_t status);
+/* Last error message of the engine, or the thread's last global error when
+ * engine == NULL (create failures). */
+const char* pd_last_error(const pd_engine* engine);
+
+/* Host-only (no device needed): the bit-exact index tables an engine for
+ * `desc` will use — patch list [P][2] (gaptooth.cpp:251-280 order unless
+ * desc->patch_ij is given) and 3x3 neighbour table [P][9] of flat macro
+ * indices i*(Neta+1)+j in build_stencil order (gaptooth.cpp:74-104).  Returns
+ * PD_MACRO_PATCH_ERROR for a patch whose stencil leaves the interior. */
+int32_t pd_patch_count(const pd_engine_desc* desc);
+pd_status pd_build_index_tables(const pd_engine_desc* desc, int32_t* patch_ij, int32_t* neighbours);
+
+pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out);
+void pd_engine_destroy(pd_engine* engine);
+/* Kernel family actually used by the engine (FAST may fall back to EXACT for
+ * shapes or features the fast kernel does not cover; never to a CPU path). */
+int32_t pd_engine_mode(const pd_engine* engine);
+/* Bit-exact index tables built by the engine: patch_ij [P][2] and the 3x3
+ * neighbour table [P][9] of flat macro indices i*(Neta+1)+j, stencil order
+ * vals[p+1][q+1] with p along xi (gaptooth.cpp:74-104).  Either may be NULL. */
+pd_status pd_engine_tables(const pd_engine* engine, int32_t* patch_ij, int32_t* neighbours);
+size_t pd_engine_device_bytes(const pd_engine* engine);
+/* Optional: run the engine on an external cudaStream_t (NULL = own stream). */
+pd_status pd_engine_set_stream(pd_engine* engine, void* cuda_stream);
+
+/* Boundary refresh arrays ("perimeter"): [S: Nxi+1][N: Nxi+1][W: Neta+1][E: Neta+1]
+ * applied in refresh_boundary's order (gaptooth.cpp:296-310): S/N rows, then
+ * W/E columns (or the periodic seam copy U(Nxi,j) = U(0,j)). */
+size_t pd_perimeter_len(int32_t Nxi, int32_t Neta);
+
+/* One gap-tooth step t -> t+tau over all patches (step_direct).  U_out gets a
+ * copy of U_in with every patch node replaced; then the boundary is refreshed
+ * from bnd (perimeter at t+tau) or, when bnd == NULL, kept from U_in (periodic
+ * seam applied).  src_time: [nt] values time(t+s*dt)/l for separable sources. */
+pd_status pd_gaptooth_step(pd_engine* e, const double* U_in_host, double* U_out_host, double t,
+                           const double* bnd_host, const double* src_time_host);
+/* One projective forward-Euler step t -> t+dt_macro (k+1 substeps fused).
+ * bnd: [k+2][perimeter] = refresh values at t+(m+1)tau (m=0..k) and t+dt, or NULL. */
+pd_status pd_projective_step(pd_engine* e, const double* U_in_host, double* U_out_host, double t,
+                             const double* bnd_host, const double* src_time_host);
+pd_status pd_projective_step_device(pd_engine* e, const double* U_in_dev, double* U_out_dev,
+                                    double t, const double* bnd_dev, const double* src_time_dev);
+/* nsteps projective steps from t0, device resident, with the blow-up guard of
+ * cpi.cpp:187-202.  U_host is in/out.  bnd: [nsteps][k+2][perimeter] or NULL
+ * (frozen).  Returns PD_MACRO_INSTABILITY when the guard trips; U_host then
+ * holds the field after the failing step, stats says which step. */
+pd_status pd_run(pd_engine* e, double* U_host, int32_t nsteps, double t0, const double* bnd_host,
+                 const double* src_time_host, pd_run_stats* stats);
+pd_status pd_run_device(pd_engine* e, double* U_dev, double* U_scratch_dev, int32_t nsteps,
+                        double t0, const double* bnd_dev, const double* src_time_dev,
+                        pd_run_stats* stats);
+
+/* Unfused micro-solver, batched: PatchIntegrator::integrate for every patch
+ * p (coefficient set coeff_set[p]) from u0 [P][n1][n2] over nt steps at t0.
+ * edge_kind[4] (E,W,N,S), edge_value/edge_slope [P][4][max(n1,n2)],
+ * robin_w[4][2].  Result in uT [P][n1][n2]. */
+pd_status pd_integrate_batch(pd_engine* e, const double* u0_host, const int32_t* edge_kind,
+                             const double* edge_value_host, const double* edge_slope_host,
+                             const double* robin_w, double t0, const double* src_time_host,
+                             double* uT_host);
+/* Lifting for P stencils [P][3][3] (vals[p+1][q+1]) centred at (xi_c,eta_c)
+ * [P][2]: u0 [P][n1][n2] plus the four edge profiles [P][4][max(n1,n2)] in
+ * E,W,N,S order (slopes for Neumann, values for Dirichlet, both for Robin:
+ * values then slopes).  dxi/deta are the macro spacings. */
+pd_status pd_lift_batch(pd_engine* e, int32_t nstencils, const double* vals_host,
+                        const double* centers_host, double* u0_host, double* edge_slope_host,
+                        double* edge_value_host);
+pd_status pd_restrict_batch(pd_engine* e, int32_t nfields, const double* u_host, double* avg_host);
+
+/* ---------------------------------------------------------------------------
+ * Host problem builder: the B200 framework's own mesh/metric setup for the
+ * BASELINE configs and the reference benchmark problems.  It samples
+ * transform_coefficients (geometry.cpp:93-125) at every micro node exactly as
+ * PatchIntegrator::sample_coeffs does (microsim.cpp:226-263), on the host.
+ * ------------------------------------------------------------------------- */
+enum {
+    PD_PROBLEM_DIFFUSION_SQUARE = 1, /* config 1: identity map, D=1, sin(pi x) sin(pi y) */
+    PD_PROBLEM_CDR_TANH = 2,         /* config 2: tanh-stretched CDR, exact solution */
+    PD_PROBLEM_ANNULUS_NONAXI = 3,   /* config 3: polar map, non-axisymmetric IC */
+    PD_PROBLEM_SHEAR_CDR = 4,        /* configs 4/5: sinusoidal non-orthogonal map */
+    PD_PROBLEM_REF_ANNULUS = 10,     /* problems::problem2_annulus  problems.cpp:110-138 */
+    PD_PROBLEM_REF_CDR = 11,         /* problems::problem1_constant(lambda)  problems.cpp:19-69 */
+    PD_PROBLEM_STEADY = 12           /* harmonic u = x + y (test_gaptooth.cpp:32-49) */
+};
+enum { PD_DT_GIVEN = 0, PD_DT_DIFFUSION = 1, PD_DT_METRIC = 2 };
+
+typedef struct pd_problem_desc {
+    int32_t problem;
+    double lambda;       /* REF_CDR stretching */
+    double beta;         /* CDR_TANH stretching */
+    double eps;          /* diffusivity */
+    double omega;        /* reaction coefficient c */
+    double vel;          /* constant velocity magnitude (CDR_TANH a = b) */
+    double amp;          /* SHEAR map amplitude (0.1) */
+    uint64_t seed;       /* SHEAR initial noise (mt19937_64) */
+    int32_t jacobi_sweeps;
+    /* SchemeConfig (scheme_config.hpp:9-37) */
+    int32_t N_xi, N_eta, Nt, k;
+    double T, tau, h_xi, h_eta;
+    int32_t nx, ny, nt;
+    int32_t bc_type;
+    double robin_w1, robin_w2;
+    int32_t quadrature;
+    int32_t mode;
+    /* pin rules; resolved by pd_problem_create */
+    int32_t dt_rule;     /* PD_DT_*: GIVEN uses tau; DIFFUSION 0.2 d^2/D; METRIC 0.2 min d^2 / max(|A|+|C|) */
+    double h_frac;       /* > 0: h = h_frac * macro spacing per direction */
+    double dt_over_tau;  /* > 0: T = Nt * dt_over_tau * tau */
+    int32_t threads;     /* host threads for coefficient sampling (0 = all) */
+} pd_problem_desc;
+
+typedef struct pd_problem pd_problem;
+
+pd_status pd_problem_create(const pd_problem_desc* desc, pd_problem** out);
+void pd_problem_destroy(pd_problem* p);
+/* The resolved description (tau, T, h filled in by the pin rules). */
+pd_status pd_problem_resolved(const pd_problem* p, pd_problem_desc* out);
+/* Engine descriptor whose table pointers stay valid while p lives. */
+pd_status pd_problem_engine_desc(const pd_problem* p, pd_engine_desc* out);
+/* GapToothEngine::initial_field (gaptooth.cpp:284-294): (Nxi+1)(Neta+1). */
+pd_status pd_problem_initial_field(const pd_problem* p, double* U_host);
+/* refresh_boundary values at time t as a perimeter array. */
+pd_status pd_problem_boundary(const pd_problem* p, double t, double* perimeter_host);
+/* Boundary table for pd_run: [nsteps][k+2][perimeter] from t0. */
+pd_status pd_problem_boundary_table(const pd_problem* p, double t0, int32_t nsteps, double* out_host);
+/* Exact solution on the macro grid at t; PD_UNSUPPORTED if none. */
+pd_status pd_problem_exact(const pd_problem* p, double t, double* U_host);
+/* max |A|+|C| over all sampled nodes (the dt pin's denominator) and the
+ * reference's single-direction stability number (microsim.cpp:253-262). */
+pd_status pd_problem_stability(const pd_problem* p, double* max_a_plus_c, double* ref_number);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PATCHDYN_B200_H */

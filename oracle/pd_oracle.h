@@ -1,0 +1,64 @@
+/*
+ * ORACLE / TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library,
+ * and only as the checker or the CPU baseline — never as the product path.
+ *
+ * CPU restatement of the reference's explicit gap-tooth hot path
+ * (/root/reference/proj/src/{gaptooth,microsim,cpi}.cpp), operation for
+ * operation in the reference's evaluation order (IEEE double, no FMA
+ * contraction: built with -ffp-contract=off), so that for b = 0 it reproduces
+ * the unmodified reference bit for bit.  Extension beyond the reference (which
+ * throws MixedTermUnsupported, microsim.cpp:239-244): the mixed derivative
+ * B*u_xi_eta with B = -b/l and the corner-ghost rule of SURVEY Appendix B.4.
+ * Parity status: b = 0 pinned against the reference itself (oracle/_ref);
+ * b != 0 pinned only by its own exactness/convergence/locality tests.
+ *
+ * Consumes the same pd_engine_desc tables as the B200 engine.
+ */
+#ifndef PD_ORACLE_H
+#define PD_ORACLE_H
+
+#include "patchdyn_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+void pdo_set_threads(int n);
+int pdo_get_threads(void);
+const char* pdo_last_error(void);
+
+/* build_stencil + slopes/values + lift for one stencil (gaptooth.cpp:74-168).
+ * slopes/values: [4][L] in E,W,N,S order, L = max(nx,ny)+1. */
+void pdo_lift(const double vals[9], double xi_c, double eta_c, double dxi, double deta,
+              double h_xi, double h_eta, int nx, int ny, double* u0, double* slopes,
+              double* values);
+/* restrict_average (gaptooth.cpp:170-194). */
+double pdo_restrict(const double* u, int n1, int n2, int quadrature);
+/* PatchIntegrator::integrate, explicit (microsim.cpp:509-552), extended with
+ * the mixed term.  coef: [6][n1][n2] solver form (A,B,C,Vx,Vy,W).  kinds[4]
+ * E,W,N,S; values/slopes [4][L]; robin_w [4][2].  src_spatial [n1][n2] and
+ * src_time [nt] (time(t0+s*dt)/l) or NULL.  u: in = initial, out = result.
+ * Returns a pd_status. */
+int pdo_integrate(const double* coef, int nx, int ny, int nt, double h_xi, double h_eta,
+                  double tau, const int* kinds, const double* values, const double* slopes,
+                  const double* robin_w, const double* src_spatial, const double* src_time,
+                  double* u);
+
+/* Engine-level restatements over the same descriptor as pd_engine_create. */
+int pdo_gaptooth_step(const pd_engine_desc* d, const double* U_in, double* U_out, double t,
+                      const double* bnd, const double* src_time);
+int pdo_projective_step(const pd_engine_desc* d, const double* U_in, double* U_out, double t,
+                        const double* bnd, const double* src_time);
+int pdo_run(const pd_engine_desc* d, double* U, int nsteps, double t0, const double* bnd,
+            const double* src_time, pd_run_stats* stats);
+/* Restricted patch averages after one gap-tooth substep for a subset of
+ * patches (indices into the patch table) — the sampled-parity and bounded
+ * CPU-baseline entry for configs too large to run whole.  Returns seconds. */
+double pdo_patch_subset(const pd_engine_desc* d, const double* U_in, double t, int nsub,
+                        const int* patch_index, double* avg_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,375 @@
+// FAST-mode fused gap-tooth kernel: register-blocked FP64 stencil.
+//
+// Mapping.  A patch of N1 x N2 micro nodes is split into
+// BI x BJ node blocks, one block per lane: LI = N1/BI lanes along xi, LJ =
+// N2/BJ along eta, LP = LI*LJ lanes per patch, G = 32/LP patches per warp.
+// Each lane keeps its nodes' state u and its nodes' folded stencil weights in
+// REGISTERS for all K micro-steps; neighbours cross lanes only through warp
+// shuffles (no shared memory or barriers in the hot loop).  The micro update
+// is the reference's explicit FTCS (microsim.cpp:313-329) with the
+// coefficients folded into per-node weights:
+//   u' = wC u + wE uE + wW uW + wN uN + wS uS + wD ((uNE+uSW)-(uNW+uSE)) + c
+// where c carries the frozen Neumann ghost offsets (microsim.cpp:146-167,
+// SURVEY B.4 corners) folded onto the patch-boundary ring once per macro step.
+//
+// Per macro step and patch: 3x3 gather through the neighbour table
+// (gaptooth.cpp:74-104), centre derivatives + quadratic lift
+// (gaptooth.cpp:63-72,154-168), edge slopes (gaptooth.cpp:132-152) as
+// shared-Lagrange dot products, K fused micro-steps, trapezoid restriction
+// (gaptooth.cpp:170-194) by a lane reduction, and the k = 0 projective
+// extrapolation (cpi.cpp:67-74) in the epilogue.
+#pragma once
+
+#include "pd_device.cuh"
+
+namespace pdb200::dev {
+
+struct FastPlan {
+    int id = -1;     // instantiation index
+    int LP = 0, G = 0, S = 0, nunits = 0;
+    int mixed = 0;
+};
+
+template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
+struct FastCfg {
+    static constexpr int N1 = N1_, N2 = N2_, BI = BI_, BJ = BJ_;
+    static constexpr bool MIXED = MIXED_;
+    static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, G = 32 / LP;
+    static constexpr int NPL = BI * BJ;          // nodes per lane
+    static constexpr int NW = MIXED ? 6 : 5;     // weights per node: C,E,W,N,S,(D)
+    static constexpr int NWL = NW * NPL;         // weight doubles per lane
+    static constexpr int S = (NWL + 1) / 2;      // 16-byte slots per lane
+    static constexpr int L = N1 > N2 ? N1 : N2;
+    static_assert(N1 % BI == 0 && N2 % BJ == 0, "block must tile the patch");
+    static_assert(LP <= 32, "patch must fit a warp");
+};
+enum { WC = 0, WE = 1, WW = 2, WN = 3, WS = 4, WD = 5 };
+constexpr int kFastWarps = 4;
+
+// ---- fold: solver-form coefficients -> lane-interleaved weight table -------
+// Table layout: unit u (one warp = G patches) owns S*32 double2 slots; slot s
+// of lane l is at ((u*S + s)*32 + l); lane-local weight index f = k*NPL + ii*BJ + jj.
+template <class Cfg>
+__global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* __restrict__ cset,
+                       double* __restrict__ W, int nunits) {
+    const size_t total = (size_t)nunits * 32 * (2 * Cfg::S);
+    const double idx2 = 1.0 / (p.mdxi * p.mdxi), idy2 = 1.0 / (p.mdeta * p.mdeta);
+    const double idx = 1.0 / (2.0 * p.mdxi), idy = 1.0 / (2.0 * p.mdeta);
+    const double ixy = 1.0 / (4.0 * p.mdxi * p.mdeta);
+    const double dt = p.mdt;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const int half = (int)(t & 1);
+        const size_t q = t >> 1;
+        const int lane = (int)(q % 32);
+        const size_t us = q / 32;
+        const int s = (int)(us % Cfg::S);
+        const size_t unit = us / Cfg::S;
+        const int f = 2 * s + half;
+        double val = 0.0;
+        const int g = lane / Cfg::LP, r = lane % Cfg::LP;
+        const long patch = (long)unit * Cfg::G + g;
+        if (g < Cfg::G && patch < p.P && f < Cfg::NWL) {
+            const int kind = f / Cfg::NPL, node = f % Cfg::NPL;
+            const int ii = node / Cfg::BJ, jj = node % Cfg::BJ;
+            const int bi = r % Cfg::LI, bj = r / Cfg::LI;
+            const int i = bi * Cfg::BI + ii, j = bj * Cfg::BJ + jj;
+            const int set = cset ? cset[patch] : (int)patch;
+            const double* c = coeffs + (size_t)set * PD_NCOEF * p.N;
+            const int k = i * p.n2 + j;
+            const double A = c[PD_COEF_A * p.N + k], B = c[PD_COEF_B * p.N + k], C = c[PD_COEF_C * p.N + k];
+            const double Vx = c[PD_COEF_VX * p.N + k], Vy = c[PD_COEF_VY * p.N + k], Wr = c[PD_COEF_W * p.N + k];
+            const double ax = A * idx2, vx = Vx * idx, cy = C * idy2, vy = Vy * idy;
+            switch (kind) {
+                case WE: val = dt * (ax - vx); break;
+                case WW: val = dt * (ax + vx); break;
+                case WN: val = dt * (cy - vy); break;
+                case WS: val = dt * (cy + vy); break;
+                case WD: val = dt * (B * ixy); break;
+                default: val = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr); break;
+            }
+        }
+        W[((unit * Cfg::S + s) * 32 + lane) * 2 + half] = val;
+    }
+}
+
+// ---- the fused step -------------------------------------------------------
+template <class Cfg>
+__global__ void __launch_bounds__(32 * kFastWarps)
+k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
+       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
+    constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LP = Cfg::LP, G = Cfg::G, NPL = Cfg::NPL;
+    constexpr int N1 = Cfg::N1, N2 = Cfg::N2, L = Cfg::L;
+    constexpr bool MIXED = Cfg::MIXED;
+    __shared__ double s_g[kFastWarps][G][4][L]; // ghost offsets per edge
+    __shared__ double s_red[kFastWarps][32];
+    if (fail_flag && *fail_flag) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int unit = blockIdx.x * kFastWarps + warp;
+    if (unit >= nunits) return; // warp-uniform
+    const int g = lane / LP, r = lane % LP;
+    const int bi = r % LI, bj = r / LI;
+    const int patch = unit * G + g;
+    const bool valid = g < G && patch < p.P;
+    const int gs = g < G ? g : 0;
+    // neighbour lanes; lanes without a neighbour inside the patch read themselves
+    const int srcE = (valid && bi < LI - 1) ? lane + 1 : lane;
+    const int srcW = (valid && bi > 0) ? lane - 1 : lane;
+    const int srcN = (valid && bj < Cfg::LJ - 1) ? lane + LI : lane;
+    const int srcS = (valid && bj > 0) ? lane - LI : lane;
+
+    // ---- weights: S coalesced 16-byte loads per lane -------------------
+    double w[2 * Cfg::S];
+    {
+        const double2* wp = reinterpret_cast<const double2*>(Wt) + (size_t)unit * Cfg::S * 32 + lane;
+#pragma unroll
+        for (int s = 0; s < Cfg::S; ++s) {
+            const double2 t = __ldg(wp + s * 32);
+            w[2 * s] = t.x;
+            w[2 * s + 1] = t.y;
+        }
+    }
+#define WT(k, ii, jj) w[(k) * NPL + (ii) * BJ + (jj)]
+
+    // ---- 3x3 stencil gather (neighbour table) --------------------------
+    double v[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + __ldg(nbr + 9 * patch + q)) : 0.0;
+
+    // centre derivatives (StencilPoly::center, gaptooth.cpp:63-72)
+    const double Dxi = p.Dxi, Deta = p.Deta;
+    const double Uxi = (v[7] - v[1]) / (2.0 * Dxi);
+    const double Ueta = (v[5] - v[3]) / (2.0 * Deta);
+    const double Uxx = (v[7] - 2.0 * v[4] + v[1]) / (Dxi * Dxi);
+    const double Uyy = (v[5] - 2.0 * v[4] + v[3]) / (Deta * Deta);
+    const double Uxy = (v[8] - v[6] - v[2] + v[0]) / (4.0 * Dxi * Deta);
+    const double C0 = v[4] - p.h_xi * p.h_xi / 24.0 * Uxx - p.h_eta * p.h_eta / 24.0 * Uyy;
+
+    // ---- ghost offsets g = +-2 delta * slope along the four edges ---------
+    // slope_E(j) = sum_q Lq(Y_j)[q] * sum_p Lp'(+h/2)[p] v[p][q]  (tensor Lagrange, gaptooth.cpp:43-61)
+    {
+        const double hx = 0.5 * p.h_xi, hy = 0.5 * p.h_eta;
+        const double ix2 = 1.0 / (Dxi * Dxi), iy2 = 1.0 / (Deta * Deta);
+        for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
+            double gv;
+            if (t < 2 * N2) {
+                const bool east = t < N2;
+                const int j = east ? t : t - N2;
+                const double X = east ? hx : -hx;
+                const double dp0 = (X - 0.5 * Dxi) * ix2, dp1 = -2.0 * X * ix2, dp2 = (X + 0.5 * Dxi) * ix2;
+                const double Y = -hy + p.mdeta * j;
+                const double q0 = 0.5 * Y * (Y - Deta) * iy2, q1 = 1.0 - Y * Y * iy2, q2 = 0.5 * Y * (Y + Deta) * iy2;
+                const double G0 = dp0 * v[0] + dp1 * v[3] + dp2 * v[6];
+                const double G1 = dp0 * v[1] + dp1 * v[4] + dp2 * v[7];
+                const double G2 = dp0 * v[2] + dp1 * v[5] + dp2 * v[8];
+                const double slope = q0 * G0 + q1 * G1 + q2 * G2;
+                gv = (east ? 2.0 : -2.0) * p.mdxi * slope;
+                s_g[warp][gs][east ? PD_EDGE_E : PD_EDGE_W][j] = gv;
+            } else {
+                const int u = t - 2 * N2;
+                const bool north = u < N1;
+                const int i = north ? u : u - N1;
+                const double Y = north ? hy : -hy;
+                const double dq0 = (Y - 0.5 * Deta) * iy2, dq1 = -2.0 * Y * iy2, dq2 = (Y + 0.5 * Deta) * iy2;
+                const double X = -hx + p.mdxi * i;
+                const double p0 = 0.5 * X * (X - Dxi) * ix2, p1 = 1.0 - X * X * ix2, p2 = 0.5 * X * (X + Dxi) * ix2;
+                const double H0 = dq0 * v[0] + dq1 * v[1] + dq2 * v[2];
+                const double H1 = dq0 * v[3] + dq1 * v[4] + dq2 * v[5];
+                const double H2 = dq0 * v[6] + dq1 * v[7] + dq2 * v[8];
+                const double slope = p0 * H0 + p1 * H1 + p2 * H2;
+                gv = (north ? 2.0 : -2.0) * p.mdeta * slope;
+                s_g[warp][gs][north ? PD_EDGE_N : PD_EDGE_S][i] = gv;
+            }
+        }
+    }
+    __syncwarp();
+    const double* gE = s_g[warp][gs][PD_EDGE_E];
+    const double* gW = s_g[warp][gs][PD_EDGE_W];
+    const double* gN = s_g[warp][gs][PD_EDGE_N];
+    const double* gS = s_g[warp][gs][PD_EDGE_S];
+
+    // ---- lift + boundary fold-in ------------------------------------------
+    double u[BI][BJ], c[BI][BJ];
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii) {
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+            const int i = bi * BI + ii, j = bj * BJ + jj;
+            const double X = -0.5 * p.h_xi + p.mdxi * i, Y = -0.5 * p.h_eta + p.mdeta * j;
+            u[ii][jj] = C0 + X * Uxi + Y * Ueta + 0.5 * X * X * Uxx + X * Y * Uxy + 0.5 * Y * Y * Uyy;
+            const bool Wb = i == 0, Eb = i == N1 - 1, Sb = j == 0, Nb = j == N2 - 1;
+            double cc = 0.0;
+            // single-edge reflections u_ghost = u_inner + g (microsim.cpp:314-323)
+            if (Wb) { cc += WT(WW, ii, jj) * gW[j]; WT(WE, ii, jj) += WT(WW, ii, jj); WT(WW, ii, jj) = 0.0; }
+            if (Eb) { cc += WT(WE, ii, jj) * gE[j]; WT(WW, ii, jj) += WT(WE, ii, jj); WT(WE, ii, jj) = 0.0; }
+            if (Sb) { cc += WT(WS, ii, jj) * gS[i]; WT(WN, ii, jj) += WT(WS, ii, jj); WT(WS, ii, jj) = 0.0; }
+            if (Nb) { cc += WT(WN, ii, jj) * gN[i]; WT(WS, ii, jj) += WT(WN, ii, jj); WT(WN, ii, jj) = 0.0; }
+            if constexpr (MIXED) {
+                if (Wb || Eb || Sb || Nb) {
+                    // the reflected node values cancel in (uNE+uSW)-(uNW+uSE); what
+                    // remains is the signed sum of ghost offsets (SURVEY B.4 corners)
+                    auto off = [&](int pp, int qq) {
+                        const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
+                        const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
+                        double o = 0.0;
+                        if (pp < 0) o += gW[qc];
+                        if (pp > N1 - 1) o += gE[qc];
+                        if (qq < 0) o += gS[pc];
+                        if (qq > N2 - 1) o += gN[pc];
+                        return o;
+                    };
+                    const double Doff = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
+                    cc += WT(WD, ii, jj) * Doff;
+                    WT(WD, ii, jj) = 0.0;
+                }
+            }
+            c[ii][jj] = cc;
+        }
+    }
+
+    // ---- K fused micro-steps, state and weights in registers --------------
+    for (int step = 0; step < p.nt; ++step) {
+        double hN[BI], hS[BI];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            hN[ii] = __shfl_sync(0xffffffffu, u[ii][0], srcN);
+            hS[ii] = __shfl_sync(0xffffffffu, u[ii][BJ - 1], srcS);
+        }
+        double cE[BJ + 2], cW[BJ + 2];
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+            cE[jj + 1] = __shfl_sync(0xffffffffu, u[0][jj], srcE);
+            cW[jj + 1] = __shfl_sync(0xffffffffu, u[BI - 1][jj], srcW);
+        }
+        if constexpr (MIXED) {
+            cE[0] = __shfl_sync(0xffffffffu, hS[0], srcE);
+            cE[BJ + 1] = __shfl_sync(0xffffffffu, hN[0], srcE);
+            cW[0] = __shfl_sync(0xffffffffu, hS[BI - 1], srcW);
+            cW[BJ + 1] = __shfl_sync(0xffffffffu, hN[BI - 1], srcW);
+        } else {
+            cE[0] = cE[BJ + 1] = cW[0] = cW[BJ + 1] = 0.0;
+        }
+        // value at block-relative (a, b), a in [-1,BI], b in [-1,BJ]
+        auto at = [&](int a, int b) -> double {
+            if (a == BI) return cE[b + 1];
+            if (a == -1) return cW[b + 1];
+            if (b == BJ) return hN[a];
+            if (b == -1) return hS[a];
+            return u[a][b];
+        };
+        double nu[BI][BJ];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+                double acc = fma(WT(WC, ii, jj), u[ii][jj], c[ii][jj]);
+                acc = fma(WT(WE, ii, jj), at(ii + 1, jj), acc);
+                acc = fma(WT(WW, ii, jj), at(ii - 1, jj), acc);
+                acc = fma(WT(WN, ii, jj), at(ii, jj + 1), acc);
+                acc = fma(WT(WS, ii, jj), at(ii, jj - 1), acc);
+                if constexpr (MIXED) {
+                    const double D = (at(ii + 1, jj + 1) + at(ii - 1, jj - 1)) - (at(ii - 1, jj + 1) + at(ii + 1, jj - 1));
+                    acc = fma(WT(WD, ii, jj), D, acc);
+                }
+                nu[ii][jj] = acc;
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) u[ii][jj] = nu[ii][jj];
+    }
+#undef WT
+
+    // ---- trapezoid restriction (gaptooth.cpp:170-194) ----------------------
+    double part = 0.0;
+    {
+        const double ox = 1.0 / (N1 - 1), oy = 1.0 / (N2 - 1);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            const int i = bi * BI + ii;
+            double row = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+                const int j = bj * BJ + jj;
+                row += ((j == 0 || j == N2 - 1) ? 0.5 * oy : oy) * u[ii][jj];
+            }
+            part += ((i == 0 || i == N1 - 1) ? 0.5 * ox : ox) * row;
+        }
+    }
+    s_red[warp][lane] = part;
+    __syncwarp();
+    if (valid && r == 0) {
+        double avg = 0.0;
+#pragma unroll
+        for (int q = 0; q < LP; ++q) avg += s_red[warp][g * LP + q];
+        const size_t node = (size_t)__ldg(nbr + 9 * patch + 4);
+        if (out_mode == 0) {
+            out[node] = avg;
+        } else if (out_mode == 1) {
+            const double U = v[4];
+            out[node] = U + p.dt_macro * ((avg - U) / p.tau); // cpi.cpp:54, 74 (k = 0)
+        } else {
+            out[patch] = avg;
+        }
+    }
+}
+
+// ---- instantiations --------------------------------------------------------
+using FC7 = FastCfg<7, 7, 1, 7, false>;
+using FC7M = FastCfg<7, 7, 1, 7, true>;
+using FC8 = FastCfg<8, 8, 2, 4, false>;
+using FC8M = FastCfg<8, 8, 2, 4, true>;
+using FC9 = FastCfg<9, 9, 3, 3, false>;
+using FC9M = FastCfg<9, 9, 3, 3, true>;
+using FC16 = FastCfg<16, 16, 2, 4, false>;
+using FC16M = FastCfg<16, 16, 2, 4, true>;
+
+#define PD_FAST_CONFIGS(X) X(0, FC7) X(1, FC7M) X(2, FC8) X(3, FC8M) X(4, FC9) X(5, FC9M) X(6, FC16) X(7, FC16M)
+
+inline bool plan_fast(const Params& p, FastPlan& plan) {
+    // only the Neumann patch conditions of every BASELINE config are folded
+    if (p.bc_type != PD_BC_NEUMANN || p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
+    int id = -1;
+#define PD_MATCH(ID, CFG) \
+    if (id < 0 && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
+    PD_FAST_CONFIGS(PD_MATCH)
+#undef PD_MATCH
+    if (id < 0) return false;
+    plan.id = id;
+    plan.mixed = p.mixed;
+#define PD_FILL(ID, CFG)                               \
+    if (id == ID) {                                    \
+        plan.LP = CFG::LP;                             \
+        plan.G = CFG::G;                               \
+        plan.S = CFG::S;                               \
+        plan.nunits = (p.P + CFG::G - 1) / CFG::G;     \
+    }
+    PD_FAST_CONFIGS(PD_FILL)
+#undef PD_FILL
+    return true;
+}
+
+inline size_t fast_weights_count(const FastPlan& plan, const Params&) {
+    return (size_t)plan.nunits * plan.S * 64;
+}
+
+inline void fold_weights(const FastPlan& plan, const Params& p, const double* coeffs, const int* cset, double* W,
+                         cudaStream_t s) {
+    const size_t total = fast_weights_count(plan, p);
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+#define PD_FOLD(ID, CFG) \
+    if (plan.id == ID) k_fold<CFG><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits);
+    PD_FAST_CONFIGS(PD_FOLD)
+#undef PD_FOLD
+}
+
+inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
+                        const int* nbr, const double* W, const int* fail, cudaStream_t s) {
+    const int blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
+#define PD_LAUNCH(ID, CFG) \
+    if (plan.id == ID) k_fast<CFG><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);
+    PD_FAST_CONFIGS(PD_LAUNCH)
+#undef PD_LAUNCH
+}
+
+} // namespace pdb200::dev

@@ -1,0 +1,617 @@
+// C-ABI implementation of the B200 gap-tooth engine (include/patchdyn_b200.h).
+//
+// Host orchestration only: validation (same error types as the reference),
+// table upload, kernel selection and launch, device-resident macro loop.
+// The kernels live in kernels_exact.cuh (reference-order EXACT mode),
+// kernels_fast.cuh (register-blocked FAST mode) and kernels_misc.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "kernels_exact.cuh"
+#include "kernels_fast.cuh"
+#include "kernels_misc.cuh"
+#include "patchdyn_b200.h"
+
+using namespace pdb200::dev;
+
+namespace pdb200 {
+namespace {
+thread_local std::string g_global_error;
+}
+void set_global_error(const std::string& m) { g_global_error = m; }
+} // namespace pdb200
+
+namespace {
+
+struct Status {
+    pd_status code;
+    std::string msg;
+};
+
+#define CUDA_TRY(expr)                                                                           \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess)                                                                   \
+            throw Status{PD_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e)};     \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count <= n && p) return;
+        free();
+        if (count == 0) return;
+        CUDA_TRY(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { free(); }
+};
+
+} // namespace
+
+struct pd_engine {
+    pd_engine_desc d{};
+    Params prm{};
+    int mode = PD_MODE_EXACT;
+    FastPlan fast{};
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::vector<int32_t> pij, nbr, cset;
+    DevBuf<int32_t> d_pij, d_nbr, d_cset, d_kinds, d_fail;
+    DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
+    DevBuf<unsigned long long> d_slot;
+    DevBuf<unsigned int> d_counter;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    size_t NF = 0, perim = 0;
+    size_t device_bytes = 0;
+
+    ~pd_engine() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+
+    void check_launch() {
+        ++launches;
+        CUDA_TRY(cudaGetLastError());
+    }
+
+    // ---- one gap-tooth substep F -> out (patch nodes) -------------------
+    void launch_step(const double* F, double* out, int out_mode, const double* srct, const int* fail) {
+        if (mode == PD_MODE_FAST) {
+            launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
+        } else {
+            k_gaptooth_exact<<<prm.P, kExactThreads, exact_smem_bytes(prm), stream>>>(
+                prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail);
+        }
+        check_launch();
+    }
+    void launch_refresh(double* out, const double* F, const double* bnd, const int* fail) {
+        const int n = 2 * (prm.Nxi + 1) + 2 * (prm.Neta + 1);
+        k_refresh<<<(n + 255) / 256, 256, 0, stream>>>(prm, out, F, bnd, fail);
+        check_launch();
+    }
+
+    // gap-tooth step (step_direct, gaptooth.cpp:360-375)
+    void gaptooth_step_dev(const double* in, double* out, const double* bnd, const double* srct, const int* fail) {
+        launch_step(in, out, OUT_FIELD, srct, fail);
+        launch_refresh(out, in, bnd, fail);
+    }
+
+    // projective step (cpi.cpp:58-77).  bnd: [k+2][perim] or null; srct [k+1][nt] or null.
+    void projective_dev(const double* in, double* out, const double* bnd, const double* srct, const int* fail) {
+        const int k = prm.k;
+        if (k == 0) {
+            launch_step(in, out, OUT_PROJECTIVE, srct, fail);
+            launch_refresh(out, in, bnd ? bnd + perim : nullptr, fail);
+            return;
+        }
+        d_chain.alloc(NF * (size_t)(k + 1));
+        const double* prev = in;
+        for (int m = 0; m <= k; ++m) {
+            double* nxt = d_chain.p + NF * m;
+            launch_step(prev, nxt, OUT_FIELD, srct ? srct + (size_t)prm.nt * m : nullptr, fail);
+            launch_refresh(nxt, prev, bnd ? bnd + perim * m : nullptr, fail);
+            prev = nxt;
+        }
+        const double* Uk = k == 0 ? in : d_chain.p + NF * (k - 1);
+        const double* Uk1 = d_chain.p + NF * k;
+        const double horizon = XSUB_host(prm.dt_macro, k * prm.tau);
+        k_extrapolate<<<(prm.P + 255) / 256, 256, 0, stream>>>(prm, out, Uk, Uk1, d_pij.p, horizon, fail);
+        check_launch();
+        launch_refresh(out, in, bnd ? bnd + perim * (k + 1) : nullptr, fail);
+    }
+    static double XSUB_host(double a, double b) { return a - b; }
+};
+
+namespace {
+
+pd_status fail_engine(pd_engine* e, const Status& s) {
+    if (e) e->err = s.msg;
+    pdb200::set_global_error(s.msg);
+    return s.code;
+}
+
+void validate_desc(const pd_engine_desc* d) {
+    auto bad = [](const std::string& m) { throw Status{PD_VALIDATION_ERROR, m}; };
+    if (!d) bad("null descriptor");
+    if (d->Nxi < 2 || d->Neta < 2) bad("coarse grid needs at least 2 intervals per direction");
+    if (d->nx < 2 || d->ny < 2) bad("micro grid needs nx, ny >= 2");
+    if (d->nt < 1) bad("micro grid needs nt >= 1");
+    if (!(d->h_xi > 0 && d->h_eta > 0 && d->tau > 0)) bad("micro grid needs positive h_xi, h_eta, tau");
+    if (d->k < 0) bad("k must be non-negative");
+    if (!(d->dt_macro > 0)) bad("macro step must be positive");
+    if (!d->coeffs) bad("coefficient table missing");
+    if (d->ncoeff_sets < 1) bad("no coefficient sets");
+    if (d->quadrature == PD_QUAD_SIMPSON && (d->nx % 2 || d->ny % 2))
+        throw Status{PD_VALIDATION_ERROR, "Simpson restriction needs an even micro resolution"};
+    if (d->bc_type == PD_BC_ROBIN && d->robin_w1 == 0.0 && d->robin_w2 == 0.0)
+        bad("robin patch conditions need nonzero weights");
+    if (d->source_kind == PD_SOURCE_SEPARABLE && !d->source_spatial) bad("separable source needs a spatial table");
+}
+
+Params make_params(const pd_engine_desc& d, int P) {
+    Params p{};
+    p.a = d.a;
+    p.b = d.b;
+    p.c = d.c;
+    p.d = d.d;
+    p.Dxi = (d.b - d.a) / d.Nxi;
+    p.Deta = (d.d - d.c) / d.Neta;
+    p.Nxi = d.Nxi;
+    p.Neta = d.Neta;
+    p.NF2 = d.Neta + 1;
+    p.periodic = d.periodic_xi ? 1 : 0;
+    p.nx = d.nx;
+    p.ny = d.ny;
+    p.n1 = d.nx + 1;
+    p.n2 = d.ny + 1;
+    p.N = p.n1 * p.n2;
+    p.L = std::max(p.n1, p.n2);
+    p.nt = d.nt;
+    p.k = d.k;
+    p.tau = d.tau;
+    p.dt_macro = d.dt_macro;
+    p.h_xi = d.h_xi;
+    p.h_eta = d.h_eta;
+    p.mdxi = d.h_xi / d.nx;
+    p.mdeta = d.h_eta / d.ny;
+    p.mdt = d.tau / d.nt;
+    p.bc_type = d.bc_type;
+    p.w1 = d.robin_w1;
+    p.w2 = d.robin_w2;
+    p.quad = d.quadrature;
+    p.P = P;
+    p.nsets = d.ncoeff_sets;
+    p.source = d.source_kind;
+    return p;
+}
+
+template <class F>
+pd_status guarded(pd_engine* e, F&& fn) {
+    try {
+        fn();
+        return PD_OK;
+    } catch (const Status& s) {
+        return fail_engine(e, s);
+    } catch (const std::exception& x) {
+        return fail_engine(e, Status{PD_VALIDATION_ERROR, x.what()});
+    }
+}
+
+void upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+}
+void download(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+}
+
+} // namespace
+
+extern "C" {
+
+int32_t pd_abi_version(void) { return PD_ABI_VERSION; }
+
+const char* pd_status_name(int32_t s) {
+    switch (s) {
+        case PD_OK: return "ok";
+        case PD_NON_POSITIVE_JACOBIAN: return "NonPositiveJacobian";
+        case PD_DERIVATIVE_MISMATCH: return "DerivativeMismatch";
+        case PD_MIXED_TERM_UNSUPPORTED: return "MixedTermUnsupported";
+        case PD_STABILITY_VIOLATION: return "StabilityViolation";
+        case PD_INSUFFICIENT_STENCIL: return "InsufficientStencil";
+        case PD_INDEX_OUT_OF_RANGE: return "IndexOutOfRange";
+        case PD_SHAPE_MISMATCH: return "ShapeMismatch";
+        case PD_INVALID_STRETCH: return "InvalidStretch";
+        case PD_DOMAIN_ERROR: return "DomainError";
+        case PD_MACRO_INSTABILITY: return "MacroInstability";
+        case PD_MACRO_PATCH_ERROR: return "MacroPatchError";
+        case PD_VALIDATION_ERROR: return "ValidationError";
+        case PD_CUDA_ERROR: return "CudaError";
+        case PD_UNSUPPORTED: return "Unsupported";
+        default: return "Unknown";
+    }
+}
+
+const char* pd_last_error(const pd_engine* e) { return e ? e->err.c_str() : pdb200::g_global_error.c_str(); }
+
+size_t pd_perimeter_len(int32_t Nxi, int32_t Neta) { return 2 * (size_t)(Nxi + 1) + 2 * (size_t)(Neta + 1); }
+
+pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
+    if (!out) return PD_VALIDATION_ERROR;
+    *out = nullptr;
+    auto e = std::make_unique<pd_engine>();
+    const pd_status st = guarded(e.get(), [&] {
+        validate_desc(desc);
+        const pd_engine_desc& d = *desc;
+        e->d = d;
+        // bit-exact index tables (host/index_tables.cpp; gaptooth.cpp:74-104, 251-280)
+        const int P = pd_patch_count(&d);
+        if (P < 1) throw Status{PD_VALIDATION_ERROR, "empty patch table"};
+        e->pij.resize(2 * (size_t)P);
+        e->nbr.resize(9 * (size_t)P);
+        {
+            const pd_status ist = pd_build_index_tables(&d, e->pij.data(), e->nbr.data());
+            if (ist != PD_OK) throw Status{ist, pd_last_error(nullptr)};
+        }
+        if (d.coeff_set) {
+            e->cset.assign(d.coeff_set, d.coeff_set + P);
+            for (int v : e->cset)
+                if (v < 0 || v >= d.ncoeff_sets) throw Status{PD_SHAPE_MISMATCH, "coefficient set index out of range"};
+        } else if (d.ncoeff_sets < P) {
+            throw Status{PD_SHAPE_MISMATCH, "fewer coefficient sets than patches and no coeff_set map"};
+        }
+        e->prm = make_params(d, P);
+        Params& p = e->prm;
+        // mixed term present?  explicit stability guard (microsim.cpp:253-262)
+        const size_t Ncoef = (size_t)d.ncoeff_sets * PD_NCOEF * p.N;
+        double max_ac = 0.0;
+        bool mixed = false;
+        for (int s = 0; s < d.ncoeff_sets; ++s) {
+            const double* c = d.coeffs + (size_t)s * PD_NCOEF * p.N;
+            for (int k = 0; k < p.N; ++k) {
+                max_ac = std::max({max_ac, std::fabs(c[PD_COEF_A * p.N + k]), std::fabs(c[PD_COEF_C * p.N + k])});
+                if (c[PD_COEF_B * p.N + k] != 0.0) mixed = true;
+            }
+        }
+        p.mixed = mixed ? 1 : 0;
+        if (mixed && d.bc_type == PD_BC_ROBIN)
+            throw Status{PD_MIXED_TERM_UNSUPPORTED, "mixed-derivative term with Robin patch conditions is not defined"};
+        const double dmin = std::min(p.mdxi, p.mdeta);
+        const double number = max_ac * p.mdt / (dmin * dmin);
+        if (number > 0.5 + 1e-12) {
+            std::ostringstream m;
+            m << "explicit micro scheme diffusive stability number " << number << " exceeds 0.5";
+            throw Status{PD_STABILITY_VIOLATION, m.str()};
+        }
+        e->NF = (size_t)(d.Nxi + 1) * (d.Neta + 1);
+        e->perim = pd_perimeter_len(d.Nxi, d.Neta);
+        // device
+        CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->own_stream = true;
+        CUDA_TRY(cudaEventCreate(&e->ev0));
+        CUDA_TRY(cudaEventCreate(&e->ev1));
+        e->d_pij.alloc(e->pij.size());
+        e->d_nbr.alloc(e->nbr.size());
+        upload(e->d_pij.p, e->pij.data(), e->pij.size() * 4, e->stream);
+        upload(e->d_nbr.p, e->nbr.data(), e->nbr.size() * 4, e->stream);
+        if (!e->cset.empty()) {
+            e->d_cset.alloc(e->cset.size());
+            upload(e->d_cset.p, e->cset.data(), e->cset.size() * 4, e->stream);
+        }
+        e->d_coeffs.alloc(Ncoef);
+        upload(e->d_coeffs.p, d.coeffs, Ncoef * 8, e->stream);
+        if (d.source_kind == PD_SOURCE_SEPARABLE) {
+            e->d_src.alloc((size_t)d.ncoeff_sets * p.N);
+            upload(e->d_src.p, d.source_spatial, (size_t)d.ncoeff_sets * p.N * 8, e->stream);
+        }
+        e->d_U.alloc(2 * e->NF);
+        e->d_fail.alloc(4);
+        e->device_bytes = Ncoef * 8 + e->pij.size() * 4 + e->nbr.size() * 4 + 2 * e->NF * 8;
+        // kernel family
+        e->mode = PD_MODE_EXACT;
+        if (d.mode == PD_MODE_FAST && d.source_kind == PD_SOURCE_ZERO) {
+            if (plan_fast(p, e->fast)) {
+                const size_t wcount = fast_weights_count(e->fast, p);
+                e->d_weights.alloc(wcount);
+                fold_weights(e->fast, p, e->d_coeffs.p, e->d_cset.p, e->d_weights.p, e->stream);
+                e->check_launch();
+                e->device_bytes += wcount * 8;
+                e->mode = PD_MODE_FAST;
+            }
+        }
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+    if (st != PD_OK) return st;
+    *out = e.release();
+    return PD_OK;
+}
+
+void pd_engine_destroy(pd_engine* e) { delete e; }
+
+int32_t pd_engine_mode(const pd_engine* e) { return e ? e->mode : -1; }
+
+pd_status pd_engine_tables(const pd_engine* e, int32_t* patch_ij, int32_t* neighbours) {
+    if (!e) return PD_VALIDATION_ERROR;
+    if (patch_ij) std::memcpy(patch_ij, e->pij.data(), e->pij.size() * 4);
+    if (neighbours) std::memcpy(neighbours, e->nbr.data(), e->nbr.size() * 4);
+    return PD_OK;
+}
+
+size_t pd_engine_device_bytes(const pd_engine* e) { return e ? e->device_bytes : 0; }
+
+pd_status pd_engine_set_stream(pd_engine* e, void* s) {
+    if (!e) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        if (e->own_stream && e->stream) CUDA_TRY(cudaStreamDestroy(e->stream));
+        if (s) {
+            e->stream = static_cast<cudaStream_t>(s);
+            e->own_stream = false;
+        } else {
+            CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+            e->own_stream = true;
+        }
+    });
+}
+
+pd_status pd_gaptooth_step(pd_engine* e, const double* U_in, double* U_out, double t, const double* bnd,
+                           const double* src_time) {
+    if (!e || !U_in || !U_out) return PD_VALIDATION_ERROR;
+    (void)t;
+    return guarded(e, [&] {
+        const size_t NF = e->NF;
+        upload(e->d_U.p, U_in, NF * 8, e->stream);
+        const double* dbnd = nullptr;
+        if (bnd) {
+            e->d_bnd.alloc(e->perim);
+            upload(e->d_bnd.p, bnd, e->perim * 8, e->stream);
+            dbnd = e->d_bnd.p;
+        }
+        const double* dsrc = nullptr;
+        if (src_time && e->prm.source) {
+            e->d_srct.alloc(e->prm.nt);
+            upload(e->d_srct.p, src_time, e->prm.nt * 8, e->stream);
+            dsrc = e->d_srct.p;
+        }
+        CUDA_TRY(cudaMemsetAsync(e->d_fail.p, 0, 8, e->stream));
+        e->gaptooth_step_dev(e->d_U.p, e->d_U.p + NF, dbnd, dsrc, nullptr);
+        download(U_out, e->d_U.p + NF, NF * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+
+pd_status pd_projective_step_device(pd_engine* e, const double* in, double* out, double t, const double* bnd,
+                                    const double* src_time) {
+    if (!e || !in || !out) return PD_VALIDATION_ERROR;
+    (void)t;
+    return guarded(e, [&] { e->projective_dev(in, out, bnd, e->prm.source ? src_time : nullptr, nullptr); });
+}
+
+pd_status pd_projective_step(pd_engine* e, const double* U_in, double* U_out, double t, const double* bnd,
+                             const double* src_time) {
+    if (!e || !U_in || !U_out) return PD_VALIDATION_ERROR;
+    (void)t;
+    return guarded(e, [&] {
+        const size_t NF = e->NF;
+        upload(e->d_U.p, U_in, NF * 8, e->stream);
+        const double* dbnd = nullptr;
+        if (bnd) {
+            e->d_bnd.alloc(e->perim * (e->prm.k + 2));
+            upload(e->d_bnd.p, bnd, e->perim * (e->prm.k + 2) * 8, e->stream);
+            dbnd = e->d_bnd.p;
+        }
+        const double* dsrc = nullptr;
+        if (src_time && e->prm.source) {
+            e->d_srct.alloc((size_t)e->prm.nt * (e->prm.k + 1));
+            upload(e->d_srct.p, src_time, (size_t)e->prm.nt * (e->prm.k + 1) * 8, e->stream);
+            dsrc = e->d_srct.p;
+        }
+        e->projective_dev(e->d_U.p, e->d_U.p + NF, dbnd, dsrc, nullptr);
+        download(U_out, e->d_U.p + NF, NF * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+
+pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps, double t0, const double* bnd,
+                        const double* src_time, pd_run_stats* stats) {
+    if (!e || !U || !scratch || nsteps < 0) return PD_VALIDATION_ERROR;
+    (void)t0;
+    pd_status result = PD_OK;
+    const pd_status st = guarded(e, [&] {
+        const size_t NF = e->NF;
+        // blow-up threshold from the initial field  cpi.cpp:142-144
+        e->d_slot.alloc((size_t)nsteps + 1);
+        e->d_counter.alloc((size_t)nsteps + 1);
+        CUDA_TRY(cudaMemsetAsync(e->d_slot.p, 0, ((size_t)nsteps + 1) * 8, e->stream));
+        CUDA_TRY(cudaMemsetAsync(e->d_counter.p, 0, ((size_t)nsteps + 1) * 4, e->stream));
+        CUDA_TRY(cudaMemsetAsync(e->d_fail.p, 0, 16, e->stream));
+        const int gblocks = (int)std::min<size_t>(1184, (NF + 255) / 256);
+        // initial scale: flags go to the scratch pair d_fail[2..3], never to the run's flag
+        k_guard<<<gblocks, 256, 0, e->stream>>>(U, NF, e->d_slot.p + nsteps, e->d_counter.p + nsteps,
+                                                e->d_fail.p + 2, e->d_fail.p + 3, 0, INFINITY);
+        e->check_launch();
+        unsigned long long s0 = 0;
+        download(&s0, e->d_slot.p + nsteps, 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+        double scale0;
+        std::memcpy(&scale0, &s0, 8);
+        const double blowup = 10.0 * std::max(scale0, 1e-12);
+        const size_t pk = e->perim * (e->prm.k + 2);
+        const size_t sk = (size_t)e->prm.nt * (e->prm.k + 1);
+        const int64_t l0 = e->launches;
+        CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
+        double* cur = U;
+        double* nxt = scratch;
+        for (int n = 0; n < nsteps; ++n) {
+            e->projective_dev(cur, nxt, bnd ? bnd + pk * n : nullptr, (src_time && e->prm.source) ? src_time + sk * n : nullptr,
+                              e->d_fail.p);
+            k_guard<<<gblocks, 256, 0, e->stream>>>(nxt, NF, e->d_slot.p, e->d_counter.p, e->d_fail.p, e->d_fail.p + 1,
+                                                    n, blowup);
+            e->check_launch();
+            std::swap(cur, nxt);
+        }
+        CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+        int fail[2] = {0, 0};
+        download(fail, e->d_fail.p, 8, e->stream);
+        std::vector<unsigned long long> slots(nsteps > 0 ? nsteps : 1);
+        if (nsteps > 0) download(slots.data(), e->d_slot.p, 8 * (size_t)nsteps, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+        // the field after the last executed step lives in buffer (done % 2 == 1 ? scratch : U)
+        const int done = fail[0] ? fail[0] : nsteps;
+        if (done % 2 == 1) CUDA_TRY(cudaMemcpyAsync(U, scratch, NF * 8, cudaMemcpyDeviceToDevice, e->stream));
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+        pd_run_stats s{};
+        s.steps_done = fail[0] ? fail[0] - 1 : nsteps;
+        s.failed_step = fail[0];
+        s.failed_nonfinite = fail[1];
+        s.blowup_threshold = blowup;
+        s.device_ms = ms;
+        s.kernel_launches = e->launches - l0;
+        if (done > 0) {
+            double um;
+            std::memcpy(&um, &slots[done - 1], 8);
+            s.umax_last = um;
+        }
+        if (stats) *stats = s;
+        if (fail[0]) {
+            std::ostringstream m;
+            m << "coarse field " << (fail[1] ? "became non-finite" : "exceeded 10x the initial magnitude")
+              << " at macro step " << fail[0] << " (t=" << fail[0] * e->prm.dt_macro
+              << "); the projective step size is likely beyond the stable range";
+            e->err = m.str();
+            result = PD_MACRO_INSTABILITY;
+        }
+    });
+    return st != PD_OK ? st : result;
+}
+
+pd_status pd_run(pd_engine* e, double* U_host, int32_t nsteps, double t0, const double* bnd, const double* src_time,
+                 pd_run_stats* stats) {
+    if (!e || !U_host) return PD_VALIDATION_ERROR;
+    pd_status result = PD_OK;
+    const pd_status st = guarded(e, [&] {
+        const size_t NF = e->NF;
+        upload(e->d_U.p, U_host, NF * 8, e->stream);
+        const double* dbnd = nullptr;
+        if (bnd) {
+            const size_t n = e->perim * (e->prm.k + 2) * (size_t)nsteps;
+            e->d_bnd.alloc(n);
+            upload(e->d_bnd.p, bnd, n * 8, e->stream);
+            dbnd = e->d_bnd.p;
+        }
+        const double* dsrc = nullptr;
+        if (src_time && e->prm.source) {
+            const size_t n = (size_t)e->prm.nt * (e->prm.k + 1) * nsteps;
+            e->d_srct.alloc(n);
+            upload(e->d_srct.p, src_time, n * 8, e->stream);
+            dsrc = e->d_srct.p;
+        }
+        result = pd_run_device(e, e->d_U.p, e->d_U.p + NF, nsteps, t0, dbnd, dsrc, stats);
+        if (result != PD_OK && result != PD_MACRO_INSTABILITY) throw Status{result, e->err};
+        download(U_host, e->d_U.p, NF * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+    return st != PD_OK ? st : result;
+}
+
+pd_status pd_integrate_batch(pd_engine* e, const double* u0, const int32_t* edge_kind, const double* ev,
+                             const double* es, const double* robin_w, double t0, const double* src_time, double* uT) {
+    if (!e || !u0 || !edge_kind || !uT) return PD_VALIDATION_ERROR;
+    (void)t0;
+    return guarded(e, [&] {
+        const Params& p = e->prm;
+        for (int k = 0; k < 4; ++k)
+            if (edge_kind[k] < 0 || edge_kind[k] > 2) throw Status{PD_VALIDATION_ERROR, "bad edge kind"};
+        if (p.mixed)
+            for (int k = 0; k < 4; ++k)
+                if (edge_kind[k] == PD_EDGE_ROBIN)
+                    throw Status{PD_MIXED_TERM_UNSUPPORTED, "mixed-derivative term with Robin edges is not defined"};
+        const size_t nu = (size_t)p.P * p.N, ne = (size_t)p.P * 4 * p.L;
+        e->d_tmp.alloc(2 * nu + 2 * ne);
+        double* du0 = e->d_tmp.p;
+        double* duT = du0 + nu;
+        double* dev_ = duT + nu;
+        double* des = dev_ + ne;
+        upload(du0, u0, nu * 8, e->stream);
+        std::vector<double> zeros;
+        if (!ev || !es) zeros.assign(ne, 0.0);
+        upload(dev_, ev ? ev : zeros.data(), ne * 8, e->stream);
+        upload(des, es ? es : zeros.data(), ne * 8, e->stream);
+        e->d_kinds.alloc(4);
+        upload(e->d_kinds.p, edge_kind, 16, e->stream);
+        double rw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (robin_w) std::memcpy(rw, robin_w, sizeof rw);
+        e->d_rw.alloc(8);
+        upload(e->d_rw.p, rw, 64, e->stream);
+        const double* dsrc = nullptr;
+        if (src_time && p.source) {
+            e->d_srct.alloc(p.nt);
+            upload(e->d_srct.p, src_time, (size_t)p.nt * 8, e->stream);
+            dsrc = e->d_srct.p;
+        }
+        k_integrate_exact<<<p.P, kExactThreads, exact_smem_bytes(p), e->stream>>>(
+            p, du0, dev_, des, e->d_kinds.p, e->d_rw.p, e->d_cset.p, e->d_coeffs.p, e->d_src.p, dsrc, duT);
+        e->check_launch();
+        download(uT, duT, nu * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+
+pd_status pd_lift_batch(pd_engine* e, int32_t n, const double* vals, const double* centers, double* u0, double* es,
+                        double* ev) {
+    if (!e || n < 1 || !vals || !centers) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        const Params& p = e->prm;
+        const size_t nu = (size_t)n * p.N, ne = (size_t)n * 4 * p.L;
+        e->d_tmp2.alloc(9 * (size_t)n + 2 * (size_t)n + nu + 2 * ne);
+        double* dv = e->d_tmp2.p;
+        double* dc = dv + 9 * (size_t)n;
+        double* du = dc + 2 * (size_t)n;
+        double* ds = du + nu;
+        double* dval = ds + ne;
+        CUDA_TRY(cudaMemsetAsync(ds, 0, 2 * ne * 8, e->stream));
+        upload(dv, vals, 9 * (size_t)n * 8, e->stream);
+        upload(dc, centers, 2 * (size_t)n * 8, e->stream);
+        k_lift_exact<<<n, kExactThreads, 0, e->stream>>>(p, dv, dc, du, ds, dval);
+        e->check_launch();
+        if (u0) download(u0, du, nu * 8, e->stream);
+        if (es) download(es, ds, ne * 8, e->stream);
+        if (ev) download(ev, dval, ne * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+
+pd_status pd_restrict_batch(pd_engine* e, int32_t n, const double* u, double* avg) {
+    if (!e || n < 1 || !u || !avg) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        const Params& p = e->prm;
+        const size_t nu = (size_t)n * p.N;
+        e->d_tmp2.alloc(nu + n);
+        upload(e->d_tmp2.p, u, nu * 8, e->stream);
+        k_restrict_exact<<<n, kExactThreads, p.n1 * 8, e->stream>>>(p, e->d_tmp2.p, e->d_tmp2.p + nu);
+        e->check_launch();
+        download(avg, e->d_tmp2.p + nu, (size_t)n * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+
+} // extern "C"
