@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 gap-tooth hot path (BASELINE.json metric).
+
+One *step* = one projective forward-Euler macro step (k = 0: one fused
+gap-tooth substep over every patch + extrapolation + boundary refresh + the
+blow-up guard) of the headline workload, config 4 (512x512 patches of 16x16
+micro nodes, K = 50 micro-steps, 9-point non-orthogonal CDR, FP64).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c4_shear] [--no-cpu-baseline] [--sweep]
+
+N > 1 is launched by torchrun (one process per GPU); every rank runs an
+independent replica of the workload (the path shards by patches, but one
+macro field has a halo exchange per substep that this round does not build —
+DESIGN.md §6), so scaling is "weak" and value = all ranks' updates / max time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np
+
+from paper_2405_08764_b200 import abi, configs  # noqa: E402
+
+BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
+METRIC = BASELINE["metric"]
+UNIT = "patch-node updates/s"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def flops_per_update(mixed: bool) -> int:
+    # folded 5-point = 1 mul + 4 FMA = 9 flop; 9-point adds 5 -> 14
+    return 14 if mixed else 9
+
+
+def workload(desc):
+    n1, n2 = desc.nx + 1, desc.ny + 1
+    i_lo = 0 if desc.problem in (abi.PD_PROBLEM_ANNULUS_NONAXI, abi.PD_PROBLEM_REF_ANNULUS) else 1
+    P = (desc.N_xi - i_lo) * (desc.N_eta - 1)
+    return P, n1 * n2, desc.nt * (desc.k + 1)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_traffic(config_name: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text())
+    ent = d.get(config_name)
+    if not ent:
+        return None, None
+    return ent.get("dram_bytes_per_launch"), ent.get("source")
+
+
+def cpu_baseline(ed, U0, P, N, K, target_s=8.0):
+    """The restated oracle (port) on this host's cores over a bounded patch sample."""
+    from oracle.pyoracle import Restated  # checker / CPU baseline only
+
+    O = Restated()
+    threads = O.threads
+    rng = np.random.default_rng(1)
+    n = min(P, 256)
+    idx = np.sort(rng.choice(P, n, replace=False)).astype(np.int32)
+    _, sec = O.patch_subset(ed, U0, 0.0, idx)
+    rate = n * N * K / max(sec, 1e-9)
+    n2 = int(min(P, max(n, rate * target_s / (N * K))))
+    idx = np.sort(rng.choice(P, n2, replace=False)).astype(np.int32)
+    _, sec = O.patch_subset(ed, U0, 0.0, idx)
+    return {"value": n2 * N * K / sec, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n2} of {P} patches, one gap-tooth substep (K={K} micro-steps each) of the "
+                      f"restated oracle (oracle/pd_oracle.c, OpenMP over patches), {sec:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path on host cores."""
+    if rank != 0:
+        return 0
+    from oracle.pyoracle import Reference, Restated, reference_available
+    from paper_2405_08764_b200.engine import Problem
+
+    desc, _ = configs.load(args.config)
+    prob = Problem(desc)
+    r = prob.desc
+    P, N, K = workload(r)
+    ed = prob.engine_desc()
+    U0 = prob.initial_field()
+    _, Bmax = None, None
+    mixed = desc.problem == abi.PD_PROBLEM_SHEAR_CDR
+    cfg = {"workload": args.config, "patches": P, "micro_nodes": N, "K": K, "macro_steps": args.steps}
+    if not mixed and reference_available():
+        # the unmodified reference (oracle/_ref): cpi::projective_step, single-threaded
+        ref = Reference().engine(r)
+        U = ref.initial_field()
+        for n in range(args.warmup):
+            U = ref.projective_step(U, n * r.T / r.Nt)
+        t0 = time.perf_counter()
+        U, sec = ref.steps(U, args.warmup, args.steps)
+        wall = time.perf_counter() - t0
+        value = P * N * K * args.steps / sec
+        kind, cores, sample = "reference", 1, f"{args.steps} full macro steps of the unmodified reference " \
+                                                 f"(single-threaded by design, proj/src/gaptooth.cpp:362)"
+    else:
+        # config 4/5: the unmodified reference rejects b != 0 (MixedTermUnsupported,
+        # microsim.cpp:239-244) -> the restated oracle (reference + mixed term), all host threads
+        O = Restated()
+        rng = np.random.default_rng(7)
+        n = min(P, 2048)
+        idx = np.sort(rng.choice(P, n, replace=False)).astype(np.int32)
+        for _ in range(args.warmup):
+            O.patch_subset(ed, U0, 0.0, idx)
+        sec = 0.0
+        for _ in range(args.steps):
+            _, s = O.patch_subset(ed, U0, 0.0, idx)
+            sec += s
+        value = n * N * K * args.steps / sec
+        kind, cores = "port", O.threads
+        sample = (f"each step: {n} of {P} patches x one gap-tooth substep of the restated oracle "
+                  f"(the reference itself rejects b != 0), {cores} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4_shear")
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_08764_b200.engine import Engine, Problem, fp64_peak
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    desc, _ = configs.load(args.config)
+    desc.mode = configs.MODE[args.mode]
+    prob = Problem(desc)
+    r = prob.desc
+    eng = Engine.from_problem(prob)
+    P, N, K = workload(r)
+    ed = prob.engine_desc()
+    mixed = eng.mode == abi.PD_MODE_FAST and desc.problem == abi.PD_PROBLEM_SHEAR_CDR or \
+        desc.problem == abi.PD_PROBLEM_SHEAR_CDR
+    U0 = prob.initial_field()
+    NF = U0.size
+    dev = torch.device("cuda", local)
+    dU = torch.from_numpy(U0.ravel()).to(dev)
+    dS = torch.empty_like(dU)
+    torch.cuda.synchronize()
+
+    # warm-up (untimed), from the same initial field
+    eng.run_device(dU.data_ptr(), dS.data_ptr(), args.warmup)
+    dU.copy_(torch.from_numpy(U0.ravel()))
+    torch.cuda.synchronize()
+
+    # ---- timed region: exactly K macro steps, device-resident -------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    stats = eng.run_device(dU.data_ptr(), dS.data_ptr(), args.steps)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = stats.device_ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    updates_rank = P * N * K * args.steps
+    value = world * updates_rank / (ms * 1e-3)
+
+    # ---- dominant kernel alone + FP64 peak + roofline ----------------------
+    kms = eng.bench_step_kernel(dU.data_ptr(), dS.data_ptr(), reps=5)
+    p64, ghz = fp64_peak(200.0)
+    bw, bw_src = peaks()
+    fpu = flops_per_update(mixed)
+    ncoef = 6 if mixed else 5
+    flops_launch = P * N * K * fpu
+    bytes_launch = P * (N * 8 * ncoef + 16)
+    t_fp = flops_launch / (p64 * 1e12)
+    t_bw = bytes_launch / (bw * 1e9)
+    traffic, traffic_src = load_traffic(args.config)
+    if t_fp >= t_bw:
+        roof = {"bound": "fp64", "achieved": flops_launch / (kms * 1e-3) / 1e12, "peak": p64, "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": bytes_launch / (kms * 1e-3) / 1e9, "peak": bw, "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = traffic
+    roof.update({
+        "kernel": "k_fast (fused gap-tooth substep)" if eng.mode == abi.PD_MODE_FAST else "k_gaptooth_exact",
+        "kernel_ms": kms, "kernel_share_of_step": kms / (ms / args.steps),
+        "flops_per_update": fpu, "algorithmic_flops_per_launch": flops_launch,
+        "algorithmic_bytes_per_launch": bytes_launch,
+        "peak_source": f"FP64 DFMA microbenchmark measured in this run at {ghz:.3f} GHz; HBM {bw} GB/s from {bw_src}",
+        "roofline_time_ms": max(t_fp, t_bw) * 1e3, "frac_of_roofline_time": max(t_fp, t_bw) * 1e3 / kms,
+        "traffic_source": traffic_src})
+
+    # ---- end to end through the host C-ABI (pd_projective_step) ------------
+    ke = max(3, min(args.steps, 20))
+    Uh = torch.from_numpy(U0.ravel().copy()).pin_memory()
+    Oh = torch.empty_like(Uh).pin_memory()
+    Uh_np, Oh_np = Uh.numpy().reshape(U0.shape), Oh.numpy().reshape(U0.shape)
+    eng.projective_step(Uh_np, 0.0)  # warm
+    barrier()
+    t0 = time.perf_counter()
+    cur, nxt = Uh_np, Oh_np
+    dtm = r.T / r.Nt
+    import ctypes as C
+    from paper_2405_08764_b200.engine import lib as _lib, _check
+    L = _lib()
+    dp = C.POINTER(C.c_double)
+    for n in range(ke):
+        _check(L.pd_projective_step(eng.h, cur.ctypes.data_as(dp), nxt.ctypes.data_as(dp), n * dtm, None, None),
+               eng.h)
+        cur, nxt = nxt, cur
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": world * P * N * K * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": NF * 8,
+           "d2h_bytes_per_step": NF * 8, "steps": ke,
+           "path": "pd_projective_step (host pinned buffers, H2D + fused kernels + D2H each step)"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "patches": P, "micro_nodes": N, "K": K,
+                       "stencil": "9-point (mixed term)" if mixed else "5-point",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "kernel_family": "fast" if eng.mode == abi.PD_MODE_FAST else "exact",
+                       "l2": f"inputs larger than L2: {eng.device_bytes / 1e9:.2f} GB of device tables streamed "
+                             f"per macro step (> 126 MB L2)"},
+            "roofline": roof, "e2e": e2e, "gpu_launches": int(stats.kernel_launches), "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(ed, U0, P, N, K)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

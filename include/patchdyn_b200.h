@@ -184,6 +184,18 @@ pd_status pd_run_device(pd_engine* e, double* U_dev, double* U_scratch_dev, int3
                         double t0, const double* bnd_dev, const double* src_time_dev,
                         pd_run_stats* stats);
 
+/* Measurement hooks (no reference analogue; used by bench.py).
+ * pd_device_count: CUDA devices visible (0 on a CPU-only host).
+ * pd_bench_step_kernel: average device time (CUDA events on the engine's
+ *   stream) of the dominant kernel alone — the fused gap-tooth kernel of one
+ *   projective substep — over `reps` back-to-back launches in_dev -> out_dev.
+ * pd_bench_fp64_peak: register-resident DFMA microbenchmark on the current
+ *   device: sustained FP64 TFLOP/s (FMA = 2 flops) over ~ms_target ms. */
+int32_t pd_device_count(void);
+pd_status pd_bench_step_kernel(pd_engine* e, const double* in_dev, double* out_dev, int32_t reps,
+                               double* ms_per_launch);
+pd_status pd_bench_fp64_peak(double ms_target, double* tflops, double* sm_clock_ghz);
+
 /* Unfused micro-solver, batched: PatchIntegrator::integrate for every patch
  * p (coefficient set coeff_set[p]) from u0 [P][n1][n2] over nt steps at t0.
  * edge_kind[4] (E,W,N,S), edge_value/edge_slope [P][4][max(n1,n2)],

@@ -20,6 +20,8 @@
 // extrapolation (cpi.cpp:67-74) in the epilogue.
 #pragma once
 
+#include <cstdlib>
+
 #include "pd_device.cuh"
 
 namespace pdb200::dev {
@@ -28,6 +30,7 @@ struct FastPlan {
     int id = -1;     // instantiation index
     int LP = 0, G = 0, S = 0, nunits = 0;
     int mixed = 0;
+    int variant = 0; // 0: difference form of the mixed term, 1: corner form
 };
 
 template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
@@ -93,7 +96,7 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
 }
 
 // ---- the fused step -------------------------------------------------------
-template <class Cfg>
+template <class Cfg, int VAR>
 __global__ void __launch_bounds__(32 * kFastWarps)
 k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
        const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
@@ -111,11 +114,12 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
     const int patch = unit * G + g;
     const bool valid = g < G && patch < p.P;
     const int gs = g < G ? g : 0;
-    // neighbour lanes; lanes without a neighbour inside the patch read themselves
-    const int srcE = (valid && bi < LI - 1) ? lane + 1 : lane;
-    const int srcW = (valid && bi > 0) ? lane - 1 : lane;
-    const int srcN = (valid && bj < Cfg::LJ - 1) ? lane + LI : lane;
-    const int srcS = (valid && bj > 0) ? lane - LI : lane;
+    // Neighbour blocks are at lane +-1 (xi) and lane +-LI (eta).  The exchange
+    // uses constant-delta shuffles (SHFL.DOWN/UP with an immediate), which
+    // overlap with DFMA issue on B200, unlike SHFL.IDX with a register lane
+    // (measured: scripts/ubench/ubench2.cu).  A lane on a
+    // patch edge receives some other finite value for the missing side; the
+    // boundary fold-in below has zeroed every weight that would read it.
 
     // ---- weights: S coalesced 16-byte loads per lane -------------------
     double w[2 * Cfg::S];
@@ -231,20 +235,20 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
         double hN[BI], hS[BI];
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
-            hN[ii] = __shfl_sync(0xffffffffu, u[ii][0], srcN);
-            hS[ii] = __shfl_sync(0xffffffffu, u[ii][BJ - 1], srcS);
+            hN[ii] = __shfl_down_sync(0xffffffffu, u[ii][0], LI);
+            hS[ii] = __shfl_up_sync(0xffffffffu, u[ii][BJ - 1], LI);
         }
         double cE[BJ + 2], cW[BJ + 2];
 #pragma unroll
         for (int jj = 0; jj < BJ; ++jj) {
-            cE[jj + 1] = __shfl_sync(0xffffffffu, u[0][jj], srcE);
-            cW[jj + 1] = __shfl_sync(0xffffffffu, u[BI - 1][jj], srcW);
+            cE[jj + 1] = __shfl_down_sync(0xffffffffu, u[0][jj], 1);
+            cW[jj + 1] = __shfl_up_sync(0xffffffffu, u[BI - 1][jj], 1);
         }
-        if constexpr (MIXED) {
-            cE[0] = __shfl_sync(0xffffffffu, hS[0], srcE);
-            cE[BJ + 1] = __shfl_sync(0xffffffffu, hN[0], srcE);
-            cW[0] = __shfl_sync(0xffffffffu, hS[BI - 1], srcW);
-            cW[BJ + 1] = __shfl_sync(0xffffffffu, hN[BI - 1], srcW);
+        if constexpr (MIXED && VAR == 1) {
+            cE[0] = __shfl_down_sync(0xffffffffu, hS[0], 1);
+            cE[BJ + 1] = __shfl_down_sync(0xffffffffu, hN[0], 1);
+            cW[0] = __shfl_up_sync(0xffffffffu, hS[BI - 1], 1);
+            cW[BJ + 1] = __shfl_up_sync(0xffffffffu, hN[BI - 1], 1);
         } else {
             cE[0] = cE[BJ + 1] = cW[0] = cW[BJ + 1] = 0.0;
         }
@@ -256,22 +260,62 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
             if (b == -1) return hS[a];
             return u[a][b];
         };
+        // Term-major order: the NPL accumulation chains of this lane advance
+        // together, so consecutive DFMAs are independent (8-way ILP per warp)
+        // and the terms that use shuffled values come last.
         double nu[BI][BJ];
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii) {
+        for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) {
-                double acc = fma(WT(WC, ii, jj), u[ii][jj], c[ii][jj]);
-                acc = fma(WT(WE, ii, jj), at(ii + 1, jj), acc);
-                acc = fma(WT(WW, ii, jj), at(ii - 1, jj), acc);
-                acc = fma(WT(WN, ii, jj), at(ii, jj + 1), acc);
-                acc = fma(WT(WS, ii, jj), at(ii, jj - 1), acc);
-                if constexpr (MIXED) {
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WC, ii, jj), u[ii][jj], c[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WN, ii, jj), at(ii, jj + 1), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WS, ii, jj), at(ii, jj - 1), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WE, ii, jj), at(ii + 1, jj), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
+        if constexpr (MIXED && VAR == 1) {
+            // corner form: D = (uNE + uSW) - (uNW + uSE), 4 DP per node
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < BJ; ++jj) {
                     const double D = (at(ii + 1, jj + 1) + at(ii - 1, jj - 1)) - (at(ii - 1, jj + 1) + at(ii + 1, jj - 1));
-                    acc = fma(WT(WD, ii, jj), D, acc);
+                    nu[ii][jj] = fma(WT(WD, ii, jj), D, nu[ii][jj]);
                 }
-                nu[ii][jj] = acc;
+        } else if constexpr (MIXED) {
+            // difference form: e(i,j) = u(i+1,j) - u(i-1,j) once per node, then
+            // D(i,j) = e(i,j+1) - e(i,j-1); e crosses lanes only at the block's
+            // eta ends.  3 DP per node instead of 4 (8 per update in total).
+            double e[BI][BJ];
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < BJ; ++jj) e[ii][jj] = at(ii + 1, jj) - at(ii - 1, jj);
+            double eN[BI], eS[BI];
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii) {
+                eN[ii] = __shfl_down_sync(0xffffffffu, e[ii][0], LI);
+                eS[ii] = __shfl_up_sync(0xffffffffu, e[ii][BJ - 1], LI);
             }
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < BJ; ++jj) {
+                    const double up = jj + 1 < BJ ? e[ii][jj + 1] : eN[ii];
+                    const double dn = jj > 0 ? e[ii][jj - 1] : eS[ii];
+                    nu[ii][jj] = fma(WT(WD, ii, jj), up - dn, nu[ii][jj]);
+                }
         }
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii)
@@ -336,6 +380,7 @@ inline bool plan_fast(const Params& p, FastPlan& plan) {
 #undef PD_MATCH
     if (id < 0) return false;
     plan.id = id;
+    if (const char* v = std::getenv("PD_FAST_VARIANT")) plan.variant = std::atoi(v); // dev A/B switch
     plan.mixed = p.mixed;
 #define PD_FILL(ID, CFG)                               \
     if (id == ID) {                                    \
@@ -366,8 +411,13 @@ inline void fold_weights(const FastPlan& plan, const Params& p, const double* co
 inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
                         const int* nbr, const double* W, const int* fail, cudaStream_t s) {
     const int blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
-#define PD_LAUNCH(ID, CFG) \
-    if (plan.id == ID) k_fast<CFG><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);
+#define PD_LAUNCH(ID, CFG)                                                                                  \
+    if (plan.id == ID) {                                                                                     \
+        if (plan.variant == 1)                                                                               \
+            k_fast<CFG, 1><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail); \
+        else                                                                                                 \
+            k_fast<CFG, 0><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail); \
+    }
     PD_FAST_CONFIGS(PD_LAUNCH)
 #undef PD_LAUNCH
 }

@@ -615,3 +615,108 @@ pd_status pd_restrict_batch(pd_engine* e, int32_t n, const double* u, double* av
 }
 
 } // extern "C"
+
+// ---------------------------------------------------------------------------
+// Measurement hooks
+// ---------------------------------------------------------------------------
+namespace {
+// 8 independent DFMA chains per thread, register resident; the result is
+// stored only if it is impossible (keeps the chains alive without traffic).
+// Block 0 / thread 0 also records clock64 and %globaltimer around its loop so
+// the host can report the SM clock the chip sustained under this FP64 load.
+__device__ inline unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void k_fp64_peak(double* sink, long long* clk, int iters, double a, double b) {
+    const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
+    long long c0 = 0;
+    unsigned long long g0 = 0;
+    if (rec) {
+        c0 = clock64();
+        g0 = globaltimer_ns();
+    }
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-3, x2 = x0 + 2e-3, x3 = x0 + 3e-3;
+    double x4 = x0 + 4e-3, x5 = x0 + 5e-3, x6 = x0 + 6e-3, x7 = x0 + 7e-3;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (s == 12345.678) sink[blockIdx.x] = s;
+    if (rec) {
+        clk[0] = clock64() - c0;
+        clk[1] = (long long)(globaltimer_ns() - g0);
+    }
+}
+} // namespace
+
+extern "C" {
+
+int32_t pd_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+pd_status pd_bench_step_kernel(pd_engine* e, const double* in_dev, double* out_dev, int32_t reps, double* ms) {
+    if (!e || !in_dev || !out_dev || reps < 1 || !ms) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        const int mode = e->prm.k == 0 ? OUT_PROJECTIVE : OUT_FIELD;
+        e->launch_step(in_dev, out_dev, mode, nullptr, nullptr); // warm
+        CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
+        for (int r = 0; r < reps; ++r) e->launch_step(in_dev, out_dev, mode, nullptr, nullptr);
+        CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
+        CUDA_TRY(cudaEventSynchronize(e->ev1));
+        float t = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&t, e->ev0, e->ev1));
+        *ms = (double)t / reps;
+    });
+}
+
+pd_status pd_bench_fp64_peak(double ms_target, double* tflops, double* ghz) {
+    try {
+        int dev = 0, sms = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int threads = 512, blocks = sms * 4;
+        DevBuf<double> sink;
+        sink.alloc(blocks);
+        DevBuf<long long> clk;
+        clk.alloc(2);
+        cudaEvent_t a, b;
+        CUDA_TRY(cudaEventCreate(&a));
+        CUDA_TRY(cudaEventCreate(&b));
+        int iters = 256;
+        float t = 0.f;
+        for (int round = 0; round < 12; ++round) {
+            CUDA_TRY(cudaEventRecord(a));
+            k_fp64_peak<<<blocks, threads>>>(sink.p, clk.p, iters, 0.9999999999, 1e-12);
+            CUDA_TRY(cudaEventRecord(b));
+            CUDA_TRY(cudaEventSynchronize(b));
+            CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+            if (t >= ms_target) break;
+            iters = (int)std::min<double>(iters * std::max(2.0, ms_target / std::max(t, 1e-3f)), 1 << 26);
+        }
+        const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+        if (tflops) *tflops = flops / (t * 1e-3) / 1e12;
+        long long hc[2] = {0, 1};
+        CUDA_TRY(cudaMemcpy(hc, clk.p, sizeof hc, cudaMemcpyDeviceToHost));
+        if (ghz) *ghz = hc[1] > 0 ? (double)hc[0] / (double)hc[1] : 0.0;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        return PD_OK;
+    } catch (const Status& s) {
+        pdb200::set_global_error(s.msg);
+        return s.code;
+    }
+}
+
+} // extern "C"

@@ -79,7 +79,10 @@ def lib() -> C.CDLL:
     L.pd_problem_boundary_table.argtypes = [vp, C.c_double, C.c_int32, _dp]
     L.pd_problem_exact.argtypes = [vp, C.c_double, _dp]
     L.pd_problem_stability.argtypes = [vp, _dp, _dp]
-    for name in ["pd_engine_create", "pd_engine_tables", "pd_engine_set_stream", "pd_gaptooth_step",
+    L.pd_device_count.restype = C.c_int32
+    L.pd_bench_step_kernel.argtypes = [vp, vp, vp, C.c_int32, _dp]
+    L.pd_bench_fp64_peak.argtypes = [C.c_double, _dp, _dp]
+    for name in ["pd_bench_step_kernel", "pd_bench_fp64_peak", "pd_engine_create", "pd_engine_tables", "pd_engine_set_stream", "pd_gaptooth_step",
                  "pd_projective_step", "pd_projective_step_device", "pd_run", "pd_run_device",
                  "pd_integrate_batch", "pd_lift_batch", "pd_restrict_batch", "pd_problem_create",
                  "pd_problem_resolved", "pd_problem_engine_desc", "pd_problem_initial_field",
@@ -160,6 +163,17 @@ class Problem:
         a, r = C.c_double(), C.c_double()
         _check(lib().pd_problem_stability(self.h, C.byref(a), C.byref(r)))
         return a.value, r.value
+
+
+def device_count() -> int:
+    return lib().pd_device_count()
+
+
+def fp64_peak(ms_target: float = 200.0):
+    """Measured FP64 DFMA throughput (TFLOP/s) and the SM clock it ran at (GHz)."""
+    tf, ghz = C.c_double(), C.c_double()
+    _check(lib().pd_bench_fp64_peak(ms_target, C.byref(tf), C.byref(ghz)))
+    return tf.value, ghz.value
 
 
 def index_tables(desc: EngineDesc):
@@ -254,6 +268,22 @@ class Engine:
         if st != abi.PD_MACRO_INSTABILITY or raise_on_instability:
             _check(st, self.h)
         return U, stats
+
+    # ---- device-resident entries (pointers are raw device addresses) ----
+    def projective_step_device(self, in_ptr: int, out_ptr: int, t: float = 0.0):
+        _check(lib().pd_projective_step_device(self.h, in_ptr, out_ptr, t, None, None), self.h)
+
+    def run_device(self, u_ptr: int, scratch_ptr: int, nsteps: int, t0: float = 0.0, raise_on_instability=True):
+        stats = RunStats()
+        st = lib().pd_run_device(self.h, u_ptr, scratch_ptr, nsteps, t0, None, None, C.byref(stats))
+        if st != abi.PD_MACRO_INSTABILITY or raise_on_instability:
+            _check(st, self.h)
+        return stats
+
+    def bench_step_kernel(self, in_ptr: int, out_ptr: int, reps: int = 5) -> float:
+        ms = C.c_double()
+        _check(lib().pd_bench_step_kernel(self.h, in_ptr, out_ptr, reps, C.byref(ms)), self.h)
+        return ms.value
 
     def integrate(self, u0, kinds, values=None, slopes=None, robin_w=None, t0=0.0, src_time=None):
         u0 = np.ascontiguousarray(u0, dtype=np.float64).reshape(self.P, self.n1, self.n2)
