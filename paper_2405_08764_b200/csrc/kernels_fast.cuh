@@ -20,7 +20,9 @@
 // extrapolation (cpi.cpp:67-74) in the epilogue.
 #pragma once
 
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "pd_device.cuh"
 
@@ -30,7 +32,12 @@ struct FastPlan {
     int id = -1;     // instantiation index
     int LP = 0, G = 0, S = 0, nunits = 0;
     int mixed = 0;
-    int variant = 0; // 0: difference form of the mixed term, 1: corner form
+    // 1: one-shot launch, difference form of the mixed term (default)
+    // 0: persistent warps + TMA bulk prefetch of the next weight tile
+    // 2: one-shot launch, corner form of the mixed term
+    int variant = 1;
+    int grid = 0;       // persistent grid (CTAs)
+    int smem_bytes = 0; // persistent dynamic shared memory per CTA
 };
 
 template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
@@ -95,50 +102,20 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
     }
 }
 
-// ---- the fused step -------------------------------------------------------
+// ---- per-patch body: lift, boundary fold-in, K micro-steps, restriction --
+// Everything after the weights (w, registers) and the 3x3 stencil (v) are in
+// hand; shared by the one-shot and the persistent kernels.
 template <class Cfg, int VAR>
-__global__ void __launch_bounds__(32 * kFastWarps)
-k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
-       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
+__device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg::S], const double (&v)[9], int lane,
+                                           bool valid, int patch, double (*sg)[4][Cfg::L], double* sred,
+                                           const int* __restrict__ nbr, double* __restrict__ out, int out_mode) {
     constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LP = Cfg::LP, G = Cfg::G, NPL = Cfg::NPL;
-    constexpr int N1 = Cfg::N1, N2 = Cfg::N2, L = Cfg::L;
+    constexpr int N1 = Cfg::N1, N2 = Cfg::N2;
     constexpr bool MIXED = Cfg::MIXED;
-    __shared__ double s_g[kFastWarps][G][4][L]; // ghost offsets per edge
-    __shared__ double s_red[kFastWarps][32];
-    if (fail_flag && *fail_flag) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int unit = blockIdx.x * kFastWarps + warp;
-    if (unit >= nunits) return; // warp-uniform
     const int g = lane / LP, r = lane % LP;
     const int bi = r % LI, bj = r / LI;
-    const int patch = unit * G + g;
-    const bool valid = g < G && patch < p.P;
     const int gs = g < G ? g : 0;
-    // Neighbour blocks are at lane +-1 (xi) and lane +-LI (eta).  The exchange
-    // uses constant-delta shuffles (SHFL.DOWN/UP with an immediate), which
-    // overlap with DFMA issue on B200, unlike SHFL.IDX with a register lane
-    // (measured: scripts/ubench/ubench2.cu, DESIGN.md section 4).  A lane on a
-    // patch edge receives some other finite value for the missing side; the
-    // boundary fold-in below has zeroed every weight that would read it.
-
-    // ---- weights: S coalesced 16-byte loads per lane -------------------
-    double w[2 * Cfg::S];
-    {
-        const double2* wp = reinterpret_cast<const double2*>(Wt) + (size_t)unit * Cfg::S * 32 + lane;
-#pragma unroll
-        for (int s = 0; s < Cfg::S; ++s) {
-            const double2 t = __ldg(wp + s * 32);
-            w[2 * s] = t.x;
-            w[2 * s + 1] = t.y;
-        }
-    }
 #define WT(k, ii, jj) w[(k) * NPL + (ii) * BJ + (jj)]
-
-    // ---- 3x3 stencil gather (neighbour table) --------------------------
-    double v[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + __ldg(nbr + 9 * patch + q)) : 0.0;
-
     // centre derivatives (StencilPoly::center, gaptooth.cpp:63-72)
     const double Dxi = p.Dxi, Deta = p.Deta;
     const double Uxi = (v[7] - v[1]) / (2.0 * Dxi);
@@ -167,7 +144,7 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
                 const double G2 = dp0 * v[2] + dp1 * v[5] + dp2 * v[8];
                 const double slope = q0 * G0 + q1 * G1 + q2 * G2;
                 gv = (east ? 2.0 : -2.0) * p.mdxi * slope;
-                s_g[warp][gs][east ? PD_EDGE_E : PD_EDGE_W][j] = gv;
+                sg[gs][east ? PD_EDGE_E : PD_EDGE_W][j] = gv;
             } else {
                 const int u = t - 2 * N2;
                 const bool north = u < N1;
@@ -181,15 +158,15 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
                 const double H2 = dq0 * v[6] + dq1 * v[7] + dq2 * v[8];
                 const double slope = p0 * H0 + p1 * H1 + p2 * H2;
                 gv = (north ? 2.0 : -2.0) * p.mdeta * slope;
-                s_g[warp][gs][north ? PD_EDGE_N : PD_EDGE_S][i] = gv;
+                sg[gs][north ? PD_EDGE_N : PD_EDGE_S][i] = gv;
             }
         }
     }
     __syncwarp();
-    const double* gE = s_g[warp][gs][PD_EDGE_E];
-    const double* gW = s_g[warp][gs][PD_EDGE_W];
-    const double* gN = s_g[warp][gs][PD_EDGE_N];
-    const double* gS = s_g[warp][gs][PD_EDGE_S];
+    const double* gE = sg[gs][PD_EDGE_E];
+    const double* gW = sg[gs][PD_EDGE_W];
+    const double* gN = sg[gs][PD_EDGE_N];
+    const double* gS = sg[gs][PD_EDGE_S];
 
     // ---- lift + boundary fold-in ------------------------------------------
     double u[BI][BJ], c[BI][BJ];
@@ -231,6 +208,12 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
     }
 
     // ---- K fused micro-steps, state and weights in registers --------------
+    // Neighbour blocks are at lane +-1 (xi) and lane +-LI (eta).  The exchange
+    // uses constant-delta shuffles (SHFL.DOWN/UP with an immediate), which
+    // overlap with DFMA issue on B200, unlike SHFL.IDX with a register lane
+    // (measured: scripts/ubench/ubench2.cu, DESIGN.md section 4).  A lane on a
+    // patch edge receives some other finite value for the missing side; the
+    // boundary fold-in above has zeroed every weight that would read it.
     for (int step = 0; step < p.nt; ++step) {
         double hN[BI], hS[BI];
 #pragma unroll
@@ -322,7 +305,6 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) u[ii][jj] = nu[ii][jj];
     }
-#undef WT
 
     // ---- trapezoid restriction (gaptooth.cpp:170-194) ----------------------
     double part = 0.0;
@@ -340,12 +322,12 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
             part += ((i == 0 || i == N1 - 1) ? 0.5 * ox : ox) * row;
         }
     }
-    s_red[warp][lane] = part;
+    sred[lane] = part;
     __syncwarp();
     if (valid && r == 0) {
         double avg = 0.0;
 #pragma unroll
-        for (int q = 0; q < LP; ++q) avg += s_red[warp][g * LP + q];
+        for (int q = 0; q < LP; ++q) avg += sred[g * LP + q];
         const size_t node = (size_t)__ldg(nbr + 9 * patch + 4);
         if (out_mode == 0) {
             out[node] = avg;
@@ -355,6 +337,146 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
         } else {
             out[patch] = avg;
         }
+    }
+#undef WT
+}
+
+// ---- the fused step, one warp-unit per launch slot -----------------------
+template <class Cfg, int VAR>
+__global__ void __launch_bounds__(32 * kFastWarps)
+k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
+       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
+    constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
+    __shared__ double s_g[kFastWarps][G][4][L]; // ghost offsets per edge
+    __shared__ double s_red[kFastWarps][32];
+    if (fail_flag && *fail_flag) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int unit = blockIdx.x * kFastWarps + warp;
+    if (unit >= nunits) return; // warp-uniform
+    const int g = lane / LP;
+    const int patch = unit * G + g;
+    const bool valid = g < G && patch < p.P;
+    double w[2 * Cfg::S];
+    {
+        const double2* wp = reinterpret_cast<const double2*>(Wt) + (size_t)unit * Cfg::S * 32 + lane;
+#pragma unroll
+        for (int s = 0; s < Cfg::S; ++s) {
+            const double2 t = __ldg(wp + s * 32);
+            w[2 * s] = t.x;
+            w[2 * s + 1] = t.y;
+        }
+    }
+    double v[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + __ldg(nbr + 9 * patch + q)) : 0.0;
+    patch_body<Cfg, VAR>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, out_mode);
+}
+
+// ---- async-copy helpers (TMA bulk copy + mbarrier, cp.async) -------------
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    uint64_t state;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+                 : "=l"(state)
+                 : "r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    (void)state;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred done;\n"
+        "PD_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "@!done bra PD_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared bulk copy (TMA engine, UBLKCP), completion counted on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// order this thread's generic-proxy shared accesses before later async-proxy writes
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <class Cfg>
+struct PersistLayout {
+    static constexpr int WB = Cfg::S * 32 * 16;                // weight tile bytes per unit
+    static constexpr int NB = ((Cfg::G * 48 + 127) / 128) * 128; // neighbour rows (12 ints per patch)
+    static constexpr int GB = Cfg::G * 4 * Cfg::L * 8;          // ghost offsets
+    static constexpr int RB = 32 * 8;                          // restriction partials
+    static constexpr int WARP_BYTES = ((WB + NB + GB + RB + 16 + 127) / 128) * 128;
+    static constexpr int CTA_BYTES = WARP_BYTES * kFastWarps;
+};
+
+// ---- the fused step, persistent warps with a bulk-async weight prefetch ----
+// Each warp walks units u, u + stride, ...; while it integrates unit u the
+// TMA engine streams unit u+stride's weight tile (S*32*16 bytes, contiguous)
+// and neighbour rows into this warp's shared-memory slot, so the HBM stream of
+// coefficients overlaps the FP64 work instead of stalling each patch start.
+template <class Cfg, int VAR>
+__global__ void __launch_bounds__(32 * kFastWarps, 3)
+k_fast_p(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
+         const int* __restrict__ nbr, const int* __restrict__ nbr12, const double* __restrict__ Wt, int nunits,
+         const int* __restrict__ fail_flag) {
+    using Lay = PersistLayout<Cfg>;
+    constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L, S = Cfg::S;
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (fail_flag && *fail_flag) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* base = smem + warp * Lay::WARP_BYTES;
+    const double2* wbuf = reinterpret_cast<const double2*>(base);
+    int* nbuf = reinterpret_cast<int*>(base + Lay::WB);
+    double(*sg)[4][L] = reinterpret_cast<double(*)[4][L]>(base + Lay::WB + Lay::NB);
+    double* sred = reinterpret_cast<double*>(base + Lay::WB + Lay::NB + Lay::GB);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + Lay::WB + Lay::NB + Lay::GB + Lay::RB);
+    const int stride = gridDim.x * kFastWarps;
+    int unit = blockIdx.x * kFastWarps + warp;
+    if (unit >= nunits) return; // warp-uniform
+    const int g = lane / LP, r = lane % LP;
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int u) {
+        if (lane == 0) {
+            mbar_expect_tx(bar, Lay::WB + G * 48);
+            bulk_g2s(base, Wt + (size_t)u * S * 64, Lay::WB, bar);
+            bulk_g2s(nbuf, nbr12 + (size_t)u * G * 12, G * 48, bar);
+        }
+    };
+    issue(unit);
+    uint32_t phase = 0;
+    for (; unit < nunits; unit += stride) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        const int patch = unit * G + g;
+        const bool valid = g < G && patch < p.P;
+        double v[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + nbuf[(g < G ? g : 0) * 12 + q]) : 0.0;
+        double w[2 * S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const double2 t = wbuf[s * 32 + lane];
+            w[2 * s] = t.x;
+            w[2 * s + 1] = t.y;
+        }
+        __syncwarp();
+        fence_proxy_async();
+        if (unit + stride < nunits) issue(unit + stride);
+        (void)r;
+        patch_body<Cfg, VAR>(p, w, v, lane, valid, patch, sg, sred, nbr, out, out_mode);
     }
 }
 
@@ -408,15 +530,43 @@ inline void fold_weights(const FastPlan& plan, const Params& p, const double* co
 #undef PD_FOLD
 }
 
+// Neighbour rows padded to 12 ints per patch, grouped by unit (bulk-copyable).
+inline std::vector<int> fast_nbr12(const FastPlan& plan, int P, const int* nbr9) {
+    std::vector<int> t((size_t)plan.nunits * plan.G * 12, 0);
+    for (int q = 0; q < P; ++q)
+        for (int k = 0; k < 9; ++k) t[(size_t)q * 12 + k] = nbr9[(size_t)q * 9 + k];
+    return t;
+}
+
+// Persistent grid: exactly the resident capacity (occupancy API) or fewer.
+inline void setup_persistent(FastPlan& plan) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define PD_OCC(ID, CFG)                                                                                           \
+    if (plan.id == ID) {                                                                                           \
+        plan.smem_bytes = PersistLayout<CFG>::CTA_BYTES;                                                           \
+        cudaFuncSetAttribute(k_fast_p<CFG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);      \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fast_p<CFG, 0>, 32 * kFastWarps, plan.smem_bytes); \
+    }
+    PD_FAST_CONFIGS(PD_OCC)
+#undef PD_OCC
+    const int units_blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
+    plan.grid = std::max(1, std::min(units_blocks, sms * std::max(per_sm, 1)));
+}
+
 inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
-                        const int* nbr, const double* W, const int* fail, cudaStream_t s) {
+                        const int* nbr, const int* nbr12, const double* W, const int* fail, cudaStream_t s) {
     const int blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
-#define PD_LAUNCH(ID, CFG)                                                                                  \
-    if (plan.id == ID) {                                                                                     \
-        if (plan.variant == 1)                                                                               \
-            k_fast<CFG, 1><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail); \
-        else                                                                                                 \
-            k_fast<CFG, 0><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail); \
+#define PD_LAUNCH(ID, CFG)                                                                                           \
+    if (plan.id == ID) {                                                                                              \
+        if (plan.variant == 2)                                                                                        \
+            k_fast<CFG, 1><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);        \
+        else if (plan.variant == 1)                                                                                   \
+            k_fast<CFG, 0><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);        \
+        else                                                                                                          \
+            k_fast_p<CFG, 0><<<plan.grid, 32 * kFastWarps, plan.smem_bytes, s>>>(p, F, out, out_mode, nbr, nbr12, W, \
+                                                                                 plan.nunits, fail);                 \
     }
     PD_FAST_CONFIGS(PD_LAUNCH)
 #undef PD_LAUNCH
