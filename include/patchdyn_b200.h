@@ -269,6 +269,11 @@ pd_status pd_problem_initial_field(const pd_problem* p, double* U_host);
 pd_status pd_problem_boundary(const pd_problem* p, double t, double* perimeter_host);
 /* Boundary table for pd_run: [nsteps][k+2][perimeter] from t0. */
 pd_status pd_problem_boundary_table(const pd_problem* p, double t0, int32_t nsteps, double* out_host);
+/* Separable-source time factors time(t)/l (microsim.cpp:272-277) for pd_run:
+ * [nsteps][k+1][nt], macro step n from t0 + n*dt, substep m from
+ * t_n + m*tau (cpi.cpp:65), micro step s at t_m + s*dt_micro
+ * (microsim.cpp:536-537).  PD_UNSUPPORTED when the source is zero. */
+pd_status pd_problem_source_time(const pd_problem* p, double t0, int32_t nsteps, double* out_host);
 /* Exact solution on the macro grid at t; PD_UNSUPPORTED if none. */
 pd_status pd_problem_exact(const pd_problem* p, double t, double* U_host);
 /* max |A|+|C| over all sampled nodes (the dt pin's denominator) and the

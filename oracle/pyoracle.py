@@ -153,6 +153,7 @@ class Reference:
         L.ref_steps.argtypes = [vp, _dp, C.c_int, C.c_int, _dp]
         L.ref_sample_coeffs.argtypes = [vp, C.c_int, _ip, _dp]
         L.ref_neighbours.argtypes = [vp, C.c_int, _ip, _ip]
+        L.ref_sample_coeffs_desc.argtypes = [pd, C.c_int, _ip, _dp]
         L.ref_integrate.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                     C.c_double, C.c_double, C.c_double, _ip, _dp, _dp, _dp, C.c_double,
                                     _dp, _dp]
@@ -163,6 +164,16 @@ class Reference:
 
     def error(self) -> str:
         return self.lib.ref_last_error().decode()
+
+    def sample_coeffs(self, pdesc: ProblemDesc, patch_ij):
+        """Reference transform_coefficients at PatchIntegrator node coordinates
+        without constructing a GapToothEngine (works for b != 0)."""
+        pij = np.ascontiguousarray(patch_ij, dtype=np.int32).reshape(-1, 2)
+        out = np.empty((len(pij), 6, pdesc.nx + 1, pdesc.ny + 1))
+        r = self.lib.ref_sample_coeffs_desc(C.byref(pdesc), len(pij), _i(pij), _d(out))
+        if r:
+            raise RuntimeError(f"reference sample_coeffs_desc: {r}: {self.error()}")
+        return out
 
     def engine(self, pdesc: ProblemDesc) -> "RefEngine":
         return RefEngine(self, pdesc)

@@ -192,6 +192,46 @@ int ref_sample_coeffs(void* h, int npatch, const int* patch_ij, double* out) {
     }
 }
 
+// Same sampling without a GapToothEngine (whose constructor rejects b != 0):
+// the problem spec from refshim::build, CoarseGrid::xi/eta and PatchIntegrator
+// node coordinates, geometry::transform_coefficients.  Used for config 4/5.
+int ref_sample_coeffs_desc(const pd_problem_desc* d, int npatch, const int* patch_ij, double* out) {
+    try {
+        const refshim::Built b = refshim::build(*d);
+        gaptooth::CoarseGrid g{b.spec.a, b.spec.b, b.spec.c, b.spec.d, d->N_xi, d->N_eta};
+        const microsim::MicroGrid mg = microsim::make_micro_grid(d->h_xi, d->h_eta, d->tau, d->nx, d->ny, d->nt);
+        const double l = b.spec.physical.l;
+        const int n1 = mg.nx + 1, n2 = mg.ny + 1;
+        microsim::CoeffSampler zero = [](double, double, double) {
+            geometry::TransformedCoefficients tc{};
+            tc.a = -1.0;
+            tc.c = -1.0;
+            return tc;
+        };
+        for (int p = 0; p < npatch; ++p) {
+            const microsim::PatchIntegrator pi(g.xi(patch_ij[2 * p]), g.eta(patch_ij[2 * p + 1]), mg, l, zero, true,
+                                               microsim::SourceSpec{}, microsim::PatchIntegrator::Scheme::ADI);
+            double* o = out + static_cast<size_t>(p) * 6 * n1 * n2;
+            const size_t N = static_cast<size_t>(n1) * n2;
+            for (int i = 0; i < n1; ++i)
+                for (int j = 0; j < n2; ++j) {
+                    const auto tc = geometry::transform_coefficients(b.spec.mapping, b.spec.physical, pi.node_xi(i),
+                                                                     pi.node_eta(j), 0.0);
+                    const size_t k = static_cast<size_t>(i) * n2 + j;
+                    o[0 * N + k] = -tc.a / l;
+                    o[1 * N + k] = std::abs(tc.b) > 1e-12 ? -tc.b / l : 0.0;
+                    o[2 * N + k] = -tc.c / l;
+                    o[3 * N + k] = tc.d / l;
+                    o[4 * N + k] = tc.e / l;
+                    o[5 * N + k] = tc.f / l;
+                }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exception(e);
+    }
+}
+
 // Neighbour indices through the reference's build_stencil (gaptooth.cpp:74-104):
 // the field holds each node's flat index, so the gathered values ARE the indices.
 int ref_neighbours(void* h, int npatch, const int* patch_ij, int* out) {

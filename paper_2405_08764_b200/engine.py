@@ -78,6 +78,8 @@ def lib() -> C.CDLL:
     L.pd_problem_boundary.argtypes = [vp, C.c_double, _dp]
     L.pd_problem_boundary_table.argtypes = [vp, C.c_double, C.c_int32, _dp]
     L.pd_problem_exact.argtypes = [vp, C.c_double, _dp]
+    L.pd_problem_source_time.argtypes = [vp, C.c_double, C.c_int32, _dp]
+    L.pd_problem_source_time.restype = C.c_int32
     L.pd_problem_stability.argtypes = [vp, _dp, _dp]
     L.pd_device_count.restype = C.c_int32
     L.pd_bench_step_kernel.argtypes = [vp, vp, vp, C.c_int32, _dp]
@@ -150,6 +152,16 @@ class Problem:
         b = np.empty((nsteps, k + 2, perimeter_len(*[s - 1 for s in self.shape])))
         _check(lib().pd_problem_boundary_table(self.h, t0, nsteps, _d(b)))
         return b
+
+    def source_time(self, t0, nsteps):
+        """[nsteps][k+1][nt] separable-source factors time(t)/l, or None (zero source)."""
+        k, nt = self.desc.k, self.desc.nt
+        out = np.empty((nsteps, k + 1, nt))
+        st = lib().pd_problem_source_time(self.h, t0, nsteps, _d(out))
+        if st == abi.PD_UNSUPPORTED:
+            return None
+        _check(st)
+        return out
 
     def exact(self, t):
         U = np.empty(self.shape)
