@@ -185,10 +185,10 @@ def test_separable_source_time_factors():
     d.N_xi = d.N_eta = 10
     d.Nt = 1001
     d.nx = d.ny = 10
-    d.nt = 250  # explicit micro-solver: 0.4 on the reference's guard (ADI is the reference default here)
+    d.nt = 500  # explicit micro-solver: 0.2 on the reference's guard (ADI is the reference default here)
     P = Problem(d)
     st = P.source_time(0.0, 2)
     dt, tau = P.desc.T / P.desc.Nt, P.desc.tau
-    assert st.shape == (2, 1, 250)
-    assert st[1, 0, 125] == pytest.approx(np.exp(dt + tau / 2), rel=1e-15)
+    assert st.shape == (2, 1, 500)
+    assert st[1, 0, 250] == pytest.approx(np.exp(dt + tau / 2), rel=1e-15)
     assert Problem(configs.load("c1_diffusion")[0]).source_time(0.0, 1) is None
