@@ -1,0 +1,299 @@
+// Drop-in C++ operator interface over the B200 C-ABI.
+//
+// Same names and call shapes as the reference's gap-tooth / CPI layer so a
+// reference user switches namespaces (patchdyn:: -> pdb200::):
+//   GapToothEngine(problem, cfg)         proj/include/patchdyn/gaptooth.hpp:85
+//   initial_field / refresh_boundary     gaptooth.hpp:87-88 (gaptooth.cpp:284-310)
+//   step / step_direct                   gaptooth.hpp:91,100 (gaptooth.cpp:360-375)
+//   cpi::projective_step                 proj/include/patchdyn/cpi.hpp:19-20 (cpi.cpp:58-77)
+//   cpi::run                             cpi.hpp:45 (cpi.cpp:134-216)
+// Mesh/metric setup stays on the host (build_tables samples
+// transform_coefficients exactly like PatchIntegrator::sample_coeffs); the
+// per-patch micro-solve, lifting, restriction and the projective axpy run in
+// the sm_100a kernels behind pd_engine_* (include/patchdyn_b200.h).
+// Errors surface as the reference's exception types (pdb200::Error family).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <memory>
+#include <sstream>
+#include <utility>
+#include <vector>
+
+#include "patchdyn_b200.h"
+#include "problems.hpp"
+
+namespace pdb200 {
+
+inline void throw_status(int st, const pd_engine* e) {
+    if (st == PD_OK) return;
+    const std::string m = pd_last_error(e);
+    switch (st) {
+        case PD_NON_POSITIVE_JACOBIAN: throw NonPositiveJacobian(m);
+        case PD_MIXED_TERM_UNSUPPORTED: throw MixedTermUnsupported(m);
+        case PD_STABILITY_VIOLATION: throw StabilityViolation(m);
+        case PD_INDEX_OUT_OF_RANGE: throw IndexOutOfRange(m);
+        case PD_SHAPE_MISMATCH: throw ShapeMismatch(m);
+        case PD_MACRO_INSTABILITY: throw MacroInstability(m);
+        case PD_MACRO_PATCH_ERROR: throw MacroPatchError(m);
+        case PD_VALIDATION_ERROR: throw ValidationError(m);
+        case PD_UNSUPPORTED: throw Unsupported(m);
+        default: throw DeviceError(m);
+    }
+}
+
+namespace gaptooth {
+
+enum class SidePolicy { DirichletFromProblem, Periodic };
+
+struct CoarseGrid {
+    double a = 0, b = 1, c = 0, d = 1;
+    int Nxi = 1, Neta = 1;
+    double dxi() const { return (b - a) / Nxi; }
+    double deta() const { return (d - c) / Neta; }
+    double xi(int i) const { return a + dxi() * i; }
+    double eta(int j) const { return c + deta() * j; }
+};
+
+struct CoarseField {
+    CoarseGrid grid;
+    bool periodic = false;
+    Field2D U;
+    bool periodic_xi() const { return periodic; }
+    double& at(int i, int j) { return U(i, j); }
+    double at(int i, int j) const { return U(i, j); }
+};
+
+class GapToothEngine {
+public:
+    GapToothEngine(const problems::ProblemSpec& problem, const cpi::SchemeConfig& cfg, int host_threads = 0)
+        : problem_(problem), cfg_(cfg) {
+        cfg_.validate(problem.b - problem.a, problem.d - problem.c);
+        if (!problem.periodic_xi && (!problem.bcW || !problem.bcE))
+            throw ValidationError("problem lacks W/E boundary functions");
+        if (!problem.bcS || !problem.bcN) throw ValidationError("problem lacks S/N boundary functions");
+        grid_ = CoarseGrid{problem.a, problem.b, problem.c, problem.d, cfg.N_xi, cfg.N_eta};
+        tables_ = build_tables(problem_, cfg_, host_threads);
+        check_stability(tables_, cfg_);
+        pd_engine* e = nullptr;
+        throw_status(pd_engine_create(&tables_.desc, &e), nullptr);
+        eng_.reset(e);
+    }
+
+    CoarseField initial_field() const {
+        CoarseField F{grid_, problem_.periodic_xi, Field2D(grid_.Nxi + 1, grid_.Neta + 1)};
+        for (int i = 0; i <= grid_.Nxi; ++i)
+            for (int j = 0; j <= grid_.Neta; ++j) F.U(i, j) = problem_.initial(grid_.xi(i), grid_.eta(j));
+        if (problem_.periodic_xi)
+            for (int j = 0; j <= grid_.Neta; ++j) F.U(grid_.Nxi, j) = F.U(0, j);
+        return F;
+    }
+
+    // refresh_boundary  gaptooth.cpp:296-310
+    void refresh_boundary(CoarseField& F, double t) const {
+        const int N1 = grid_.Nxi, N2 = grid_.Neta;
+        for (int i = 0; i <= N1; ++i) {
+            F.U(i, 0) = problem_.bcS(grid_.xi(i), t);
+            F.U(i, N2) = problem_.bcN(grid_.xi(i), t);
+        }
+        if (problem_.periodic_xi) {
+            for (int j = 0; j <= N2; ++j) F.U(N1, j) = F.U(0, j);
+        } else {
+            for (int j = 0; j <= N2; ++j) {
+                F.U(0, j) = problem_.bcW(grid_.eta(j), t);
+                F.U(N1, j) = problem_.bcE(grid_.eta(j), t);
+            }
+        }
+    }
+
+    // One gap-tooth step t -> t+tau (the direct path; there is no cached
+    // linear-response shortcut on the device, so step == step_direct).
+    CoarseField step(const CoarseField& F, double t) const { return step_direct(F, t); }
+
+    CoarseField step_direct(const CoarseField& F, double t) const {
+        CoarseField out{grid_, F.periodic, Field2D(F.U.n1(), F.U.n2())};
+        const std::vector<double> bnd = perimeter(t + cfg_.tau);
+        const std::vector<double> src = source_factors(t, 0);
+        throw_status(pd_gaptooth_step(eng_.get(), F.U.data(), out.U.data(), t, bnd.data(),
+                                      src.empty() ? nullptr : src.data()),
+                     eng_.get());
+        return out;
+    }
+
+    const CoarseGrid& grid() const { return grid_; }
+    const cpi::SchemeConfig& config() const { return cfg_; }
+    const problems::ProblemSpec& problem() const { return problem_; }
+    pd_engine* device() const { return eng_.get(); }
+    int kernel_family() const { return pd_engine_mode(eng_.get()); }
+
+    // refresh values at t in the pd_perimeter layout
+    std::vector<double> perimeter(double t) const {
+        const int N1 = grid_.Nxi, N2 = grid_.Neta;
+        std::vector<double> b(pd_perimeter_len(N1, N2), 0.0);
+        for (int i = 0; i <= N1; ++i) {
+            b[i] = problem_.bcS(grid_.xi(i), t);
+            b[N1 + 1 + i] = problem_.bcN(grid_.xi(i), t);
+        }
+        if (!problem_.periodic_xi)
+            for (int j = 0; j <= N2; ++j) {
+                b[2 * (N1 + 1) + j] = problem_.bcW(grid_.eta(j), t);
+                b[2 * (N1 + 1) + N2 + 1 + j] = problem_.bcE(grid_.eta(j), t);
+            }
+        return b;
+    }
+
+    // separable source factors time(t')/l for k+1 substeps starting at t (microsim.cpp:272-277)
+    std::vector<double> source_factors(double t, int k) const {
+        if (problem_.source_zero) return {};
+        const double mdt = cfg_.tau / cfg_.nt;
+        std::vector<double> f(static_cast<size_t>(k + 1) * cfg_.nt);
+        for (int m = 0; m <= k; ++m)
+            for (int s = 0; s < cfg_.nt; ++s)
+                f[static_cast<size_t>(m) * cfg_.nt + s] = problem_.source_time((t + m * cfg_.tau) + s * mdt) / problem_.physical.l;
+        return f;
+    }
+
+private:
+    struct EngineDeleter {
+        void operator()(pd_engine* e) const { pd_engine_destroy(e); }
+    };
+    problems::ProblemSpec problem_;
+    cpi::SchemeConfig cfg_;
+    CoarseGrid grid_;
+    EngineTables tables_;
+    std::unique_ptr<pd_engine, EngineDeleter> eng_;
+};
+
+} // namespace gaptooth
+
+namespace cpi {
+
+// projective_step  cpi.cpp:58-77: k+1 fused substeps + extrapolation + refresh
+inline gaptooth::CoarseField projective_step(const gaptooth::GapToothEngine& engine, const gaptooth::CoarseField& U,
+                                             double t) {
+    const SchemeConfig& cfg = engine.config();
+    std::vector<double> bnd;
+    for (int m = 0; m <= cfg.k; ++m) {
+        const std::vector<double> b = engine.perimeter((t + m * cfg.tau) + cfg.tau);
+        bnd.insert(bnd.end(), b.begin(), b.end());
+    }
+    const std::vector<double> last = engine.perimeter(t + cfg.dt());
+    bnd.insert(bnd.end(), last.begin(), last.end());
+    const std::vector<double> src = engine.source_factors(t, cfg.k);
+    gaptooth::CoarseField out{U.grid, U.periodic, Field2D(U.U.n1(), U.U.n2())};
+    throw_status(pd_projective_step(engine.device(), U.U.data(), out.U.data(), t, bnd.data(),
+                                    src.empty() ? nullptr : src.data()),
+                 engine.device());
+    return out;
+}
+
+struct RunOptions {
+    std::vector<double> snapshot_times;
+    std::vector<std::pair<int, int>> probe_nodes;
+    int progress_every = 0;
+    std::function<void(int, double, double)> progress;
+};
+struct Snapshot {
+    double t = 0.0;
+    std::vector<double> U;
+};
+struct ProbeSeries {
+    int i = 0, j = 0;
+    std::vector<double> values;
+};
+struct RunResult {
+    std::vector<double> times;
+    std::vector<double> step_max_pct_err;
+    double max_pct_err = 0.0;
+    std::vector<Snapshot> snapshots;
+    std::vector<ProbeSeries> probes;
+    gaptooth::CoarseField final_field;
+};
+
+// max_percent_error  cpi.cpp:79-94
+inline double max_percent_error(const gaptooth::GapToothEngine& engine, const gaptooth::CoarseField& U, double t) {
+    const auto& p = engine.problem();
+    if (!p.has_exact()) return 0.0;
+    const auto& g = engine.grid();
+    const int i_lo = U.periodic_xi() ? 0 : 1;
+    double worst = 0.0;
+    for (int i = i_lo; i <= g.Nxi - 1; ++i)
+        for (int j = 1; j <= g.Neta - 1; ++j) {
+            const double ex = p.exact(g.xi(i), g.eta(j), t);
+            if (std::abs(ex) < 1e-12) continue;
+            worst = std::max(worst, std::abs(U.at(i, j) - ex) / std::abs(ex) * 100.0);
+        }
+    return worst;
+}
+
+// cpi::run  cpi.cpp:134-216.  Without diagnostics requested, the whole macro
+// loop stays on the device (pd_run: one launch sequence, blow-up guard on the
+// device); with probes/snapshots/exact errors it runs in segments between the
+// steps that need the field on the host.
+inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& opts = {}) {
+    const SchemeConfig& cfg = engine.config();
+    const double dt = cfg.dt();
+    gaptooth::CoarseField U = engine.initial_field();
+    engine.refresh_boundary(U, 0.0);
+    RunResult res;
+    std::vector<int> snap;
+    for (double ts : opts.snapshot_times) snap.push_back(std::clamp(static_cast<int>(std::lround(ts / dt)), 0, cfg.Nt));
+    auto maybe_snapshot = [&](int n, double t) {
+        for (int& s : snap)
+            if (s == n) {
+                res.snapshots.push_back(Snapshot{t, U.U.raw()});
+                s = -1;
+                break;
+            }
+    };
+    for (auto [pi, pj] : opts.probe_nodes) res.probes.push_back(ProbeSeries{pi, pj, {}});
+    maybe_snapshot(0, 0.0);
+    const bool per_step = !opts.probe_nodes.empty() || engine.problem().has_exact() || !snap.empty() ||
+                          opts.progress_every > 0;
+    const int chunk = per_step ? 1 : cfg.Nt;
+    const int k = cfg.k;
+    const size_t L = pd_perimeter_len(cfg.N_xi, cfg.N_eta);
+    for (int n = 0; n < cfg.Nt; n += chunk) {
+        const int m = std::min(chunk, cfg.Nt - n);
+        std::vector<double> bnd, src;
+        for (int q = 0; q < m; ++q) {
+            const double t = (n + q) * dt;
+            for (int s = 0; s <= k; ++s) {
+                const auto b = engine.perimeter((t + s * cfg.tau) + cfg.tau);
+                bnd.insert(bnd.end(), b.begin(), b.end());
+            }
+            const auto b = engine.perimeter(t + dt);
+            bnd.insert(bnd.end(), b.begin(), b.end());
+            const auto f = engine.source_factors(t, k);
+            src.insert(src.end(), f.begin(), f.end());
+        }
+        (void)L;
+        pd_run_stats st{};
+        const int rc = pd_run(engine.device(), U.U.data(), m, n * dt, bnd.data(), src.empty() ? nullptr : src.data(),
+                              &st);
+        if (rc == PD_MACRO_INSTABILITY) {
+            std::ostringstream os;
+            os << pd_last_error(engine.device());
+            throw MacroInstability(os.str());
+        }
+        throw_status(rc, engine.device());
+        for (int q = 0; q < m; ++q) res.times.push_back((n + q + 1) * dt);
+        const double t1 = (n + m) * dt;
+        for (auto& ps : res.probes) ps.values.push_back(U.at(ps.i, ps.j));
+        if (engine.problem().has_exact()) {
+            const double e = max_percent_error(engine, U, t1);
+            res.step_max_pct_err.push_back(e);
+            res.max_pct_err = std::max(res.max_pct_err, e);
+        }
+        maybe_snapshot(n + m, t1);
+        if (opts.progress_every > 0 && opts.progress && (n + m) % opts.progress_every == 0)
+            opts.progress(n + m, t1, res.max_pct_err);
+    }
+    res.final_field = std::move(U);
+    return res;
+}
+
+} // namespace cpi
+} // namespace pdb200

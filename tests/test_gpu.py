@@ -294,3 +294,26 @@ def test_annulus_16x10_golden_trajectory(gpu):
         done = target
         scale = max(np.abs(gold[key]).max(), 1.0)
         assert np.abs(U - gold[key]).max() < 1e-9 * scale, key
+
+
+# ---------------------------------------------------------------------------
+# the C++ drop-in API (examples/dropin_c1.cpp: the reference's call sequence)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_cpp_dropin_runs_config1(mode, tmp_path, gpu):
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = ROOT / "build" / "bin" / "dropin_c1"
+    assert exe.exists(), "built by __graft_entry__.build() (make -C paper_2405_08764_b200/csrc)"
+    out = tmp_path / "u.bin"
+    r = subprocess.run([str(exe), mode, str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert f"kernel_family={mode}" in r.stdout and "steps=200" in r.stdout
+    U = np.fromfile(out, dtype=np.float64).reshape(20, 20)
+    if mode == "exact":
+        assert np.array_equal(U, FINALS["c1_diffusion_final"])
+        assert "max_pct_err=%.12f" % float(FINALS["c1_diffusion_maxpct"]) in r.stdout
+    else:
+        assert rel(U, FINALS["c1_diffusion_final"]) < TOL
