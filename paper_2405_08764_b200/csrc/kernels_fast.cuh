@@ -89,11 +89,16 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
             const double A = c[PD_COEF_A * p.N + k], B = c[PD_COEF_B * p.N + k], C = c[PD_COEF_C * p.N + k];
             const double Vx = c[PD_COEF_VX * p.N + k], Vy = c[PD_COEF_VY * p.N + k], Wr = c[PD_COEF_W * p.N + k];
             const double ax = A * idx2, vx = Vx * idx, cy = C * idy2, vy = Vy * idy;
+            const double wE = dt * (ax - vx), wW = dt * (ax + vx), wN = dt * (cy - vy), wS = dt * (cy + vy);
+            // Neumann reflection u_ghost = u_inner + g (microsim.cpp:314-323): the
+            // inward weight absorbs the outward one; the outward slot keeps the
+            // original weight for the per-patch ghost constant (zeroed in k_fast).
+            const bool Wb = i == 0, Eb = i == Cfg::N1 - 1, Sb = j == 0, Nb = j == Cfg::N2 - 1;
             switch (kind) {
-                case WE: val = dt * (ax - vx); break;
-                case WW: val = dt * (ax + vx); break;
-                case WN: val = dt * (cy - vy); break;
-                case WS: val = dt * (cy + vy); break;
+                case WE: val = Wb ? wE + wW : wE; break;
+                case WW: val = Eb ? wW + wE : wW; break;
+                case WN: val = Sb ? wN + wS : wN; break;
+                case WS: val = Nb ? wS + wN : wS; break;
                 case WD: val = dt * (B * ixy); break;
                 default: val = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr); break;
             }
@@ -107,7 +112,7 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
 // hand; shared by the one-shot and the persistent kernels.
 template <class Cfg, int VAR>
 __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg::S], const double (&v)[9], int lane,
-                                           bool valid, int patch, double (*sg)[4][Cfg::L], double* sred,
+                                           bool valid, int patch, double (*sg)[8][Cfg::L], double* sred,
                                            const int* __restrict__ nbr, double* __restrict__ out, int out_mode) {
     constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LP = Cfg::LP, G = Cfg::G, NPL = Cfg::NPL;
     constexpr int N1 = Cfg::N1, N2 = Cfg::N2;
@@ -116,50 +121,37 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     const int bi = r % LI, bj = r / LI;
     const int gs = g < G ? g : 0;
 #define WT(k, ii, jj) w[(k) * NPL + (ii) * BJ + (jj)]
-    // centre derivatives (StencilPoly::center, gaptooth.cpp:63-72)
-    const double Dxi = p.Dxi, Deta = p.Deta;
-    const double Uxi = (v[7] - v[1]) / (2.0 * Dxi);
-    const double Ueta = (v[5] - v[3]) / (2.0 * Deta);
-    const double Uxx = (v[7] - 2.0 * v[4] + v[1]) / (Dxi * Dxi);
-    const double Uyy = (v[5] - 2.0 * v[4] + v[3]) / (Deta * Deta);
-    const double Uxy = (v[8] - v[6] - v[2] + v[0]) / (4.0 * Dxi * Deta);
-    const double C0 = v[4] - p.h_xi * p.h_xi / 24.0 * Uxx - p.h_eta * p.h_eta / 24.0 * Uyy;
+    // centre derivatives (StencilPoly::center, gaptooth.cpp:63-72); reciprocals
+    // come precomputed from the host (no device divisions)
+    const double Uxi = (v[7] - v[1]) * p.i2Dxi;
+    const double Ueta = (v[5] - v[3]) * p.i2Deta;
+    const double hUxx = 0.5 * ((v[7] - 2.0 * v[4] + v[1]) * p.iDxi2);
+    const double hUyy = 0.5 * ((v[5] - 2.0 * v[4] + v[3]) * p.iDeta2);
+    const double Uxy = (v[8] - v[6] - v[2] + v[0]) * p.i4DD;
+    const double C0 = v[4] - p.c24x * (2.0 * hUxx) - p.c24y * (2.0 * hUyy);
 
     // ---- ghost offsets g = +-2 delta * slope along the four edges ---------
-    // slope_E(j) = sum_q Lq(Y_j)[q] * sum_p Lp'(+h/2)[p] v[p][q]  (tensor Lagrange, gaptooth.cpp:43-61)
-    {
-        const double hx = 0.5 * p.h_xi, hy = 0.5 * p.h_eta;
-        const double ix2 = 1.0 / (Dxi * Dxi), iy2 = 1.0 / (Deta * Deta);
-        for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
-            double gv;
-            if (t < 2 * N2) {
-                const bool east = t < N2;
-                const int j = east ? t : t - N2;
-                const double X = east ? hx : -hx;
-                const double dp0 = (X - 0.5 * Dxi) * ix2, dp1 = -2.0 * X * ix2, dp2 = (X + 0.5 * Dxi) * ix2;
-                const double Y = -hy + p.mdeta * j;
-                const double q0 = 0.5 * Y * (Y - Deta) * iy2, q1 = 1.0 - Y * Y * iy2, q2 = 0.5 * Y * (Y + Deta) * iy2;
-                const double G0 = dp0 * v[0] + dp1 * v[3] + dp2 * v[6];
-                const double G1 = dp0 * v[1] + dp1 * v[4] + dp2 * v[7];
-                const double G2 = dp0 * v[2] + dp1 * v[5] + dp2 * v[8];
-                const double slope = q0 * G0 + q1 * G1 + q2 * G2;
-                gv = (east ? 2.0 : -2.0) * p.mdxi * slope;
-                sg[gs][east ? PD_EDGE_E : PD_EDGE_W][j] = gv;
-            } else {
-                const int u = t - 2 * N2;
-                const bool north = u < N1;
-                const int i = north ? u : u - N1;
-                const double Y = north ? hy : -hy;
-                const double dq0 = (Y - 0.5 * Deta) * iy2, dq1 = -2.0 * Y * iy2, dq2 = (Y + 0.5 * Deta) * iy2;
-                const double X = -hx + p.mdxi * i;
-                const double p0 = 0.5 * X * (X - Dxi) * ix2, p1 = 1.0 - X * X * ix2, p2 = 0.5 * X * (X + Dxi) * ix2;
-                const double H0 = dq0 * v[0] + dq1 * v[1] + dq2 * v[2];
-                const double H1 = dq0 * v[3] + dq1 * v[4] + dq2 * v[5];
-                const double H2 = dq0 * v[6] + dq1 * v[7] + dq2 * v[8];
-                const double slope = p0 * H0 + p1 * H1 + p2 * H2;
-                gv = (north ? 2.0 : -2.0) * p.mdeta * slope;
-                sg[gs][north ? PD_EDGE_N : PD_EDGE_S][i] = gv;
-            }
+    // slope_E(j) = sum_q Lq(Y_j)[q] * sum_p Lp'(+h/2)[p] v[p][q] (tensor Lagrange,
+    // gaptooth.cpp:43-61, weights from the host).  Lanes of a patch share the
+    // 2*N1 + 2*N2 entries; then, for the mixed term, the boundary-ring offsets
+    // Doff (the reflected node values cancel in (uNE+uSW)-(uNW+uSE); what
+    // remains is a signed sum of ghost offsets, SURVEY B.4 corners).
+    for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
+        if (t < 2 * N2) {
+            const int e = t < N2 ? PD_EDGE_E : PD_EDGE_W, j = t < N2 ? t : t - N2;
+            const double* d = p.dlag[e];
+            const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
+            const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
+            const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
+            sg[gs][e][j] = p.gsc[e] * (p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2);
+        } else {
+            const int u = t - 2 * N2;
+            const int e = u < N1 ? PD_EDGE_N : PD_EDGE_S, i = u < N1 ? u : u - N1;
+            const double* d = p.dlag[e];
+            const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
+            const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
+            const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
+            sg[gs][e][i] = p.gsc[e] * (p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2);
         }
     }
     __syncwarp();
@@ -167,39 +159,60 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     const double* gW = sg[gs][PD_EDGE_W];
     const double* gN = sg[gs][PD_EDGE_N];
     const double* gS = sg[gs][PD_EDGE_S];
+    if constexpr (MIXED) {
+        auto off = [&](int pp, int qq) {
+            const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
+            const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
+            double o = 0.0;
+            if (pp < 0) o += gW[qc];
+            if (pp > N1 - 1) o += gE[qc];
+            if (qq < 0) o += gS[pc];
+            if (qq > N2 - 1) o += gN[pc];
+            return o;
+        };
+        for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
+            int e, i, j, k;
+            if (t < 2 * N2) {
+                e = t < N2 ? PD_EDGE_E : PD_EDGE_W;
+                k = j = t < N2 ? t : t - N2;
+                i = e == PD_EDGE_E ? N1 - 1 : 0;
+            } else {
+                const int u = t - 2 * N2;
+                e = u < N1 ? PD_EDGE_N : PD_EDGE_S;
+                k = i = u < N1 ? u : u - N1;
+                j = e == PD_EDGE_N ? N2 - 1 : 0;
+            }
+            sg[gs][4 + e][k] = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
+        }
+        __syncwarp();
+    }
 
     // ---- lift + boundary fold-in ------------------------------------------
+    // Static reflections (wE += wW on the W edge, ...) are folded into the
+    // table by k_fold; the outward slot still holds the original weight, used
+    // here once for the per-patch constant and then zeroed.
     double u[BI][BJ], c[BI][BJ];
 #pragma unroll
     for (int ii = 0; ii < BI; ++ii) {
+        const int i = bi * BI + ii;
+        const double X = -0.5 * p.h_xi + p.mdxi * i;
+        const double Ai = C0 + X * (Uxi + X * hUxx), Bi = Ueta + X * Uxy;
 #pragma unroll
         for (int jj = 0; jj < BJ; ++jj) {
-            const int i = bi * BI + ii, j = bj * BJ + jj;
-            const double X = -0.5 * p.h_xi + p.mdxi * i, Y = -0.5 * p.h_eta + p.mdeta * j;
-            u[ii][jj] = C0 + X * Uxi + Y * Ueta + 0.5 * X * X * Uxx + X * Y * Uxy + 0.5 * Y * Y * Uyy;
+            const int j = bj * BJ + jj;
+            const double Y = -0.5 * p.h_eta + p.mdeta * j;
+            u[ii][jj] = Ai + Y * (Bi + Y * hUyy); // quadratic lift (gaptooth.cpp:154-168)
             const bool Wb = i == 0, Eb = i == N1 - 1, Sb = j == 0, Nb = j == N2 - 1;
             double cc = 0.0;
             // single-edge reflections u_ghost = u_inner + g (microsim.cpp:314-323)
-            if (Wb) { cc += WT(WW, ii, jj) * gW[j]; WT(WE, ii, jj) += WT(WW, ii, jj); WT(WW, ii, jj) = 0.0; }
-            if (Eb) { cc += WT(WE, ii, jj) * gE[j]; WT(WW, ii, jj) += WT(WE, ii, jj); WT(WE, ii, jj) = 0.0; }
-            if (Sb) { cc += WT(WS, ii, jj) * gS[i]; WT(WN, ii, jj) += WT(WS, ii, jj); WT(WS, ii, jj) = 0.0; }
-            if (Nb) { cc += WT(WN, ii, jj) * gN[i]; WT(WS, ii, jj) += WT(WN, ii, jj); WT(WN, ii, jj) = 0.0; }
+            if (Wb) { cc = fma(WT(WW, ii, jj), gW[j], cc); WT(WW, ii, jj) = 0.0; }
+            if (Eb) { cc = fma(WT(WE, ii, jj), gE[j], cc); WT(WE, ii, jj) = 0.0; }
+            if (Sb) { cc = fma(WT(WS, ii, jj), gS[i], cc); WT(WS, ii, jj) = 0.0; }
+            if (Nb) { cc = fma(WT(WN, ii, jj), gN[i], cc); WT(WN, ii, jj) = 0.0; }
             if constexpr (MIXED) {
                 if (Wb || Eb || Sb || Nb) {
-                    // the reflected node values cancel in (uNE+uSW)-(uNW+uSE); what
-                    // remains is the signed sum of ghost offsets (SURVEY B.4 corners)
-                    auto off = [&](int pp, int qq) {
-                        const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
-                        const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
-                        double o = 0.0;
-                        if (pp < 0) o += gW[qc];
-                        if (pp > N1 - 1) o += gE[qc];
-                        if (qq < 0) o += gS[pc];
-                        if (qq > N2 - 1) o += gN[pc];
-                        return o;
-                    };
-                    const double Doff = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
-                    cc += WT(WD, ii, jj) * Doff;
+                    const double* dd = sg[gs][4 + (Wb ? PD_EDGE_W : Eb ? PD_EDGE_E : Sb ? PD_EDGE_S : PD_EDGE_N)];
+                    cc = fma(WT(WD, ii, jj), dd[(Wb || Eb) ? j : i], cc);
                     WT(WD, ii, jj) = 0.0;
                 }
             }
@@ -347,7 +360,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
 k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
        const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
     constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
-    __shared__ double s_g[kFastWarps][G][4][L]; // ghost offsets per edge
+    __shared__ double s_g[kFastWarps][G][8][L]; // ghost offsets + mixed-term ring offsets per edge
     __shared__ double s_red[kFastWarps][32];
     if (fail_flag && *fail_flag) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -412,7 +425,7 @@ template <class Cfg>
 struct PersistLayout {
     static constexpr int WB = Cfg::S * 32 * 16;                // weight tile bytes per unit
     static constexpr int NB = ((Cfg::G * 48 + 127) / 128) * 128; // neighbour rows (12 ints per patch)
-    static constexpr int GB = Cfg::G * 4 * Cfg::L * 8;          // ghost offsets
+    static constexpr int GB = Cfg::G * 8 * Cfg::L * 8;          // ghost offsets + ring offsets
     static constexpr int RB = 32 * 8;                          // restriction partials
     static constexpr int WARP_BYTES = ((WB + NB + GB + RB + 16 + 127) / 128) * 128;
     static constexpr int CTA_BYTES = WARP_BYTES * kFastWarps;
@@ -436,7 +449,7 @@ k_fast_p(Params p, const double* __restrict__ F, double* __restrict__ out, int o
     unsigned char* base = smem + warp * Lay::WARP_BYTES;
     const double2* wbuf = reinterpret_cast<const double2*>(base);
     int* nbuf = reinterpret_cast<int*>(base + Lay::WB);
-    double(*sg)[4][L] = reinterpret_cast<double(*)[4][L]>(base + Lay::WB + Lay::NB);
+    double(*sg)[8][L] = reinterpret_cast<double(*)[8][L]>(base + Lay::WB + Lay::NB);
     double* sred = reinterpret_cast<double*>(base + Lay::WB + Lay::NB + Lay::GB);
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + Lay::WB + Lay::NB + Lay::GB + Lay::RB);
     const int stride = gridDim.x * kFastWarps;

@@ -33,6 +33,13 @@ struct Params {
     int P, nsets;
     int mixed;  // any B != 0
     int source; // PD_SOURCE_*
+    // FAST-mode constants, computed once on the host (no divisions on the device)
+    double i2Dxi, i2Deta, iDxi2, iDeta2, i4DD; // 1/(2D), 1/D^2, 1/(4 Dxi Deta)
+    double c24x, c24y;                          // h^2/24 (box-average constant of the lift)
+    double dlag[4][3];   // Lagrange derivative weights at +-h/2: E, W (xi) and N, S (eta)
+    double lagq[33][3];  // Lagrange value weights at the E/W edge nodes Y_j (j < n2)
+    double lagp[33][3];  // Lagrange value weights at the N/S edge nodes X_i (i < n1)
+    double gsc[4];       // ghost scale +-2 delta per edge (microsim.cpp:166)
 };
 
 // One micro edge condition in shared memory (EdgeCondition + Ghost,

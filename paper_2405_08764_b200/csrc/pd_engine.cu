@@ -201,6 +201,34 @@ Params make_params(const pd_engine_desc& d, int P) {
     p.P = P;
     p.nsets = d.ncoeff_sets;
     p.source = d.source_kind;
+    // FAST-mode constants: degree-2 Lagrange basis on {-D,0,D} (gaptooth.cpp:17-29)
+    p.i2Dxi = 1.0 / (2.0 * p.Dxi);
+    p.i2Deta = 1.0 / (2.0 * p.Deta);
+    p.iDxi2 = 1.0 / (p.Dxi * p.Dxi);
+    p.iDeta2 = 1.0 / (p.Deta * p.Deta);
+    p.i4DD = 1.0 / (4.0 * p.Dxi * p.Deta);
+    p.c24x = d.h_xi * d.h_xi / 24.0;
+    p.c24y = d.h_eta * d.h_eta / 24.0;
+    auto lag = [](double X, double D, double* o) {
+        o[0] = 0.5 * X * (X - D) / (D * D);
+        o[1] = 1.0 - X * X / (D * D);
+        o[2] = 0.5 * X * (X + D) / (D * D);
+    };
+    auto dlag = [](double X, double D, double* o) {
+        o[0] = (X - 0.5 * D) / (D * D);
+        o[1] = -2.0 * X / (D * D);
+        o[2] = (X + 0.5 * D) / (D * D);
+    };
+    dlag(0.5 * d.h_xi, p.Dxi, p.dlag[0]);
+    dlag(-0.5 * d.h_xi, p.Dxi, p.dlag[1]);
+    dlag(0.5 * d.h_eta, p.Deta, p.dlag[2]);
+    dlag(-0.5 * d.h_eta, p.Deta, p.dlag[3]);
+    for (int j = 0; j < p.n2 && j < 33; ++j) lag(-0.5 * d.h_eta + p.mdeta * j, p.Deta, p.lagq[j]);
+    for (int i = 0; i < p.n1 && i < 33; ++i) lag(-0.5 * d.h_xi + p.mdxi * i, p.Dxi, p.lagp[i]);
+    p.gsc[PD_EDGE_E] = 2.0 * p.mdxi;
+    p.gsc[PD_EDGE_W] = -2.0 * p.mdxi;
+    p.gsc[PD_EDGE_N] = 2.0 * p.mdeta;
+    p.gsc[PD_EDGE_S] = -2.0 * p.mdeta;
     return p;
 }
 
