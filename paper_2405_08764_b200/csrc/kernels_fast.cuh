@@ -26,6 +26,10 @@
 
 #include "pd_device.cuh"
 
+#ifndef PD_STEP_UNROLL
+#define PD_STEP_UNROLL 1 // micro-step loop unroll (dev knob)
+#endif
+
 namespace pdb200::dev {
 
 struct FastPlan {
@@ -38,6 +42,9 @@ struct FastPlan {
     int variant = 1;
     int grid = 0;       // persistent grid (CTAs)
     int smem_bytes = 0; // persistent dynamic shared memory per CTA
+    int first_wave = 0; // one-shot: CTAs resident at once (occupancy x SMs)
+    int stagger_ns = 0; // one-shot: start offset per residency slot
+    int sms = 148;
 };
 
 template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
@@ -54,7 +61,8 @@ struct FastCfg {
     static_assert(LP <= 32, "patch must fit a warp");
 };
 enum { WC = 0, WE = 1, WW = 2, WN = 3, WS = 4, WD = 5 };
-constexpr int kFastWarps = 4;
+constexpr int kFastWarps = 1; // one warp per CTA: warps retire and are replaced independently
+constexpr int kStepUnroll = PD_STEP_UNROLL;
 
 // ---- fold: solver-form coefficients -> lane-interleaved weight table -------
 // Table layout: unit u (one warp = G patches) owns S*32 double2 slots; slot s
@@ -202,7 +210,10 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const int j = bj * BJ + jj;
             const double Y = -0.5 * p.h_eta + p.mdeta * j;
             u[ii][jj] = Ai + Y * (Bi + Y * hUyy); // quadratic lift (gaptooth.cpp:154-168)
-            const bool Wb = i == 0, Eb = i == N1 - 1, Sb = j == 0, Nb = j == N2 - 1;
+            // only block-edge nodes can be patch-edge nodes: written so the
+            // compiler drops the impossible cases at compile time
+            const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
+            const bool Sb = jj == 0 && bj == 0, Nb = jj == BJ - 1 && bj == Cfg::LJ - 1;
             double cc = 0.0;
             // single-edge reflections u_ghost = u_inner + g (microsim.cpp:314-323)
             if (Wb) { cc = fma(WT(WW, ii, jj), gW[j], cc); WT(WW, ii, jj) = 0.0; }
@@ -227,6 +238,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     // (measured: scripts/ubench/ubench2.cu).  A lane on a
     // patch edge receives some other finite value for the missing side; the
     // boundary fold-in above has zeroed every weight that would read it.
+#pragma unroll kStepUnroll
     for (int step = 0; step < p.nt; ++step) {
         double hN[BI], hS[BI];
 #pragma unroll
@@ -330,9 +342,11 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) {
                 const int j = bj * BJ + jj;
-                row += ((j == 0 || j == N2 - 1) ? 0.5 * oy : oy) * u[ii][jj];
+                const bool edge = (jj == 0 && bj == 0) || (jj == BJ - 1 && bj == Cfg::LJ - 1);
+                row += (edge ? 0.5 * oy : oy) * u[ii][jj];
             }
-            part += ((i == 0 || i == N1 - 1) ? 0.5 * ox : ox) * row;
+            const bool edge = (ii == 0 && bi == 0) || (ii == BI - 1 && bi == LI - 1);
+            part += (edge ? 0.5 * ox : ox) * row;
         }
     }
     sred[lane] = part;
@@ -358,7 +372,8 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 template <class Cfg, int VAR>
 __global__ void __launch_bounds__(32 * kFastWarps)
 k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
-       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
+       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag, int first_wave, int stagger_ns,
+       int sms) {
     constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
     __shared__ double s_g[kFastWarps][G][8][L]; // ghost offsets + mixed-term ring offsets per edge
     __shared__ double s_red[kFastWarps][32];
@@ -366,9 +381,20 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int unit = blockIdx.x * kFastWarps + warp;
     if (unit >= nunits) return; // warp-uniform
+    // Every patch costs the same, so without intervention the resident warps of
+    // an SM run in lock-step: all in the latency-bound prologue, then all in the
+    // FP64 loop.  Offsetting the first residency wave by slot staggers them for
+    // the whole launch (each retiring warp's successor inherits its phase), and
+    // the prologues overlap other warps' FP64 work.
+    if (stagger_ns > 0 && (int)blockIdx.x < first_wave) __nanosleep((unsigned)(((int)blockIdx.x / sms) * stagger_ns));
     const int g = lane / LP;
     const int patch = unit * G + g;
     const bool valid = g < G && patch < p.P;
+    // The stencil gather is a dependent pair (index, then value): issue the
+    // index loads first so they are not queued behind the weight tile.
+    int idx[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) idx[q] = valid ? __ldg(nbr + 9 * patch + q) : 0;
     double w[2 * Cfg::S];
     {
         const double2* wp = reinterpret_cast<const double2*>(Wt) + (size_t)unit * Cfg::S * 32 + lane;
@@ -381,7 +407,7 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
     }
     double v[9];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + __ldg(nbr + 9 * patch + q)) : 0.0;
+    for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + idx[q]) : 0.0;
     patch_body<Cfg, VAR>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, out_mode);
 }
 
@@ -427,7 +453,7 @@ struct PersistLayout {
     static constexpr int NB = ((Cfg::G * 48 + 127) / 128) * 128; // neighbour rows (12 ints per patch)
     static constexpr int GB = Cfg::G * 8 * Cfg::L * 8;          // ghost offsets + ring offsets
     static constexpr int RB = 32 * 8;                          // restriction partials
-    static constexpr int WARP_BYTES = ((WB + NB + GB + RB + 16 + 127) / 128) * 128;
+    static constexpr int WARP_BYTES = ((WB + NB + GB + RB + 32 + 127) / 128) * 128; // + mbarrier + loop state
     static constexpr int CTA_BYTES = WARP_BYTES * kFastWarps;
 };
 
@@ -452,27 +478,30 @@ k_fast_p(Params p, const double* __restrict__ F, double* __restrict__ out, int o
     double(*sg)[8][L] = reinterpret_cast<double(*)[8][L]>(base + Lay::WB + Lay::NB);
     double* sred = reinterpret_cast<double*>(base + Lay::WB + Lay::NB + Lay::GB);
     uint64_t* bar = reinterpret_cast<uint64_t*>(base + Lay::WB + Lay::NB + Lay::GB + Lay::RB);
+    // loop-carried state lives in shared memory (volatile), not in registers:
+    // the hot loop inside patch_body needs all 168 the compiler may use
+    volatile int* st = reinterpret_cast<volatile int*>(bar + 1);
     const int stride = gridDim.x * kFastWarps;
-    int unit = blockIdx.x * kFastWarps + warp;
-    if (unit >= nunits) return; // warp-uniform
-    const int g = lane / LP, r = lane % LP;
+    const int first = blockIdx.x * kFastWarps + warp;
+    if (first >= nunits) return; // warp-uniform
     if (lane == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        st[0] = first;
+        st[1] = 0;
+        mbar_expect_tx(bar, Lay::WB + G * 48);
+        bulk_g2s(base, Wt + (size_t)first * S * 64, Lay::WB, bar);
+        bulk_g2s(nbuf, nbr12 + (size_t)first * G * 12, G * 48, bar);
     }
     __syncwarp();
-    auto issue = [&](int u) {
-        if (lane == 0) {
-            mbar_expect_tx(bar, Lay::WB + G * 48);
-            bulk_g2s(base, Wt + (size_t)u * S * 64, Lay::WB, bar);
-            bulk_g2s(nbuf, nbr12 + (size_t)u * G * 12, G * 48, bar);
-        }
-    };
-    issue(unit);
-    uint32_t phase = 0;
-    for (; unit < nunits; unit += stride) {
+    while (true) {
+        const int unit = st[0];
+        if (unit >= nunits) break;
+        const uint32_t phase = static_cast<uint32_t>(st[1]);
+        int ln;
+        asm volatile("mov.u32 %0, %%laneid;" : "=r"(ln));
+        const int g = ln / LP;
         mbar_wait(bar, phase);
-        phase ^= 1;
         const int patch = unit * G + g;
         const bool valid = g < G && patch < p.P;
         double v[9];
@@ -481,15 +510,98 @@ k_fast_p(Params p, const double* __restrict__ F, double* __restrict__ out, int o
         double w[2 * S];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            const double2 t = wbuf[s * 32 + lane];
+            const double2 t = wbuf[s * 32 + ln];
             w[2 * s] = t.x;
             w[2 * s + 1] = t.y;
         }
         __syncwarp();
         fence_proxy_async();
-        if (unit + stride < nunits) issue(unit + stride);
-        (void)r;
+        if (ln == 0) {
+            const int nxt = unit + stride;
+            st[0] = nxt;
+            st[1] = static_cast<int>(phase ^ 1u);
+            if (nxt < nunits) {
+                mbar_expect_tx(bar, Lay::WB + G * 48);
+                bulk_g2s(base, Wt + (size_t)nxt * S * 64, Lay::WB, bar);
+                bulk_g2s(nbuf, nbr12 + (size_t)nxt * G * 12, G * 48, bar);
+            }
+        }
+        __syncwarp();
+        patch_body<Cfg, VAR>(p, w, v, ln, valid, patch, sg, sred, nbr, out, out_mode);
+        __syncwarp();
+    }
+}
+
+// ---- two patch groups per warp, straight-line, TMA prefetch of the second --
+// The second unit's weight tile and neighbour rows stream into this warp's
+// shared-memory slot (cp.async.bulk + mbarrier) while the first unit runs its
+// K micro-steps, halving the exposed per-unit prologue latency without the
+// loop-carried state of a persistent kernel.
+template <class Cfg, int VAR>
+__global__ void __launch_bounds__(32 * kFastWarps)
+k_fast2(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
+        const int* __restrict__ nbr12, const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
+    using Lay = PersistLayout<Cfg>;
+    constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L, S = Cfg::S;
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (fail_flag && *fail_flag) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* base = smem + warp * Lay::WARP_BYTES;
+    const double2* wbuf = reinterpret_cast<const double2*>(base);
+    int* nbuf = reinterpret_cast<int*>(base + Lay::WB);
+    double(*sg)[8][L] = reinterpret_cast<double(*)[8][L]>(base + Lay::WB + Lay::NB);
+    double* sred = reinterpret_cast<double*>(base + Lay::WB + Lay::NB + Lay::GB);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + Lay::WB + Lay::NB + Lay::GB + Lay::RB);
+    const int u0 = 2 * (blockIdx.x * kFastWarps + warp), u1 = u0 + 1;
+    if (u0 >= nunits) return; // warp-uniform
+    const bool two = u1 < nunits;
+    if (lane == 0 && two) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, Lay::WB + G * 48);
+        bulk_g2s(base, Wt + (size_t)u1 * S * 64, Lay::WB, bar);
+        bulk_g2s(nbuf, nbr12 + (size_t)u1 * G * 12, G * 48, bar);
+    }
+    const int g = lane / LP;
+    {
+        const int patch = u0 * G + g;
+        const bool valid = g < G && patch < p.P;
+        int idx[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) idx[q] = valid ? __ldg(nbr + 9 * patch + q) : 0;
+        double w[2 * S];
+        const double2* wp = reinterpret_cast<const double2*>(Wt) + (size_t)u0 * S * 32 + lane;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const double2 t = __ldg(wp + s * 32);
+            w[2 * s] = t.x;
+            w[2 * s + 1] = t.y;
+        }
+        double v[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + idx[q]) : 0.0;
         patch_body<Cfg, VAR>(p, w, v, lane, valid, patch, sg, sred, nbr, out, out_mode);
+    }
+    if (!two) return;
+    __syncwarp();
+    mbar_wait(bar, 0);
+    {
+        int ln;
+        asm volatile("mov.u32 %0, %%laneid;" : "=r"(ln));
+        const int g1 = ln / LP;
+        const int patch = u1 * G + g1;
+        const bool valid = g1 < G && patch < p.P;
+        double v[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + nbuf[(g1 < G ? g1 : 0) * 12 + q]) : 0.0;
+        double w[2 * S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const double2 t = wbuf[s * 32 + ln];
+            w[2 * s] = t.x;
+            w[2 * s + 1] = t.y;
+        }
+        patch_body<Cfg, VAR>(p, w, v, ln, valid, patch, sg, sred, nbr, out, out_mode);
     }
 }
 
@@ -560,12 +672,22 @@ inline void setup_persistent(FastPlan& plan) {
     if (plan.id == ID) {                                                                                           \
         plan.smem_bytes = PersistLayout<CFG>::CTA_BYTES;                                                           \
         cudaFuncSetAttribute(k_fast_p<CFG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);      \
+        cudaFuncSetAttribute(k_fast2<CFG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);       \
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fast_p<CFG, 0>, 32 * kFastWarps, plan.smem_bytes); \
     }
     PD_FAST_CONFIGS(PD_OCC)
 #undef PD_OCC
     const int units_blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
     plan.grid = std::max(1, std::min(units_blocks, sms * std::max(per_sm, 1)));
+    int per_sm1 = 0;
+#define PD_OCC1(ID, CFG) \
+    if (plan.id == ID) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_fast<CFG, 0>, 32 * kFastWarps, 0);
+    PD_FAST_CONFIGS(PD_OCC1)
+#undef PD_OCC1
+    plan.sms = sms;
+    plan.first_wave = sms * std::max(per_sm1, 1);
+    plan.stagger_ns = 1000;
+    if (const char* v = std::getenv("PD_STAGGER_NS")) plan.stagger_ns = std::atoi(v); // dev knob
 }
 
 inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
@@ -573,10 +695,13 @@ inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, 
     const int blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
 #define PD_LAUNCH(ID, CFG)                                                                                           \
     if (plan.id == ID) {                                                                                              \
-        if (plan.variant == 2)                                                                                        \
-            k_fast<CFG, 1><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);        \
+        if (plan.variant == 3)                                                                                        \
+            k_fast2<CFG, 0><<<(plan.nunits + 2 * kFastWarps - 1) / (2 * kFastWarps), 32 * kFastWarps,                \
+                              plan.smem_bytes, s>>>(p, F, out, out_mode, nbr, nbr12, W, plan.nunits, fail);        \
+        else if (plan.variant == 2)                                                                                   \
+            k_fast<CFG, 1><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail, plan.first_wave, plan.stagger_ns, plan.sms);        \
         else if (plan.variant == 1)                                                                                   \
-            k_fast<CFG, 0><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);        \
+            k_fast<CFG, 0><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail, plan.first_wave, plan.stagger_ns, plan.sms);        \
         else                                                                                                          \
             k_fast_p<CFG, 0><<<plan.grid, 32 * kFastWarps, plan.smem_bytes, s>>>(p, F, out, out_mode, nbr, nbr12, W, \
                                                                                  plan.nunits, fail);                 \
