@@ -45,6 +45,7 @@ struct FastPlan {
     int first_wave = 0; // one-shot: CTAs resident at once (occupancy x SMs)
     int stagger_ns = 0; // one-shot: start offset per residency slot
     int sms = 148;
+    int big = 0;        // 32x32 patches: kernels_fast_big.cuh (one CTA of 4 warps per patch)
 };
 
 template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>

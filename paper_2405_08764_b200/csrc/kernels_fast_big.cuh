@@ -1,0 +1,359 @@
+// FAST-mode fused gap-tooth kernel for large patches (32x32 micro nodes, the
+// biggest config-5 shape): one CTA of WPP = 4 warps per patch.
+//
+// Same per-node algebra as kernels_fast.cuh (folded weights in registers,
+// difference form of the mixed term, per-patch ghost constant), but a patch
+// of 1024 nodes needs 128 lanes of 2x4 nodes: lane r = bj*LI + bi with LI = 16,
+// so xi-neighbours (bi +- 1) share a warp and exchange through immediate-delta
+// shuffles, while eta-neighbours cross warps every second block row.  The
+// eta halo rows therefore go through shared memory: each lane publishes its
+// block's bottom and top rows, one CTA barrier per micro-step (rows are
+// double-buffered by step parity), and reads back the row above/below over
+// columns i0-1 .. i0+2, which also yields the xi-differences e(i, j0-1) and
+// e(i, j0+BJ) of the mixed term without a second exchange.
+#pragma once
+
+#include "kernels_fast.cuh"
+
+namespace pdb200::dev {
+
+template <int N_, bool MIXED_>
+struct BigCfg {
+    static constexpr int N1 = N_, N2 = N_, BI = 2, BJ = 4;
+    static constexpr bool MIXED = MIXED_;
+    static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, WPP = LP / 32;
+    static constexpr int NPL = BI * BJ, NW = MIXED ? 6 : 5, NWL = NW * NPL, S = (NWL + 1) / 2;
+    static constexpr int L = N_;
+    static constexpr int ROW = N1 + 4; // padded row: column i at index i + 2
+    static_assert(LP % 32 == 0 && LI <= 32, "rows of blocks must not straddle warps");
+};
+
+// Weight tile of warp w of patch q at unit q*WPP + w: the FastCfg layout with
+// one "unit" per warp (lane r = w*32 + lane of the patch).
+template <class Cfg>
+__global__ void k_fold_big(Params p, const double* __restrict__ coeffs, const int* __restrict__ cset,
+                           double* __restrict__ W, int nunits) {
+    const size_t total = (size_t)nunits * 32 * (2 * Cfg::S);
+    const double idx2 = 1.0 / (p.mdxi * p.mdxi), idy2 = 1.0 / (p.mdeta * p.mdeta);
+    const double idx = 1.0 / (2.0 * p.mdxi), idy = 1.0 / (2.0 * p.mdeta);
+    const double ixy = 1.0 / (4.0 * p.mdxi * p.mdeta);
+    const double dt = p.mdt;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const int half = (int)(t & 1);
+        const size_t q = t >> 1;
+        const int lane = (int)(q % 32);
+        const size_t us = q / 32;
+        const int s = (int)(us % Cfg::S);
+        const size_t unit = us / Cfg::S;
+        const int f = 2 * s + half;
+        const long patch = (long)(unit / Cfg::WPP);
+        const int r = (int)(unit % Cfg::WPP) * 32 + lane;
+        double val = 0.0;
+        if (patch < p.P && f < Cfg::NWL) {
+            const int kind = f / Cfg::NPL, node = f % Cfg::NPL;
+            const int ii = node / Cfg::BJ, jj = node % Cfg::BJ;
+            const int bi = r % Cfg::LI, bj = r / Cfg::LI;
+            const int i = bi * Cfg::BI + ii, j = bj * Cfg::BJ + jj;
+            const int set = cset ? cset[patch] : (int)patch;
+            const double* c = coeffs + (size_t)set * PD_NCOEF * p.N;
+            const int k = i * p.n2 + j;
+            const double A = c[PD_COEF_A * p.N + k], B = c[PD_COEF_B * p.N + k], C = c[PD_COEF_C * p.N + k];
+            const double Vx = c[PD_COEF_VX * p.N + k], Vy = c[PD_COEF_VY * p.N + k], Wr = c[PD_COEF_W * p.N + k];
+            const double ax = A * idx2, vx = Vx * idx, cy = C * idy2, vy = Vy * idy;
+            const double wE = dt * (ax - vx), wW = dt * (ax + vx), wN = dt * (cy - vy), wS = dt * (cy + vy);
+            const bool Wb = i == 0, Eb = i == Cfg::N1 - 1, Sb = j == 0, Nb = j == Cfg::N2 - 1;
+            switch (kind) { // same static Neumann reflection as k_fold
+                case WE: val = Wb ? wE + wW : wE; break;
+                case WW: val = Eb ? wW + wE : wW; break;
+                case WN: val = Sb ? wN + wS : wN; break;
+                case WS: val = Nb ? wS + wN : wS; break;
+                case WD: val = dt * (B * ixy); break;
+                default: val = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr); break;
+            }
+        }
+        W[((unit * Cfg::S + s) * 32 + lane) * 2 + half] = val;
+    }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(32 * Cfg::WPP, 3)
+k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
+           const int* __restrict__ nbr, const double* __restrict__ Wt, const int* __restrict__ fail_flag) {
+    constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LJ = Cfg::LJ, NPL = Cfg::NPL, S = Cfg::S;
+    constexpr int N1 = Cfg::N1, N2 = Cfg::N2, ROW = Cfg::ROW, WPP = Cfg::WPP;
+    constexpr bool MIXED = Cfg::MIXED;
+    __shared__ double s_g[8][Cfg::L];                   // ghost offsets + mixed ring offsets
+    __shared__ __align__(16) double s_row[2][LJ][2][ROW]; // [parity][block row][bottom, top][padded column]
+    __shared__ double s_red[WPP];
+    if (fail_flag && *fail_flag) return;
+    const int patch = blockIdx.x;
+    const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+    const int bi = r % LI, bj = r / LI;
+    const int i0 = bi * BI, j0 = bj * BJ;
+
+    // ---- loads: stencil indices first, then the weight tile ----------------
+    int idx[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) idx[q] = __ldg(nbr + 9 * patch + q);
+    double w[2 * S];
+    {
+        const double2* wp = reinterpret_cast<const double2*>(Wt) + ((size_t)patch * WPP + warp) * S * 32 + lane;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const double2 t = __ldg(wp + s * 32);
+            w[2 * s] = t.x;
+            w[2 * s + 1] = t.y;
+        }
+    }
+#define WT(k, ii, jj) w[(k) * NPL + (ii) * BJ + (jj)]
+    double v[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) v[q] = __ldg(F + idx[q]);
+    // zero the row pads once (columns -2, -1, N1, N1+1 are never written)
+    for (int t = r; t < 2 * LJ * 2 * 4; t += 32 * WPP) {
+        const int pad = t & 3, rest = t >> 2;
+        (&s_row[0][0][0][0])[rest * ROW + (pad < 2 ? pad : N1 + pad)] = 0.0;
+    }
+
+    // ---- centre derivatives, ghost offsets, ring offsets (as patch_body) ----
+    const double Uxi = (v[7] - v[1]) * p.i2Dxi;
+    const double Ueta = (v[5] - v[3]) * p.i2Deta;
+    const double hUxx = 0.5 * ((v[7] - 2.0 * v[4] + v[1]) * p.iDxi2);
+    const double hUyy = 0.5 * ((v[5] - 2.0 * v[4] + v[3]) * p.iDeta2);
+    const double Uxy = (v[8] - v[6] - v[2] + v[0]) * p.i4DD;
+    const double C0 = v[4] - p.c24x * (2.0 * hUxx) - p.c24y * (2.0 * hUyy);
+    for (int t = r; t < 2 * N2 + 2 * N1; t += 32 * WPP) {
+        if (t < 2 * N2) {
+            const int e = t < N2 ? PD_EDGE_E : PD_EDGE_W, j = t < N2 ? t : t - N2;
+            const double* d = p.dlag[e];
+            const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
+            const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
+            const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
+            s_g[e][j] = p.gsc[e] * (p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2);
+        } else {
+            const int u = t - 2 * N2;
+            const int e = u < N1 ? PD_EDGE_N : PD_EDGE_S, i = u < N1 ? u : u - N1;
+            const double* d = p.dlag[e];
+            const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
+            const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
+            const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
+            s_g[e][i] = p.gsc[e] * (p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2);
+        }
+    }
+    __syncthreads();
+    const double* gE = s_g[PD_EDGE_E];
+    const double* gW = s_g[PD_EDGE_W];
+    const double* gN = s_g[PD_EDGE_N];
+    const double* gS = s_g[PD_EDGE_S];
+    if constexpr (MIXED) {
+        auto off = [&](int pp, int qq) {
+            const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
+            const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
+            double o = 0.0;
+            if (pp < 0) o += gW[qc];
+            if (pp > N1 - 1) o += gE[qc];
+            if (qq < 0) o += gS[pc];
+            if (qq > N2 - 1) o += gN[pc];
+            return o;
+        };
+        for (int t = r; t < 2 * N2 + 2 * N1; t += 32 * WPP) {
+            int e, i, j, k;
+            if (t < 2 * N2) {
+                e = t < N2 ? PD_EDGE_E : PD_EDGE_W;
+                k = j = t < N2 ? t : t - N2;
+                i = e == PD_EDGE_E ? N1 - 1 : 0;
+            } else {
+                const int u = t - 2 * N2;
+                e = u < N1 ? PD_EDGE_N : PD_EDGE_S;
+                k = i = u < N1 ? u : u - N1;
+                j = e == PD_EDGE_N ? N2 - 1 : 0;
+            }
+            s_g[4 + e][k] = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
+        }
+        __syncthreads();
+    }
+
+    // ---- lift + boundary fold-in ------------------------------------------
+    double u[BI][BJ], c[BI][BJ];
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii) {
+        const int i = i0 + ii;
+        const double X = -0.5 * p.h_xi + p.mdxi * i;
+        const double Ai = C0 + X * (Uxi + X * hUxx), Bi = Ueta + X * Uxy;
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+            const int j = j0 + jj;
+            const double Y = -0.5 * p.h_eta + p.mdeta * j;
+            u[ii][jj] = Ai + Y * (Bi + Y * hUyy);
+            const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
+            const bool Sb = jj == 0 && bj == 0, Nb = jj == BJ - 1 && bj == LJ - 1;
+            double cc = 0.0;
+            if (Wb) { cc = fma(WT(WW, ii, jj), gW[j], cc); WT(WW, ii, jj) = 0.0; }
+            if (Eb) { cc = fma(WT(WE, ii, jj), gE[j], cc); WT(WE, ii, jj) = 0.0; }
+            if (Sb) { cc = fma(WT(WS, ii, jj), gS[i], cc); WT(WS, ii, jj) = 0.0; }
+            if (Nb) { cc = fma(WT(WN, ii, jj), gN[i], cc); WT(WN, ii, jj) = 0.0; }
+            if constexpr (MIXED) {
+                if (Wb || Eb || Sb || Nb) {
+                    const double* dd = s_g[4 + (Wb ? PD_EDGE_W : Eb ? PD_EDGE_E : Sb ? PD_EDGE_S : PD_EDGE_N)];
+                    cc = fma(WT(WD, ii, jj), dd[(Wb || Eb) ? j : i], cc);
+                    WT(WD, ii, jj) = 0.0;
+                }
+            }
+            c[ii][jj] = cc;
+        }
+    }
+
+    // ---- K fused micro-steps ------------------------------------------------
+    const int bjS = bj > 0 ? bj - 1 : bj, bjN = bj < LJ - 1 ? bj + 1 : bj; // patch edges read finite junk
+    for (int step = 0; step < p.nt; ++step) {
+        const int par = step & 1;
+        double* mine = &s_row[par][bj][0][i0 + 2];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            mine[ii] = u[ii][0];             // bottom row of the block
+            mine[ROW + ii] = u[ii][BJ - 1];  // top row
+        }
+        __syncthreads();
+        // eta halos + their xi-differences from the neighbouring block rows
+        const double* rs = &s_row[par][bjS][1][i0 + 2]; // top row of the block below
+        const double* rn = &s_row[par][bjN][0][i0 + 2]; // bottom row of the block above
+        double hS[BI], hN[BI], eS[BI], eN[BI];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            hS[ii] = rs[ii];
+            hN[ii] = rn[ii];
+        }
+        if constexpr (MIXED) {
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii) {
+                eS[ii] = rs[ii + 1] - rs[ii - 1];
+                eN[ii] = rn[ii + 1] - rn[ii - 1];
+            }
+        }
+        double cE[BJ], cW[BJ];
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+            cE[jj] = __shfl_down_sync(0xffffffffu, u[0][jj], 1);
+            cW[jj] = __shfl_up_sync(0xffffffffu, u[BI - 1][jj], 1);
+        }
+        auto at = [&](int a, int b) -> double { // block-relative, a in [-1,BI], b in [-1,BJ] (no corners)
+            if (a == BI) return cE[b];
+            if (a == -1) return cW[b];
+            if (b == BJ) return hN[a];
+            if (b == -1) return hS[a];
+            return u[a][b];
+        };
+        double nu[BI][BJ];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WC, ii, jj), u[ii][jj], c[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WN, ii, jj), at(ii, jj + 1), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WS, ii, jj), at(ii, jj - 1), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WE, ii, jj), at(ii + 1, jj), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
+        if constexpr (MIXED) {
+            double e[BI][BJ];
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < BJ; ++jj) e[ii][jj] = at(ii + 1, jj) - at(ii - 1, jj);
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < BJ; ++jj) {
+                    const double upv = jj + 1 < BJ ? e[ii][jj + 1] : eN[ii];
+                    const double dnv = jj > 0 ? e[ii][jj - 1] : eS[ii];
+                    nu[ii][jj] = fma(WT(WD, ii, jj), upv - dnv, nu[ii][jj]);
+                }
+        }
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) u[ii][jj] = nu[ii][jj];
+    }
+#undef WT
+
+    // ---- trapezoid restriction: lane partials, warp reduce, CTA reduce -------
+    double part = 0.0;
+    {
+        const double ox = 1.0 / (N1 - 1), oy = 1.0 / (N2 - 1);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            double row = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+                const bool edge = (jj == 0 && bj == 0) || (jj == BJ - 1 && bj == LJ - 1);
+                row += (edge ? 0.5 * oy : oy) * u[ii][jj];
+            }
+            const bool edge = (ii == 0 && bi == 0) || (ii == BI - 1 && bi == LI - 1);
+            part += (edge ? 0.5 * ox : ox) * row;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) s_red[warp] = part;
+    __syncthreads();
+    if (r == 0) {
+        double avg = 0.0;
+#pragma unroll
+        for (int q = 0; q < WPP; ++q) avg += s_red[q];
+        const size_t node = (size_t)idx[4];
+        if (out_mode == 0) {
+            out[node] = avg;
+        } else if (out_mode == 1) {
+            const double U = v[4];
+            out[node] = U + p.dt_macro * ((avg - U) / p.tau); // cpi.cpp:54, 74 (k = 0)
+        } else {
+            out[patch] = avg;
+        }
+    }
+}
+
+using BC32 = BigCfg<32, false>;
+using BC32M = BigCfg<32, true>;
+
+} // namespace pdb200::dev
+
+namespace pdb200::dev {
+
+inline bool plan_big(const Params& p, FastPlan& plan) {
+    if (p.bc_type != PD_BC_NEUMANN || p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
+    if (!(p.n1 == 32 && p.n2 == 32)) return false;
+    plan.big = 1;
+    plan.mixed = p.mixed;
+    plan.id = p.mixed ? 101 : 100;
+    plan.LP = BC32::LP;
+    plan.G = 1;
+    plan.S = p.mixed ? BC32M::S : BC32::S;
+    plan.nunits = p.P * BC32::WPP;
+    return true;
+}
+
+inline void fold_big(const FastPlan& plan, const Params& p, const double* coeffs, const int* cset, double* W,
+                     cudaStream_t s) {
+    const size_t total = (size_t)plan.nunits * plan.S * 64;
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+    if (plan.mixed) k_fold_big<BC32M><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits);
+    else k_fold_big<BC32><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits);
+}
+
+inline void launch_big(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
+                       const int* nbr, const double* W, const int* fail, cudaStream_t s) {
+    if (plan.mixed) k_fast_big<BC32M><<<p.P, 32 * BC32M::WPP, 0, s>>>(p, F, out, out_mode, nbr, W, fail);
+    else k_fast_big<BC32><<<p.P, 32 * BC32::WPP, 0, s>>>(p, F, out, out_mode, nbr, W, fail);
+}
+
+} // namespace pdb200::dev

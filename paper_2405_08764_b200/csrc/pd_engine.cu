@@ -17,6 +17,7 @@
 
 #include "kernels_exact.cuh"
 #include "kernels_fast.cuh"
+#include "kernels_fast_big.cuh"
 #include "kernels_misc.cuh"
 #include "patchdyn_b200.h"
 
@@ -95,7 +96,9 @@ struct pd_engine {
 
     // ---- one gap-tooth substep F -> out (patch nodes) -------------------
     void launch_step(const double* F, double* out, int out_mode, const double* srct, const int* fail) {
-        if (mode == PD_MODE_FAST) {
+        if (mode == PD_MODE_FAST && fast.big) {
+            launch_big(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
+        } else if (mode == PD_MODE_FAST) {
             launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_nbr12.p, d_weights.p, fail, stream);
         } else {
             k_gaptooth_exact<<<prm.P, kExactThreads, exact_smem_bytes(prm), stream>>>(
@@ -356,7 +359,14 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
         // kernel family
         e->mode = PD_MODE_EXACT;
         if (d.mode == PD_MODE_FAST && d.source_kind == PD_SOURCE_ZERO) {
-            if (plan_fast(p, e->fast)) {
+            if (plan_big(p, e->fast)) {
+                const size_t wcount = fast_weights_count(e->fast, p);
+                e->d_weights.alloc(wcount);
+                fold_big(e->fast, p, e->d_coeffs.p, e->d_cset.p, e->d_weights.p, e->stream);
+                e->check_launch();
+                e->device_bytes += wcount * 8;
+                e->mode = PD_MODE_FAST;
+            } else if (plan_fast(p, e->fast)) {
                 const size_t wcount = fast_weights_count(e->fast, p);
                 e->d_weights.alloc(wcount);
                 fold_weights(e->fast, p, e->d_coeffs.p, e->d_cset.p, e->d_weights.p, e->stream);

@@ -317,3 +317,22 @@ def test_cpp_dropin_runs_config1(mode, tmp_path, gpu):
         assert "max_pct_err=%.12f" % float(FINALS["c1_diffusion_maxpct"]) in r.stdout
     else:
         assert rel(U, FINALS["c1_diffusion_final"]) < TOL
+
+
+# ---------------------------------------------------------------------------
+# config-5 shapes: 8x8 and 32x32 patches (the 32x32 FAST kernel spans 4 warps)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("nodes", [8, 32])
+def test_config5_shapes_fast_vs_oracle(nodes, restated, gpu):
+    base, _ = configs.load("c5_sweep")
+    d = configs.sweep_desc(base, 8 if nodes == 32 else 10, nodes, 10)
+    P = Problem(d)
+    ed = P.engine_desc()
+    U0 = P.initial_field()
+    E = Engine.from_problem(P, mode=FAST)
+    assert E.mode == FAST
+    _, Uo, _ = restated.run(ed, U0, 6)
+    Ug, _ = E.run(U0, 6)
+    assert rel(Ug, Uo) < TOL
+    Ux, _ = Engine.from_problem(P, mode=EXACT).run(U0, 6)
+    assert np.array_equal(Ux, Uo)
