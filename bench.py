@@ -197,6 +197,75 @@ def run_reference(args, rank, world):
     return 0
 
 
+def run_sweep(args):
+    """BASELINE config 5: updates/s and roofline fraction at every sweep point,
+    next to the restated CPU oracle on a bounded patch sample (host cores)."""
+    import gc
+
+    import torch
+
+    from oracle.pyoracle import Restated
+    from paper_2405_08764_b200.engine import Engine, Problem, fp64_peak
+
+    base, vals = configs.load("c5_sweep")
+    sizes = [int(x) for x in vals["sweep.log2_patches"].split(",")]
+    nodes_l = [int(x) for x in vals["sweep.micro_nodes"].split(",")]
+    Ks = [int(x) for x in vals["sweep.K"].split(",")]
+    if args.sweep_max_log2:
+        sizes = [s for s in sizes if s <= args.sweep_max_log2]
+    p64, ghz = fp64_peak(200.0)
+    bw, bw_src = peaks()
+    O = Restated()
+    out_path = ROOT / "profiles" / f"c5_sweep_{args.tag}.jsonl"
+    rows = []
+    for nodes in nodes_l:
+        for lp in sizes:
+            for K in Ks:
+                d = configs.sweep_desc(base, lp, nodes, K)
+                t0 = time.perf_counter()
+                prob = Problem(d)
+                eng = Engine.from_problem(prob)
+                build_s = time.perf_counter() - t0
+                P, N, Kk = workload(prob.desc)
+                U0 = prob.initial_field()
+                dU = torch.from_numpy(U0.ravel()).cuda()
+                dS = torch.empty_like(dU)
+                eng.run_device(dU.data_ptr(), dS.data_ptr(), 3)  # warm-up
+                dU.copy_(torch.from_numpy(U0.ravel()))
+                steps = max(3, min(20, int(2e11 // (P * N * K)) or 3))
+                torch.cuda.synchronize()
+                st = eng.run_device(dU.data_ptr(), dS.data_ptr(), steps)
+                kms = eng.bench_step_kernel(dU.data_ptr(), dS.data_ptr(), reps=3)
+                upd = P * N * K
+                flops, byts = upd * 14, P * (N * 48 + 16)
+                t_fp, t_bw = flops / (p64 * 1e12), byts / (bw * 1e9)
+                bound = "fp64" if t_fp >= t_bw else "hbm"
+                frac = max(t_fp, t_bw) / (kms * 1e-3)
+                # CPU oracle on a bounded sample (about 1 s of host work)
+                ed = prob.engine_desc()
+                n = min(P, max(8, int(2e7 // (N * K))))
+                idx = np.sort(np.random.default_rng(lp).choice(P, n, replace=False)).astype(np.int32)
+                _, csec = O.patch_subset(ed, U0, 0.0, idx)
+                row = {"config": "c5_sweep", "log2_patches": lp, "patches": P, "micro_nodes": f"{nodes}x{nodes}", "K": K,
+                       "kernel_family": "fast" if eng.mode == abi.PD_MODE_FAST else "exact",
+                       "updates_per_s": upd / (kms * 1e-3), "step_updates_per_s": upd * steps / (st.device_ms * 1e-3),
+                       "kernel_ms": kms, "ms_per_macro_step": st.device_ms / steps, "roofline_bound": bound,
+                       "roofline_frac": frac, "fp64_peak_tflops": p64, "hbm_peak_gbs": bw,
+                       "achieved_tflops": flops / (kms * 1e-3) / 1e12, "achieved_gbs": byts / (kms * 1e-3) / 1e9,
+                       "cpu_oracle_updates_per_s": n * N * K / csec, "cpu_cores": O.threads, "cpu_sample_patches": n,
+                       "host_build_s": build_s, "device_gb": eng.device_bytes / 1e9}
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                del eng, prob, dU, dS
+                gc.collect()
+                torch.cuda.empty_cache()
+    (ROOT / "profiles").mkdir(exist_ok=True)
+    with open(out_path, "w") as f:
+        for r in rows:
+            f.write(json.dumps(r) + "\n")
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -206,7 +275,12 @@ def main():
     ap.add_argument("--config", default="c4_shear")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="config-5 sweep -> profiles/c5_sweep_<tag>.jsonl")
+    ap.add_argument("--sweep-max-log2", type=int, default=0)
+    ap.add_argument("--tag", default="r01")
     args = ap.parse_args()
+    if args.sweep:
+        return run_sweep(args)
     if args.warmup < 3:
         args.warmup = 3
 

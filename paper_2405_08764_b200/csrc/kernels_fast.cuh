@@ -21,31 +21,17 @@
 #pragma once
 
 #include <algorithm>
-#include <cstdlib>
-#include <vector>
 
 #include "pd_device.cuh"
 
-#ifndef PD_STEP_UNROLL
-#define PD_STEP_UNROLL 1 // micro-step loop unroll (dev knob)
-#endif
 
 namespace pdb200::dev {
 
 struct FastPlan {
-    int id = -1;     // instantiation index
+    int id = -1; // instantiation index
     int LP = 0, G = 0, S = 0, nunits = 0;
     int mixed = 0;
-    // 1: one-shot launch, difference form of the mixed term (default)
-    // 0: persistent warps + TMA bulk prefetch of the next weight tile
-    // 2: one-shot launch, corner form of the mixed term
-    int variant = 1;
-    int grid = 0;       // persistent grid (CTAs)
-    int smem_bytes = 0; // persistent dynamic shared memory per CTA
-    int first_wave = 0; // one-shot: CTAs resident at once (occupancy x SMs)
-    int stagger_ns = 0; // one-shot: start offset per residency slot
-    int sms = 148;
-    int big = 0;        // 32x32 patches: kernels_fast_big.cuh (one CTA of 4 warps per patch)
+    int big = 0; // 32x32 patches: kernels_fast_big.cuh (one CTA of 4 warps per patch)
 };
 
 template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
@@ -63,7 +49,6 @@ struct FastCfg {
 };
 enum { WC = 0, WE = 1, WW = 2, WN = 3, WS = 4, WD = 5 };
 constexpr int kFastWarps = 1; // one warp per CTA: warps retire and are replaced independently
-constexpr int kStepUnroll = PD_STEP_UNROLL;
 
 // ---- fold: solver-form coefficients -> lane-interleaved weight table -------
 // Table layout: unit u (one warp = G patches) owns S*32 double2 slots; slot s
@@ -119,7 +104,7 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
 // ---- per-patch body: lift, boundary fold-in, K micro-steps, restriction --
 // Everything after the weights (w, registers) and the 3x3 stencil (v) are in
 // hand; shared by the one-shot and the persistent kernels.
-template <class Cfg, int VAR>
+template <class Cfg>
 __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg::S], const double (&v)[9], int lane,
                                            bool valid, int patch, double (*sg)[8][Cfg::L], double* sred,
                                            const int* __restrict__ nbr, double* __restrict__ out, int out_mode) {
@@ -239,7 +224,6 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     // (measured: scripts/ubench/ubench2.cu).  A lane on a
     // patch edge receives some other finite value for the missing side; the
     // boundary fold-in above has zeroed every weight that would read it.
-#pragma unroll kStepUnroll
     for (int step = 0; step < p.nt; ++step) {
         double hN[BI], hS[BI];
 #pragma unroll
@@ -253,14 +237,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             cE[jj + 1] = __shfl_down_sync(0xffffffffu, u[0][jj], 1);
             cW[jj + 1] = __shfl_up_sync(0xffffffffu, u[BI - 1][jj], 1);
         }
-        if constexpr (MIXED && VAR == 1) {
-            cE[0] = __shfl_down_sync(0xffffffffu, hS[0], 1);
-            cE[BJ + 1] = __shfl_down_sync(0xffffffffu, hN[0], 1);
-            cW[0] = __shfl_up_sync(0xffffffffu, hS[BI - 1], 1);
-            cW[BJ + 1] = __shfl_up_sync(0xffffffffu, hN[BI - 1], 1);
-        } else {
-            cE[0] = cE[BJ + 1] = cW[0] = cW[BJ + 1] = 0.0;
-        }
+        cE[0] = cE[BJ + 1] = cW[0] = cW[BJ + 1] = 0.0; // corners are not exchanged (difference form)
         // value at block-relative (a, b), a in [-1,BI], b in [-1,BJ]
         auto at = [&](int a, int b) -> double {
             if (a == BI) return cE[b + 1];
@@ -293,16 +270,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
-        if constexpr (MIXED && VAR == 1) {
-            // corner form: D = (uNE + uSW) - (uNW + uSE), 4 DP per node
-#pragma unroll
-            for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-                for (int jj = 0; jj < BJ; ++jj) {
-                    const double D = (at(ii + 1, jj + 1) + at(ii - 1, jj - 1)) - (at(ii - 1, jj + 1) + at(ii + 1, jj - 1));
-                    nu[ii][jj] = fma(WT(WD, ii, jj), D, nu[ii][jj]);
-                }
-        } else if constexpr (MIXED) {
+        if constexpr (MIXED) {
             // difference form: e(i,j) = u(i+1,j) - u(i-1,j) once per node, then
             // D(i,j) = e(i,j+1) - e(i,j-1); e crosses lanes only at the block's
             // eta ends.  3 DP per node instead of 4 (8 per update in total).
@@ -370,11 +338,10 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 }
 
 // ---- the fused step, one warp-unit per launch slot -----------------------
-template <class Cfg, int VAR>
+template <class Cfg>
 __global__ void __launch_bounds__(32 * kFastWarps)
 k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
-       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag, int first_wave, int stagger_ns,
-       int sms) {
+       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
     constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
     __shared__ double s_g[kFastWarps][G][8][L]; // ghost offsets + mixed-term ring offsets per edge
     __shared__ double s_red[kFastWarps][32];
@@ -382,12 +349,6 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int unit = blockIdx.x * kFastWarps + warp;
     if (unit >= nunits) return; // warp-uniform
-    // Every patch costs the same, so without intervention the resident warps of
-    // an SM run in lock-step: all in the latency-bound prologue, then all in the
-    // FP64 loop.  Offsetting the first residency wave by slot staggers them for
-    // the whole launch (each retiring warp's successor inherits its phase), and
-    // the prologues overlap other warps' FP64 work.
-    if (stagger_ns > 0 && (int)blockIdx.x < first_wave) __nanosleep((unsigned)(((int)blockIdx.x / sms) * stagger_ns));
     const int g = lane / LP;
     const int patch = unit * G + g;
     const bool valid = g < G && patch < p.P;
@@ -409,201 +370,7 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
     double v[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + idx[q]) : 0.0;
-    patch_body<Cfg, VAR>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, out_mode);
-}
-
-// ---- async-copy helpers (TMA bulk copy + mbarrier, cp.async) -------------
-__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    uint64_t state;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
-                 : "=l"(state)
-                 : "r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-    (void)state;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred done;\n"
-        "PD_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
-        "@!done bra PD_WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// global -> shared bulk copy (TMA engine, UBLKCP), completion counted on bar
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// order this thread's generic-proxy shared accesses before later async-proxy writes
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-template <class Cfg>
-struct PersistLayout {
-    static constexpr int WB = Cfg::S * 32 * 16;                // weight tile bytes per unit
-    static constexpr int NB = ((Cfg::G * 48 + 127) / 128) * 128; // neighbour rows (12 ints per patch)
-    static constexpr int GB = Cfg::G * 8 * Cfg::L * 8;          // ghost offsets + ring offsets
-    static constexpr int RB = 32 * 8;                          // restriction partials
-    static constexpr int WARP_BYTES = ((WB + NB + GB + RB + 32 + 127) / 128) * 128; // + mbarrier + loop state
-    static constexpr int CTA_BYTES = WARP_BYTES * kFastWarps;
-};
-
-// ---- the fused step, persistent warps with a bulk-async weight prefetch ----
-// Each warp walks units u, u + stride, ...; while it integrates unit u the
-// TMA engine streams unit u+stride's weight tile (S*32*16 bytes, contiguous)
-// and neighbour rows into this warp's shared-memory slot, so the HBM stream of
-// coefficients overlaps the FP64 work instead of stalling each patch start.
-template <class Cfg, int VAR>
-__global__ void __launch_bounds__(32 * kFastWarps, 3)
-k_fast_p(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
-         const int* __restrict__ nbr, const int* __restrict__ nbr12, const double* __restrict__ Wt, int nunits,
-         const int* __restrict__ fail_flag) {
-    using Lay = PersistLayout<Cfg>;
-    constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L, S = Cfg::S;
-    extern __shared__ __align__(128) unsigned char smem[];
-    if (fail_flag && *fail_flag) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char* base = smem + warp * Lay::WARP_BYTES;
-    const double2* wbuf = reinterpret_cast<const double2*>(base);
-    int* nbuf = reinterpret_cast<int*>(base + Lay::WB);
-    double(*sg)[8][L] = reinterpret_cast<double(*)[8][L]>(base + Lay::WB + Lay::NB);
-    double* sred = reinterpret_cast<double*>(base + Lay::WB + Lay::NB + Lay::GB);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + Lay::WB + Lay::NB + Lay::GB + Lay::RB);
-    // loop-carried state lives in shared memory (volatile), not in registers:
-    // the hot loop inside patch_body needs all 168 the compiler may use
-    volatile int* st = reinterpret_cast<volatile int*>(bar + 1);
-    const int stride = gridDim.x * kFastWarps;
-    const int first = blockIdx.x * kFastWarps + warp;
-    if (first >= nunits) return; // warp-uniform
-    if (lane == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        st[0] = first;
-        st[1] = 0;
-        mbar_expect_tx(bar, Lay::WB + G * 48);
-        bulk_g2s(base, Wt + (size_t)first * S * 64, Lay::WB, bar);
-        bulk_g2s(nbuf, nbr12 + (size_t)first * G * 12, G * 48, bar);
-    }
-    __syncwarp();
-    while (true) {
-        const int unit = st[0];
-        if (unit >= nunits) break;
-        const uint32_t phase = static_cast<uint32_t>(st[1]);
-        int ln;
-        asm volatile("mov.u32 %0, %%laneid;" : "=r"(ln));
-        const int g = ln / LP;
-        mbar_wait(bar, phase);
-        const int patch = unit * G + g;
-        const bool valid = g < G && patch < p.P;
-        double v[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + nbuf[(g < G ? g : 0) * 12 + q]) : 0.0;
-        double w[2 * S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const double2 t = wbuf[s * 32 + ln];
-            w[2 * s] = t.x;
-            w[2 * s + 1] = t.y;
-        }
-        __syncwarp();
-        fence_proxy_async();
-        if (ln == 0) {
-            const int nxt = unit + stride;
-            st[0] = nxt;
-            st[1] = static_cast<int>(phase ^ 1u);
-            if (nxt < nunits) {
-                mbar_expect_tx(bar, Lay::WB + G * 48);
-                bulk_g2s(base, Wt + (size_t)nxt * S * 64, Lay::WB, bar);
-                bulk_g2s(nbuf, nbr12 + (size_t)nxt * G * 12, G * 48, bar);
-            }
-        }
-        __syncwarp();
-        patch_body<Cfg, VAR>(p, w, v, ln, valid, patch, sg, sred, nbr, out, out_mode);
-        __syncwarp();
-    }
-}
-
-// ---- two patch groups per warp, straight-line, TMA prefetch of the second --
-// The second unit's weight tile and neighbour rows stream into this warp's
-// shared-memory slot (cp.async.bulk + mbarrier) while the first unit runs its
-// K micro-steps, halving the exposed per-unit prologue latency without the
-// loop-carried state of a persistent kernel.
-template <class Cfg, int VAR>
-__global__ void __launch_bounds__(32 * kFastWarps)
-k_fast2(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
-        const int* __restrict__ nbr12, const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
-    using Lay = PersistLayout<Cfg>;
-    constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L, S = Cfg::S;
-    extern __shared__ __align__(128) unsigned char smem[];
-    if (fail_flag && *fail_flag) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char* base = smem + warp * Lay::WARP_BYTES;
-    const double2* wbuf = reinterpret_cast<const double2*>(base);
-    int* nbuf = reinterpret_cast<int*>(base + Lay::WB);
-    double(*sg)[8][L] = reinterpret_cast<double(*)[8][L]>(base + Lay::WB + Lay::NB);
-    double* sred = reinterpret_cast<double*>(base + Lay::WB + Lay::NB + Lay::GB);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(base + Lay::WB + Lay::NB + Lay::GB + Lay::RB);
-    const int u0 = 2 * (blockIdx.x * kFastWarps + warp), u1 = u0 + 1;
-    if (u0 >= nunits) return; // warp-uniform
-    const bool two = u1 < nunits;
-    if (lane == 0 && two) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(bar, Lay::WB + G * 48);
-        bulk_g2s(base, Wt + (size_t)u1 * S * 64, Lay::WB, bar);
-        bulk_g2s(nbuf, nbr12 + (size_t)u1 * G * 12, G * 48, bar);
-    }
-    const int g = lane / LP;
-    {
-        const int patch = u0 * G + g;
-        const bool valid = g < G && patch < p.P;
-        int idx[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) idx[q] = valid ? __ldg(nbr + 9 * patch + q) : 0;
-        double w[2 * S];
-        const double2* wp = reinterpret_cast<const double2*>(Wt) + (size_t)u0 * S * 32 + lane;
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const double2 t = __ldg(wp + s * 32);
-            w[2 * s] = t.x;
-            w[2 * s + 1] = t.y;
-        }
-        double v[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + idx[q]) : 0.0;
-        patch_body<Cfg, VAR>(p, w, v, lane, valid, patch, sg, sred, nbr, out, out_mode);
-    }
-    if (!two) return;
-    __syncwarp();
-    mbar_wait(bar, 0);
-    {
-        int ln;
-        asm volatile("mov.u32 %0, %%laneid;" : "=r"(ln));
-        const int g1 = ln / LP;
-        const int patch = u1 * G + g1;
-        const bool valid = g1 < G && patch < p.P;
-        double v[9];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + nbuf[(g1 < G ? g1 : 0) * 12 + q]) : 0.0;
-        double w[2 * S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const double2 t = wbuf[s * 32 + ln];
-            w[2 * s] = t.x;
-            w[2 * s + 1] = t.y;
-        }
-        patch_body<Cfg, VAR>(p, w, v, ln, valid, patch, sg, sred, nbr, out, out_mode);
-    }
+    patch_body<Cfg>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, out_mode);
 }
 
 // ---- instantiations --------------------------------------------------------
@@ -628,7 +395,6 @@ inline bool plan_fast(const Params& p, FastPlan& plan) {
 #undef PD_MATCH
     if (id < 0) return false;
     plan.id = id;
-    if (const char* v = std::getenv("PD_FAST_VARIANT")) plan.variant = std::atoi(v); // dev A/B switch
     plan.mixed = p.mixed;
 #define PD_FILL(ID, CFG)                               \
     if (id == ID) {                                    \
@@ -656,57 +422,11 @@ inline void fold_weights(const FastPlan& plan, const Params& p, const double* co
 #undef PD_FOLD
 }
 
-// Neighbour rows padded to 12 ints per patch, grouped by unit (bulk-copyable).
-inline std::vector<int> fast_nbr12(const FastPlan& plan, int P, const int* nbr9) {
-    std::vector<int> t((size_t)plan.nunits * plan.G * 12, 0);
-    for (int q = 0; q < P; ++q)
-        for (int k = 0; k < 9; ++k) t[(size_t)q * 12 + k] = nbr9[(size_t)q * 9 + k];
-    return t;
-}
-
-// Persistent grid: exactly the resident capacity (occupancy API) or fewer.
-inline void setup_persistent(FastPlan& plan) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#define PD_OCC(ID, CFG)                                                                                           \
-    if (plan.id == ID) {                                                                                           \
-        plan.smem_bytes = PersistLayout<CFG>::CTA_BYTES;                                                           \
-        cudaFuncSetAttribute(k_fast_p<CFG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);      \
-        cudaFuncSetAttribute(k_fast2<CFG, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);       \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fast_p<CFG, 0>, 32 * kFastWarps, plan.smem_bytes); \
-    }
-    PD_FAST_CONFIGS(PD_OCC)
-#undef PD_OCC
-    const int units_blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
-    plan.grid = std::max(1, std::min(units_blocks, sms * std::max(per_sm, 1)));
-    int per_sm1 = 0;
-#define PD_OCC1(ID, CFG) \
-    if (plan.id == ID) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, k_fast<CFG, 0>, 32 * kFastWarps, 0);
-    PD_FAST_CONFIGS(PD_OCC1)
-#undef PD_OCC1
-    plan.sms = sms;
-    plan.first_wave = sms * std::max(per_sm1, 1);
-    plan.stagger_ns = 1000;
-    if (const char* v = std::getenv("PD_STAGGER_NS")) plan.stagger_ns = std::atoi(v); // dev knob
-}
-
 inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
-                        const int* nbr, const int* nbr12, const double* W, const int* fail, cudaStream_t s) {
+                        const int* nbr, const double* W, const int* fail, cudaStream_t s) {
     const int blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
-#define PD_LAUNCH(ID, CFG)                                                                                           \
-    if (plan.id == ID) {                                                                                              \
-        if (plan.variant == 3)                                                                                        \
-            k_fast2<CFG, 0><<<(plan.nunits + 2 * kFastWarps - 1) / (2 * kFastWarps), 32 * kFastWarps,                \
-                              plan.smem_bytes, s>>>(p, F, out, out_mode, nbr, nbr12, W, plan.nunits, fail);        \
-        else if (plan.variant == 2)                                                                                   \
-            k_fast<CFG, 1><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail, plan.first_wave, plan.stagger_ns, plan.sms);        \
-        else if (plan.variant == 1)                                                                                   \
-            k_fast<CFG, 0><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail, plan.first_wave, plan.stagger_ns, plan.sms);        \
-        else                                                                                                          \
-            k_fast_p<CFG, 0><<<plan.grid, 32 * kFastWarps, plan.smem_bytes, s>>>(p, F, out, out_mode, nbr, nbr12, W, \
-                                                                                 plan.nunits, fail);                 \
-    }
+#define PD_LAUNCH(ID, CFG) \
+    if (plan.id == ID) k_fast<CFG><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);
     PD_FAST_CONFIGS(PD_LAUNCH)
 #undef PD_LAUNCH
 }

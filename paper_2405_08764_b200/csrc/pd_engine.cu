@@ -73,7 +73,7 @@ struct pd_engine {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     std::vector<int32_t> pij, nbr, cset;
-    DevBuf<int32_t> d_pij, d_nbr, d_nbr12, d_cset, d_kinds, d_fail;
+    DevBuf<int32_t> d_pij, d_nbr, d_cset, d_kinds, d_fail;
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
     DevBuf<unsigned long long> d_slot;
     DevBuf<unsigned int> d_counter;
@@ -99,7 +99,7 @@ struct pd_engine {
         if (mode == PD_MODE_FAST && fast.big) {
             launch_big(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
         } else if (mode == PD_MODE_FAST) {
-            launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_nbr12.p, d_weights.p, fail, stream);
+            launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
         } else {
             k_gaptooth_exact<<<prm.P, kExactThreads, exact_smem_bytes(prm), stream>>>(
                 prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail);
@@ -371,11 +371,6 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
                 e->d_weights.alloc(wcount);
                 fold_weights(e->fast, p, e->d_coeffs.p, e->d_cset.p, e->d_weights.p, e->stream);
                 e->check_launch();
-                const std::vector<int> n12 = fast_nbr12(e->fast, P, e->nbr.data());
-                e->d_nbr12.alloc(n12.size());
-                upload(e->d_nbr12.p, n12.data(), n12.size() * 4, e->stream);
-                setup_persistent(e->fast);
-                CUDA_TRY(cudaGetLastError());
                 e->device_bytes += wcount * 8;
                 e->mode = PD_MODE_FAST;
             }
