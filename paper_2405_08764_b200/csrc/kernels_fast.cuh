@@ -318,12 +318,19 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             part += (edge ? 0.5 * ox : ox) * row;
         }
     }
-    sred[lane] = part;
-    __syncwarp();
-    if (valid && r == 0) {
-        double avg = 0.0;
+    double avg = 0.0;
+    if constexpr (LP == 32) { // one patch per warp: butterfly reduction
 #pragma unroll
-        for (int q = 0; q < LP; ++q) avg += sred[g * LP + q];
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        avg = part;
+    } else { // several patches per warp: lane r == 0 of each sums its LP partials
+        sred[lane] = part;
+        __syncwarp();
+        if (r == 0)
+#pragma unroll
+            for (int q = 0; q < LP; ++q) avg += sred[g * LP + q];
+    }
+    if (valid && r == 0) {
         const size_t node = (size_t)__ldg(nbr + 9 * patch + 4);
         if (out_mode == 0) {
             out[node] = avg;

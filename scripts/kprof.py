@@ -8,6 +8,10 @@ d, _ = configs.load('c4_shear')
 which = sys.argv[1] if len(sys.argv) > 1 else 'c4'
 if which == 'k200':
     d = configs.sweep_desc(d, 16, 16, 200)
+elif which == 'c4k200':
+    d = configs.copy_desc(d, nt=200)
+elif which == 'k1':
+    d = configs.copy_desc(d, nt=1)
 elif which == 'k10':
     d = configs.sweep_desc(d, 18, 16, 10)
 P = Problem(d)
