@@ -213,9 +213,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             mine[ii] = u[ii][0];             // bottom row of the block
             mine[ROW + ii] = u[ii][BJ - 1];  // top row
         }
-#if PD_BIGX != 1
         __syncthreads();
-#endif
         // eta halos + their xi-differences from the neighbouring block rows
         const double* rs = &s_row[par][bjS][1][i0 + 2]; // top row of the block below
         const double* rn = &s_row[par][bjN][0][i0 + 2]; // bottom row of the block above
