@@ -306,11 +306,9 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
         const double ox = 1.0 / (N1 - 1), oy = 1.0 / (N2 - 1);
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
-            const int i = bi * BI + ii;
             double row = 0.0;
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) {
-                const int j = bj * BJ + jj;
                 const bool edge = (jj == 0 && bj == 0) || (jj == BJ - 1 && bj == Cfg::LJ - 1);
                 row += (edge ? 0.5 * oy : oy) * u[ii][jj];
             }

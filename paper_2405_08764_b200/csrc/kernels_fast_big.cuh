@@ -4,13 +4,15 @@
 // Same per-node algebra as kernels_fast.cuh (folded weights in registers,
 // difference form of the mixed term, per-patch ghost constant), but a patch
 // of 1024 nodes needs 128 lanes of 2x4 nodes: lane r = bj*LI + bi with LI = 16,
-// so xi-neighbours (bi +- 1) share a warp and exchange through immediate-delta
-// shuffles, while eta-neighbours cross warps every second block row.  The
-// eta halo rows therefore go through shared memory: each lane publishes its
-// block's bottom and top rows, one CTA barrier per micro-step (rows are
-// double-buffered by step parity), and reads back the row above/below over
-// columns i0-1 .. i0+2, which also yields the xi-differences e(i, j0-1) and
-// e(i, j0+BJ) of the mixed term without a second exchange.
+// so a warp holds block rows bj = 2w (lanes 0-15) and 2w+1 (lanes 16-31).
+// Odd block rows store their block MIRRORED in eta (local jj = BJ-1 is the
+// physical bottom row).  Then, for every lane, local "north" is the partner
+// half of its own warp (one SHFL.BFLY 16, no selects) and local "south" is
+// the neighbouring warp: each lane publishes its local row jj = 0 to shared
+// memory (double-buffered by step parity, one CTA barrier per micro-step) and
+// reads the partner row over columns i0-1 .. i0+2, which also yields the mixed
+// term's xi-differences there without a second exchange.  Mirroring swaps the
+// N/S weights and negates the mixed weight of odd block rows (k_fold_big).
 #pragma once
 
 #include "kernels_fast.cuh"
@@ -50,10 +52,12 @@ __global__ void k_fold_big(Params p, const double* __restrict__ coeffs, const in
         const int r = (int)(unit % Cfg::WPP) * 32 + lane;
         double val = 0.0;
         if (patch < p.P && f < Cfg::NWL) {
-            const int kind = f / Cfg::NPL, node = f % Cfg::NPL;
+            const int lkind = f / Cfg::NPL, node = f % Cfg::NPL;
             const int ii = node / Cfg::BJ, jj = node % Cfg::BJ;
             const int bi = r % Cfg::LI, bj = r / Cfg::LI;
-            const int i = bi * Cfg::BI + ii, j = bj * Cfg::BJ + jj;
+            const bool flip = bj & 1; // mirrored block row: local N/S = physical S/N
+            const int i = bi * Cfg::BI + ii, j = bj * Cfg::BJ + (flip ? Cfg::BJ - 1 - jj : jj);
+            const int kind = flip && lkind == WN ? WS : flip && lkind == WS ? WN : lkind;
             const int set = cset ? cset[patch] : (int)patch;
             const double* c = coeffs + (size_t)set * PD_NCOEF * p.N;
             const int k = i * p.n2 + j;
@@ -67,7 +71,7 @@ __global__ void k_fold_big(Params p, const double* __restrict__ coeffs, const in
                 case WW: val = Eb ? wW + wE : wW; break;
                 case WN: val = Sb ? wN + wS : wN; break;
                 case WS: val = Nb ? wS + wN : wS; break;
-                case WD: val = dt * (B * ixy); break;
+                case WD: val = flip ? -(dt * (B * ixy)) : dt * (B * ixy); break;
                 default: val = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr); break;
             }
         }
@@ -83,13 +87,14 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     constexpr int N1 = Cfg::N1, N2 = Cfg::N2, ROW = Cfg::ROW, WPP = Cfg::WPP;
     constexpr bool MIXED = Cfg::MIXED;
     __shared__ double s_g[8][Cfg::L];                   // ghost offsets + mixed ring offsets
-    __shared__ __align__(16) double s_row[2][LJ][2][ROW]; // [parity][block row][bottom, top][padded column]
+    __shared__ __align__(16) double s_row[2][LJ][ROW]; // [parity][block row][padded column]: local row jj = 0
     __shared__ double s_red[WPP];
     if (fail_flag && *fail_flag) return;
     const int patch = blockIdx.x;
     const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
     const int bi = r % LI, bj = r / LI;
     const int i0 = bi * BI, j0 = bj * BJ;
+    const bool flip = bj & 1; // mirrored block row (local jj <-> physical j0 + BJ-1-jj)
 
     // ---- loads: stencil indices first, then the weight tile ----------------
     int idx[9];
@@ -110,10 +115,11 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
 #pragma unroll
     for (int q = 0; q < 9; ++q) v[q] = __ldg(F + idx[q]);
     // zero the row pads once (columns -2, -1, N1, N1+1 are never written)
-    for (int t = r; t < 2 * LJ * 2 * 4; t += 32 * WPP) {
+    for (int t = r; t < 2 * LJ * 4; t += 32 * WPP) {
         const int pad = t & 3, rest = t >> 2;
-        (&s_row[0][0][0][0])[rest * ROW + (pad < 2 ? pad : N1 + pad)] = 0.0;
+        (&s_row[0][0][0])[rest * ROW + (pad < 2 ? pad : N1 + pad)] = 0.0;
     }
+
 
     // ---- centre derivatives, ghost offsets, ring offsets (as patch_body) ----
     const double Uxi = (v[7] - v[1]) * p.i2Dxi;
@@ -174,7 +180,11 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     }
 
     // ---- lift + boundary fold-in ------------------------------------------
+    // A physical eta edge can only be a local row jj = 0 (bj = 0 unmirrored: S;
+    // bj = LJ-1 mirrored: N); its outward weight sits in the local S slot.
     double u[BI][BJ], c[BI][BJ];
+    const bool etaEdge = bj == 0 || bj == LJ - 1;
+    const double* gEta = flip ? gN : gS;
 #pragma unroll
     for (int ii = 0; ii < BI; ++ii) {
         const int i = i0 + ii;
@@ -182,20 +192,21 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
         const double Ai = C0 + X * (Uxi + X * hUxx), Bi = Ueta + X * Uxy;
 #pragma unroll
         for (int jj = 0; jj < BJ; ++jj) {
-            const int j = j0 + jj;
+            const int j = flip ? j0 + BJ - 1 - jj : j0 + jj;
             const double Y = -0.5 * p.h_eta + p.mdeta * j;
             u[ii][jj] = Ai + Y * (Bi + Y * hUyy);
             const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
-            const bool Sb = jj == 0 && bj == 0, Nb = jj == BJ - 1 && bj == LJ - 1;
+            const bool Hb = jj == 0 && etaEdge; // physical S (unmirrored) or N (mirrored) edge
             double cc = 0.0;
             if (Wb) { cc = fma(WT(WW, ii, jj), gW[j], cc); WT(WW, ii, jj) = 0.0; }
             if (Eb) { cc = fma(WT(WE, ii, jj), gE[j], cc); WT(WE, ii, jj) = 0.0; }
-            if (Sb) { cc = fma(WT(WS, ii, jj), gS[i], cc); WT(WS, ii, jj) = 0.0; }
-            if (Nb) { cc = fma(WT(WN, ii, jj), gN[i], cc); WT(WN, ii, jj) = 0.0; }
+            if (Hb) { cc = fma(WT(WS, ii, jj), gEta[i], cc); WT(WS, ii, jj) = 0.0; }
             if constexpr (MIXED) {
-                if (Wb || Eb || Sb || Nb) {
-                    const double* dd = s_g[4 + (Wb ? PD_EDGE_W : Eb ? PD_EDGE_E : Sb ? PD_EDGE_S : PD_EDGE_N)];
-                    cc = fma(WT(WD, ii, jj), dd[(Wb || Eb) ? j : i], cc);
+                if (Wb || Eb || Hb) {
+                    // ring offsets are physical; the mirrored mixed weight carries a minus sign
+                    const double* dd = s_g[4 + (Wb ? PD_EDGE_W : Eb ? PD_EDGE_E : flip ? PD_EDGE_N : PD_EDGE_S)];
+                    const double o = dd[(Wb || Eb) ? j : i];
+                    cc = fma(WT(WD, ii, jj), flip ? -o : o, cc);
                     WT(WD, ii, jj) = 0.0;
                 }
             }
@@ -204,31 +215,27 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     }
 
     // ---- K fused micro-steps ------------------------------------------------
-    const int bjS = bj > 0 ? bj - 1 : bj, bjN = bj < LJ - 1 ? bj + 1 : bj; // patch edges read finite junk
+    // local S partner row: the neighbouring warp's block row (clamped at the
+    // patch edge, where the weights that would read it are zero)
+    const int bjX = flip ? (bj + 1 < LJ ? bj + 1 : bj) : (bj > 0 ? bj - 1 : bj);
+    double* const mine0 = &s_row[0][bj][i0 + 2];
+    const double* const rx0 = &s_row[0][bjX][i0 + 2];
     for (int step = 0; step < p.nt; ++step) {
-        const int par = step & 1;
-        double* mine = &s_row[par][bj][0][i0 + 2];
+        const int po = (step & 1) * LJ * ROW;
+        double* mine = mine0 + po;
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii) {
-            mine[ii] = u[ii][0];             // bottom row of the block
-            mine[ROW + ii] = u[ii][BJ - 1];  // top row
-        }
+        for (int ii = 0; ii < BI; ++ii) mine[ii] = u[ii][0]; // local row jj = 0
         __syncthreads();
-        // eta halos + their xi-differences from the neighbouring block rows
-        const double* rs = &s_row[par][bjS][1][i0 + 2]; // top row of the block below
-        const double* rn = &s_row[par][bjN][0][i0 + 2]; // bottom row of the block above
+        const double* rx = rx0 + po;
         double hS[BI], hN[BI], eS[BI], eN[BI];
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
-            hS[ii] = rs[ii];
-            hN[ii] = rn[ii];
+            hS[ii] = rx[ii];
+            hN[ii] = __shfl_xor_sync(0xffffffffu, u[ii][BJ - 1], 16); // partner half of this warp
         }
         if constexpr (MIXED) {
 #pragma unroll
-            for (int ii = 0; ii < BI; ++ii) {
-                eS[ii] = rs[ii + 1] - rs[ii - 1];
-                eN[ii] = rn[ii + 1] - rn[ii - 1];
-            }
+            for (int ii = 0; ii < BI; ++ii) eS[ii] = rx[ii + 1] - rx[ii - 1];
         }
         double cE[BJ], cW[BJ];
 #pragma unroll
@@ -251,25 +258,27 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WN, ii, jj), at(ii, jj + 1), nu[ii][jj]);
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WS, ii, jj), at(ii, jj - 1), nu[ii][jj]);
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
             for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WE, ii, jj), at(ii + 1, jj), nu[ii][jj]);
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WN, ii, jj), at(ii, jj + 1), nu[ii][jj]);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WS, ii, jj), at(ii, jj - 1), nu[ii][jj]);
         if constexpr (MIXED) {
             double e[BI][BJ];
 #pragma unroll
             for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
                 for (int jj = 0; jj < BJ; ++jj) e[ii][jj] = at(ii + 1, jj) - at(ii - 1, jj);
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii) eN[ii] = __shfl_xor_sync(0xffffffffu, e[ii][BJ - 1], 16);
 #pragma unroll
             for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
@@ -295,7 +304,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             double row = 0.0;
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) {
-                const bool edge = (jj == 0 && bj == 0) || (jj == BJ - 1 && bj == LJ - 1);
+                const bool edge = jj == 0 && etaEdge; // physical eta edges are local rows jj = 0
                 row += (edge ? 0.5 * oy : oy) * u[ii][jj];
             }
             const bool edge = (ii == 0 && bi == 0) || (ii == BI - 1 && bi == LI - 1);

@@ -10,6 +10,8 @@ if which == 'k200':
     d = configs.sweep_desc(d, 16, 16, 200)
 elif which == 'c4k200':
     d = configs.copy_desc(d, nt=200)
+elif which == 'big':
+    d = configs.sweep_desc(d, 16, 32, 200)
 elif which == 'k1':
     d = configs.copy_desc(d, nt=1)
 elif which == 'k10':
