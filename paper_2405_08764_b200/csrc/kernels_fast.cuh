@@ -101,6 +101,39 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
     }
 }
 
+// ---- mixed-term ring offsets ------------------------------------------------
+// For a boundary-ring node the reflected node values cancel in
+// (uNE + uSW) - (uNW + uSE) (u_ghost = u_inner + off, corner
+// ghosts carry both edges' offsets); what remains is a signed difference of
+// the node's own edge offsets plus, at the two ends of the edge, the
+// neighbouring edges' offsets.  Ring entry t: E (j = t), W, N (i), S order.
+template <int N1, int N2>
+__device__ __forceinline__ int e_of_ring(int t, int& e, int& k) {
+    const bool xi_edge = t < 2 * N2;
+    const int L = xi_edge ? N2 : N1, u = xi_edge ? t : t - 2 * N2;
+    const bool first = u < L;
+    k = first ? u : u - L;
+    e = xi_edge ? (first ? PD_EDGE_E : PD_EDGE_W) : (first ? PD_EDGE_N : PD_EDGE_S);
+    return e;
+}
+template <int N1, int N2>
+__device__ __forceinline__ double ring_offset(const double* gE, const double* gW, const double* gN, const double* gS,
+                                              int t) {
+    const bool xi_edge = t < 2 * N2;
+    const int L = xi_edge ? N2 : N1, M = xi_edge ? N1 : N2, u = xi_edge ? t : t - 2 * N2;
+    const bool first = u < L; // E or N: +, W or S: -
+    const int k = first ? u : u - L;
+    const double* ge = xi_edge ? (first ? gE : gW) : (first ? gN : gS);
+    const double* gh = xi_edge ? gN : gE; // edge crossing the k = L-1 end
+    const double* gl = xi_edge ? gS : gW; // edge crossing the k = 0 end
+    const int a = first ? M - 1 : 1, b = first ? M - 2 : 0;
+    const double d = ge[k + 1 < L ? k + 1 : L - 1] - ge[k > 0 ? k - 1 : 0];
+    double o = first ? d : -d;
+    if (k == L - 1) o += gh[a] - gh[b];
+    if (k == 0) o += gl[b] - gl[a];
+    return o;
+}
+
 // ---- per-patch body: lift, boundary fold-in, K micro-steps, restriction --
 // Everything after the weights (w, registers) and the 3x3 stencil (v) are in
 // hand; shared by the one-shot and the persistent kernels.
@@ -154,29 +187,9 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     const double* gN = sg[gs][PD_EDGE_N];
     const double* gS = sg[gs][PD_EDGE_S];
     if constexpr (MIXED) {
-        auto off = [&](int pp, int qq) {
-            const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
-            const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
-            double o = 0.0;
-            if (pp < 0) o += gW[qc];
-            if (pp > N1 - 1) o += gE[qc];
-            if (qq < 0) o += gS[pc];
-            if (qq > N2 - 1) o += gN[pc];
-            return o;
-        };
         for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
-            int e, i, j, k;
-            if (t < 2 * N2) {
-                e = t < N2 ? PD_EDGE_E : PD_EDGE_W;
-                k = j = t < N2 ? t : t - N2;
-                i = e == PD_EDGE_E ? N1 - 1 : 0;
-            } else {
-                const int u = t - 2 * N2;
-                e = u < N1 ? PD_EDGE_N : PD_EDGE_S;
-                k = i = u < N1 ? u : u - N1;
-                j = e == PD_EDGE_N ? N2 - 1 : 0;
-            }
-            sg[gs][4 + e][k] = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
+            int e, k;
+            sg[gs][4 + e_of_ring<N1, N2>(t, e, k)][k] = ring_offset<N1, N2>(gE, gW, gN, gS, t);
         }
         __syncwarp();
     }
