@@ -4,7 +4,10 @@
 // cdr_coefficients, sin(pi x) sin(pi y), homogeneous Dirichlet data), runs it
 // on the B200 and writes the final macro field (raw float64) to argv[2].
 //
-//   dropin_c1 <fast|exact> <out.bin>
+//   dropin_c1 <fast|exact> <out.bin> [linear_cache: off|auto|on]
+// The BASELINE pin is linear_cache = off (the micro-solve is the hot path);
+// the reference's own default, auto, takes GapToothEngine::step's
+// linear-response shortcut for this problem (gaptooth.cpp:213-224).
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -46,6 +49,10 @@ int main(int argc, char** argv) {
     cfg.T = cfg.Nt * (5.0 * cfg.tau);
     cfg.solver = cpi::SchemeConfig::Solver::Explicit;
     cfg.mode = std::strcmp(argv[1], "exact") == 0 ? PD_MODE_EXACT : PD_MODE_FAST;
+    const char* lc = argc > 3 ? argv[3] : "off";
+    cfg.linear_cache = std::strcmp(lc, "auto") == 0 ? cpi::SchemeConfig::LinearCache::Auto
+                       : std::strcmp(lc, "on") == 0 ? cpi::SchemeConfig::LinearCache::On
+                                                    : cpi::SchemeConfig::LinearCache::Off;
 
     try {
         const gaptooth::GapToothEngine engine(p, cfg);
@@ -53,8 +60,9 @@ int main(int argc, char** argv) {
         std::ofstream f(argv[2], std::ios::binary);
         f.write(reinterpret_cast<const char*>(res.final_field.U.data()),
                 static_cast<std::streamsize>(res.final_field.U.size() * sizeof(double)));
-        std::printf("kernel_family=%s steps=%zu max_pct_err=%.12f\n",
-                    engine.kernel_family() == PD_MODE_FAST ? "fast" : "exact", res.times.size(), res.max_pct_err);
+        std::printf("kernel_family=%s linear_cache=%d steps=%zu max_pct_err=%.12f\n",
+                    engine.kernel_family() == PD_MODE_FAST ? "fast" : "exact", int(engine.uses_linear_cache()),
+                    res.times.size(), res.max_pct_err);
     } catch (const Error& e) {
         std::fprintf(stderr, "error %d: %s\n", e.status, e.what());
         return 3;

@@ -23,6 +23,10 @@
  *                                  dirichlet_edge_values + lift
  *                                  proj/src/gaptooth.cpp:74-168
  * pd_restrict_batch                restrict_average  proj/src/gaptooth.cpp:170-194
+ * pd_evolve_batch                  evolve_patch on given stencils  gaptooth.cpp:312-353
+ * pd_linear_weights                GapToothEngine::build_row_weights  gaptooth.cpp:377-394
+ * pd_engine_set_linear /           GapToothEngine::step's linear-response path
+ *   pd_engine_set_step_kind        (linear_cache, gaptooth.cpp:213-224, 396-418)
  * pd_last_error / pd_status        typed exceptions proj/include/patchdyn/errors.hpp:9-61
  *
  * Host-side problem builder (mesh/metric setup, stays on the host as in the
@@ -212,6 +216,33 @@ pd_status pd_lift_batch(pd_engine* e, int32_t nstencils, const double* vals_host
                         const double* centers_host, double* u0_host, double* edge_slope_host,
                         double* edge_value_host);
 pd_status pd_restrict_batch(pd_engine* e, int32_t nfields, const double* u_host, double* avg_host);
+
+/* Linear-response path.  With time-independent coefficients, a zero source
+ * and one integrator per eta-row the reference's GapToothEngine::step (when
+ * SchemeConfig::linear_cache enables it, gaptooth.cpp:213-224) replaces the
+ * micro-solve by a 9-point macro stencil whose row weights are the patch
+ * responses to the 9 unit stencils (build_row_weights, gaptooth.cpp:377-394;
+ * step, :396-418).
+ * pd_evolve_batch: evolve_patch (gaptooth.cpp:312-353) of n given stencils
+ *   [n][3][3] (vals[p+1][q+1]) with the integrator and centre of patch
+ *   patch_index[m]; out[m] = the restricted average.  EXACT arithmetic (bit-
+ *   identical to the reference), whatever the engine's kernel family.
+ * pd_linear_weights: row_w [Neta+1][3][3] (rows 0 and Neta zero) built like
+ *   build_row_weights from row j's patch (i0, j), i0 = periodic ? 0 : 1.
+ *   PD_VALIDATION_ERROR (the reference's message) when ineligible.
+ * pd_engine_set_linear: upload row weights (NULL drops them).
+ * pd_engine_set_step_kind: PD_STEP_DIRECT (micro-solve, the default) or
+ *   PD_STEP_LINEAR; every step entry point (pd_gaptooth_step,
+ *   pd_projective_step[_device], pd_run[_device], pd_bench_step_kernel) then
+ *   uses that step.  The linear step accumulates in the reference's order and
+ *   is bit-identical to GapToothEngine::step's fast path. */
+enum { PD_STEP_DIRECT = 0, PD_STEP_LINEAR = 1 };
+pd_status pd_evolve_batch(pd_engine* e, int32_t n, const int32_t* patch_index, const double* stencils_host,
+                          double t, double* out_host);
+pd_status pd_linear_weights(pd_engine* e, double* row_w_host);
+pd_status pd_engine_set_linear(pd_engine* e, const double* row_w_host);
+pd_status pd_engine_set_step_kind(pd_engine* e, int32_t kind);
+int32_t pd_engine_step_kind(const pd_engine* e);
 
 /* ---------------------------------------------------------------------------
  * Host problem builder: the B200 framework's own mesh/metric setup for the

@@ -354,6 +354,7 @@ typedef struct {
     int* pij;        /* [P][2] */
     const int* cset; /* [P] or NULL */
     int n1, n2, L;
+    const double* row_w; /* [Neta+1][9] linear-response weights, or NULL = direct path */
 } eng_t;
 
 static int eng_init(eng_t* e, const pd_engine_desc* d) {
@@ -362,6 +363,7 @@ static int eng_init(eng_t* e, const pd_engine_desc* d) {
     e->n2 = d->ny + 1;
     e->L = e->n1 > e->n2 ? e->n1 : e->n2;
     e->cset = d->coeff_set;
+    e->row_w = NULL;
     if (d->patch_ij) {
         e->P = d->npatches;
         e->pij = (int*)malloc(sizeof(int) * 2 * e->P);
@@ -404,8 +406,10 @@ static void refresh(const pd_engine_desc* d, double* U, const double* bnd) {
 }
 
 /* one patch: build_stencil + evolve_patch  gaptooth.cpp:74-104, 312-353 */
-static int evolve_patch(const eng_t* e, const double* F, int p, double t, const double* src_time,
-                        double* work, double* avg) {
+/* vals != NULL: evolve the given 3x3 values with patch p's integrator and
+ * centre instead of gathering them from F (build_row_weights, gaptooth.cpp:377-394). */
+static int evolve_patch_vals(const eng_t* e, const double* vals, const double* F, int p, double t,
+                             const double* src_time, double* work, double* avg) {
     const pd_engine_desc* d = e->d;
     const int i = e->pij[2 * p], j = e->pij[2 * p + 1];
     const int n1 = e->n1, n2 = e->n2, L = e->L, N = n1 * n2, NF2 = d->Neta + 1;
@@ -422,12 +426,13 @@ static int evolve_patch(const eng_t* e, const double* F, int p, double t, const 
         s.xi_c = d->a + s.dxi * iw;
         for (int pp = -1; pp <= 1; ++pp) {
             const int ip = ((iw + pp) % d->Nxi + d->Nxi) % d->Nxi;
-            for (int q = -1; q <= 1; ++q) s.v[pp + 1][q + 1] = F[ip * NF2 + j + q];
+            for (int q = -1; q <= 1; ++q) s.v[pp + 1][q + 1] = vals ? vals[3 * (pp + 1) + q + 1] : F[ip * NF2 + j + q];
         }
     } else {
         s.xi_c = d->a + s.dxi * i;
         for (int pp = -1; pp <= 1; ++pp)
-            for (int q = -1; q <= 1; ++q) s.v[pp + 1][q + 1] = F[(i + pp) * NF2 + j + q];
+            for (int q = -1; q <= 1; ++q)
+                s.v[pp + 1][q + 1] = vals ? vals[3 * (pp + 1) + q + 1] : F[(i + pp) * NF2 + j + q];
     }
     double* u = work;
     double* slopes = work + N;
@@ -455,11 +460,42 @@ static int evolve_patch(const eng_t* e, const double* F, int p, double t, const 
     return PD_OK;
 }
 
+static int evolve_patch(const eng_t* e, const double* F, int p, double t, const double* src_time,
+                        double* work, double* avg) {
+    return evolve_patch_vals(e, NULL, F, p, t, src_time, work, avg);
+}
+
 static size_t work_len(const eng_t* e) { return (size_t)e->n1 * e->n2 + 8 * e->L; }
+
+/* GapToothEngine::step, linear-response path  gaptooth.cpp:396-418 */
+static void linear_step(const eng_t* e, const double* F, double* out, const double* bnd) {
+    const pd_engine_desc* d = e->d;
+    const int N1 = d->Nxi, NF2 = d->Neta + 1;
+    const size_t NF = (size_t)(N1 + 1) * NF2;
+    memcpy(out, F, sizeof(double) * NF);
+    const int i_lo = d->periodic_xi ? 0 : 1, i_hi = N1 - 1;
+    for (int j = 1; j <= d->Neta - 1; ++j) {
+        const double* w = e->row_w + 9 * j;
+        for (int i = i_lo; i <= i_hi; ++i) {
+            double acc = 0.0;
+            for (int p = -1; p <= 1; ++p) {
+                int ip = i + p;
+                if (d->periodic_xi) ip = ((ip % N1) + N1) % N1;
+                for (int q = -1; q <= 1; ++q) acc += w[3 * (p + 1) + q + 1] * F[ip * NF2 + j + q];
+            }
+            out[i * NF2 + j] = acc;
+        }
+    }
+    refresh(d, out, bnd);
+}
 
 static int step_direct(const eng_t* e, const double* F, double* out, double t, const double* bnd,
                        const double* src_time) {
     const pd_engine_desc* d = e->d;
+    if (e->row_w) {
+        linear_step(e, F, out, bnd);
+        return PD_OK;
+    }
     const size_t NF = (size_t)(d->Nxi + 1) * (d->Neta + 1);
     memcpy(out, F, sizeof(double) * NF); /* CoarseField out = F  gaptooth.cpp:361 */
     int status = PD_OK;
@@ -533,10 +569,21 @@ int pdo_projective_step(const pd_engine_desc* d, const double* U_in, double* U_o
 
 /* cpi::run's macro loop with the blow-up guard  cpi.cpp:142-202.  U must hold
  * the initial field with its boundary already refreshed at t0. */
+static int run_impl(const pd_engine_desc* d, const double* row_w, double* U, int nsteps, double t0,
+                    const double* bnd, const double* src_time, pd_run_stats* stats);
 int pdo_run(const pd_engine_desc* d, double* U, int nsteps, double t0, const double* bnd,
             const double* src_time, pd_run_stats* stats) {
+    return run_impl(d, NULL, U, nsteps, t0, bnd, src_time, stats);
+}
+int pdo_linear_run(const pd_engine_desc* d, const double* row_w, double* U, int nsteps, double t0,
+                   const double* bnd, pd_run_stats* stats) {
+    return run_impl(d, row_w, U, nsteps, t0, bnd, NULL, stats);
+}
+static int run_impl(const pd_engine_desc* d, const double* row_w, double* U, int nsteps, double t0,
+                    const double* bnd, const double* src_time, pd_run_stats* stats) {
     eng_t e;
     eng_init(&e, d);
+    e.row_w = row_w;
     const size_t NF = (size_t)(d->Nxi + 1) * (d->Neta + 1), perim = perim_len(d->Nxi, d->Neta);
     double scale0 = 0.0;
     for (size_t q = 0; q < NF; ++q) scale0 = fmax(scale0, fabs(U[q]));
@@ -601,4 +648,78 @@ double pdo_patch_subset(const pd_engine_desc* d, const double* U_in, double t, i
     const double dt = now_s() - t0;
     eng_free(&e);
     return bad ? -dt : dt;
+}
+
+/* ---- linear-response path  gaptooth.cpp:377-418 --------------------------- */
+
+int pdo_evolve_batch(const pd_engine_desc* d, int n, const int* patch_index, const double* stencils, double t,
+                     double* out) {
+    eng_t e;
+    eng_init(&e, d);
+    int status = PD_OK;
+    double* work = (double*)malloc(sizeof(double) * work_len(&e));
+    for (int m = 0; m < n && status == PD_OK; ++m) {
+        if (patch_index[m] < 0 || patch_index[m] >= e.P) {
+            snprintf(g_err, sizeof g_err, "patch index %d outside [0,%d)", patch_index[m], e.P);
+            status = PD_INDEX_OUT_OF_RANGE;
+            break;
+        }
+        status = evolve_patch_vals(&e, stencils + 9 * (size_t)m, NULL, patch_index[m], t, NULL, work, &out[m]);
+    }
+    free(work);
+    eng_free(&e);
+    return status;
+}
+
+/* build_row_weights: the 9 unit-impulse responses of row j's integrator,
+ * centred at (xi(i0), eta(j)), i0 = periodic ? 0 : 1; row_w [Neta+1][9]
+ * (rows 0 and Neta left zero). */
+int pdo_linear_weights(const pd_engine_desc* d, double* row_w) {
+    eng_t e;
+    eng_init(&e, d);
+    const int i0 = d->periodic_xi ? 0 : 1;
+    memset(row_w, 0, sizeof(double) * 9 * (d->Neta + 1));
+    int status = PD_OK;
+    double* work = (double*)malloc(sizeof(double) * work_len(&e));
+    for (int j = 1; j <= d->Neta - 1 && status == PD_OK; ++j) {
+        int p = -1;
+        for (int q = 0; q < e.P; ++q)
+            if (e.pij[2 * q] == i0 && e.pij[2 * q + 1] == j) {
+                p = q;
+                break;
+            }
+        if (p < 0) {
+            snprintf(g_err, sizeof g_err, "row %d has no patch at i = %d", j, i0);
+            status = PD_VALIDATION_ERROR;
+            break;
+        }
+        for (int k = 0; k < 9 && status == PD_OK; ++k) {
+            double vals[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            vals[k] = 1.0;
+            status = evolve_patch_vals(&e, vals, NULL, p, 0.0, NULL, work, &row_w[9 * j + k]);
+        }
+    }
+    free(work);
+    eng_free(&e);
+    return status;
+}
+
+int pdo_linear_step(const pd_engine_desc* d, const double* row_w, const double* U_in, double* U_out,
+                    const double* bnd) {
+    eng_t e;
+    eng_init(&e, d);
+    e.row_w = row_w;
+    linear_step(&e, U_in, U_out, bnd);
+    eng_free(&e);
+    return PD_OK;
+}
+
+int pdo_linear_projective_step(const pd_engine_desc* d, const double* row_w, const double* U_in, double* U_out,
+                               double t, const double* bnd) {
+    eng_t e;
+    eng_init(&e, d);
+    e.row_w = row_w;
+    const int st = projective(&e, U_in, U_out, t, bnd, NULL);
+    eng_free(&e);
+    return st;
 }

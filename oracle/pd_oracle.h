@@ -58,6 +58,21 @@ int pdo_run(const pd_engine_desc* d, double* U, int nsteps, double t0, const dou
 double pdo_patch_subset(const pd_engine_desc* d, const double* U_in, double t, int nsub,
                         const int* patch_index, double* avg_out);
 
+/* Linear-response path (GapToothEngine::step with linear_cache, gaptooth.cpp:377-418).
+ * evolve_batch: evolve_patch for n given stencils [n][3][3] (vals[p+1][q+1]) with patch
+ * patch_index[m]'s integrator and centre.  linear_weights: build_row_weights,
+ * row_w [Neta+1][9].  linear_step / _projective_step / _run: the 9-point macro
+ * stencil with the row weights in place of the micro-solve. */
+int pdo_evolve_batch(const pd_engine_desc* d, int n, const int* patch_index, const double* stencils, double t,
+                     double* out);
+int pdo_linear_weights(const pd_engine_desc* d, double* row_w);
+int pdo_linear_step(const pd_engine_desc* d, const double* row_w, const double* U_in, double* U_out,
+                    const double* bnd);
+int pdo_linear_projective_step(const pd_engine_desc* d, const double* row_w, const double* U_in, double* U_out,
+                               double t, const double* bnd);
+int pdo_linear_run(const pd_engine_desc* d, const double* row_w, double* U, int nsteps, double t0,
+                   const double* bnd, pd_run_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,11 @@ class Restated:
         L.pdo_run.argtypes = [desc_p, _dp, C.c_int, C.c_double, _dp, _dp, C.POINTER(RunStats)]
         L.pdo_patch_subset.argtypes = [desc_p, _dp, C.c_double, C.c_int, _ip, _dp]
         L.pdo_patch_subset.restype = C.c_double
+        L.pdo_evolve_batch.argtypes = [desc_p, C.c_int, _ip, _dp, C.c_double, _dp]
+        L.pdo_linear_weights.argtypes = [desc_p, _dp]
+        L.pdo_linear_step.argtypes = [desc_p, _dp, _dp, _dp, _dp]
+        L.pdo_linear_projective_step.argtypes = [desc_p, _dp, _dp, _dp, C.c_double, _dp]
+        L.pdo_linear_run.argtypes = [desc_p, _dp, _dp, C.c_int, C.c_double, _dp, C.POINTER(RunStats)]
         if threads is not None:
             L.pdo_set_threads(int(threads))
 
@@ -118,6 +123,40 @@ class Restated:
         r = self.lib.pdo_run(C.byref(desc), _d(U), nsteps, t0, _d(bnd), _d(src_time), C.byref(stats))
         return r, U, stats
 
+    # linear-response path  gaptooth.cpp:377-418
+    def evolve_batch(self, desc: EngineDesc, patch_index, stencils, t=0.0):
+        idx = np.ascontiguousarray(patch_index, dtype=np.int32)
+        st = np.ascontiguousarray(stencils, dtype=np.float64).reshape(len(idx), 9)
+        out = np.empty(len(idx))
+        r = self.lib.pdo_evolve_batch(C.byref(desc), len(idx), _i(idx), _d(st), t, _d(out))
+        return r, out
+
+    def linear_weights(self, desc: EngineDesc):
+        w = np.zeros((desc.Neta + 1, 3, 3))
+        r = self.lib.pdo_linear_weights(C.byref(desc), _d(w))
+        return r, w
+
+    def linear_step(self, desc: EngineDesc, row_w, U, bnd=None):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        w = np.ascontiguousarray(row_w, dtype=np.float64)
+        out = np.empty_like(U)
+        r = self.lib.pdo_linear_step(C.byref(desc), _d(w), _d(U), _d(out), _d(bnd))
+        return r, out
+
+    def linear_projective_step(self, desc: EngineDesc, row_w, U, t, bnd=None):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        w = np.ascontiguousarray(row_w, dtype=np.float64)
+        out = np.empty_like(U)
+        r = self.lib.pdo_linear_projective_step(C.byref(desc), _d(w), _d(U), _d(out), t, _d(bnd))
+        return r, out
+
+    def linear_run(self, desc: EngineDesc, row_w, U0, nsteps, t0=0.0, bnd=None):
+        U = np.array(U0, dtype=np.float64, copy=True, order="C")
+        w = np.ascontiguousarray(row_w, dtype=np.float64)
+        stats = RunStats()
+        r = self.lib.pdo_linear_run(C.byref(desc), _d(w), _d(U), nsteps, t0, _d(bnd), C.byref(stats))
+        return r, U, stats
+
     def patch_subset(self, desc: EngineDesc, U, t, patch_index):
         U = np.ascontiguousarray(U, dtype=np.float64)
         idx = np.ascontiguousarray(patch_index, dtype=np.int32)
@@ -144,6 +183,8 @@ class Reference:
         pd = C.POINTER(ProblemDesc)
         vp = C.c_void_p
         L.ref_engine_create.argtypes = [pd, C.POINTER(vp)]
+        L.ref_engine_create_lc.argtypes = [pd, C.c_int, C.POINTER(vp)]
+        L.ref_step.argtypes = [vp, _dp, _dp, C.c_double]
         L.ref_engine_destroy.argtypes = [vp]
         L.ref_initial_field.argtypes = [vp, _dp]
         L.ref_refresh_boundary.argtypes = [vp, _dp, C.c_double]
@@ -175,8 +216,9 @@ class Reference:
             raise RuntimeError(f"reference sample_coeffs_desc: {r}: {self.error()}")
         return out
 
-    def engine(self, pdesc: ProblemDesc) -> "RefEngine":
-        return RefEngine(self, pdesc)
+    def engine(self, pdesc: ProblemDesc, linear_cache: str = "off") -> "RefEngine":
+        """linear_cache: 'off' (the BASELINE pin, B3), 'auto' (the reference's default) or 'on'."""
+        return RefEngine(self, pdesc, linear_cache)
 
     def integrate(self, coef5, nx, ny, nt, h_xi, h_eta, tau, xi_c, eta_c, kinds, values, slopes,
                   robin_w, u0, t0=0.0, coef_table=None):
@@ -207,12 +249,14 @@ class Reference:
 
 
 class RefEngine:
-    def __init__(self, ref: Reference, pdesc: ProblemDesc):
+    LINEAR_CACHE = {"auto": 0, "on": 1, "off": 2}
+
+    def __init__(self, ref: Reference, pdesc: ProblemDesc, linear_cache: str = "off"):
         self.ref = ref
         self.L = ref.lib
         self.h = C.c_void_p()
         self.pdesc = pdesc
-        r = self.L.ref_engine_create(C.byref(pdesc), C.byref(self.h))
+        r = self.L.ref_engine_create_lc(C.byref(pdesc), self.LINEAR_CACHE[linear_cache], C.byref(self.h))
         if r != 0:
             raise RuntimeError(f"reference engine: status {r}: {ref.error()}")
         self.shape = (pdesc.N_xi + 1, pdesc.N_eta + 1)
@@ -238,6 +282,15 @@ class RefEngine:
         r = self.L.ref_step_direct(self.h, _d(U), _d(out), t)
         if r:
             raise RuntimeError(f"reference step_direct: {r}: {self.ref.error()}")
+        return out
+
+    def step(self, U, t):
+        """GapToothEngine::step: the linear-response path when the engine enabled it."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty_like(U)
+        r = self.L.ref_step(self.h, _d(U), _d(out), t)
+        if r:
+            raise RuntimeError(f"reference step: {r}: {self.ref.error()}")
         return out
 
     def projective_step(self, U, t):

@@ -73,6 +73,22 @@ int ref_engine_create(const pd_problem_desc* d, void** out) {
     }
 }
 
+// linear_cache: 0 Auto, 1 On, 2 Off (SchemeConfig::LinearCache, scheme_config.hpp:30-31)
+int ref_engine_create_lc(const pd_problem_desc* d, int linear_cache, void** out) {
+    try {
+        auto r = std::make_unique<RefEngine>();
+        r->built = refshim::build(*d);
+        r->built.cfg.linear_cache = linear_cache == 0   ? cpi::SchemeConfig::LinearCache::Auto
+                                    : linear_cache == 1 ? cpi::SchemeConfig::LinearCache::On
+                                                        : cpi::SchemeConfig::LinearCache::Off;
+        r->eng = std::make_unique<gaptooth::GapToothEngine>(r->built.spec, r->built.cfg);
+        *out = r.release();
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exception(e);
+    }
+}
+
 void ref_engine_destroy(void* h) { delete static_cast<RefEngine*>(h); }
 
 int ref_initial_field(void* h, double* U) {
@@ -96,6 +112,19 @@ int ref_step_direct(void* h, const double* Uin, double* Uout, double t) {
     try {
         const gaptooth::CoarseField F = field_from(*r, Uin);
         const gaptooth::CoarseField G = r->eng->step_direct(F, t);
+        std::memcpy(Uout, G.U.data(), G.U.size() * sizeof(double));
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exception(e);
+    }
+}
+
+// GapToothEngine::step (linear-response path when the engine enabled it)
+int ref_step(void* h, const double* Uin, double* Uout, double t) {
+    auto* r = static_cast<RefEngine*>(h);
+    try {
+        const gaptooth::CoarseField F = field_from(*r, Uin);
+        const gaptooth::CoarseField G = r->eng->step(F, t);
         std::memcpy(Uout, G.U.data(), G.U.size() * sizeof(double));
         return 0;
     } catch (const std::exception& e) {

@@ -32,6 +32,7 @@ PD_EDGE_E, PD_EDGE_W, PD_EDGE_N, PD_EDGE_S = 0, 1, 2, 3
 PD_QUAD_TRAPEZOID, PD_QUAD_SIMPSON = 0, 1
 PD_SOURCE_ZERO, PD_SOURCE_SEPARABLE = 0, 1
 PD_MODE_FAST, PD_MODE_EXACT = 0, 1
+PD_STEP_DIRECT, PD_STEP_LINEAR = 0, 1
 PD_COEF_A, PD_COEF_B, PD_COEF_C, PD_COEF_VX, PD_COEF_VY, PD_COEF_W = 0, 1, 2, 3, 4, 5
 PD_NCOEF = 6
 

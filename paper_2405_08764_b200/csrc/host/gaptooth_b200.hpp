@@ -77,6 +77,20 @@ public:
         grid_ = CoarseGrid{problem.a, problem.b, problem.c, problem.d, cfg.N_xi, cfg.N_eta};
         tables_ = build_tables(problem_, cfg_, host_threads);
         check_stability(tables_, cfg_);
+        // linear_cache  gaptooth.cpp:213-224
+        const bool linear_eligible =
+            problem.coeffs_time_independent && problem.source_zero && problem.coeffs_xi_independent;
+        switch (cfg.linear_cache) {
+            case cpi::SchemeConfig::LinearCache::Off: use_fast_ = false; break;
+            case cpi::SchemeConfig::LinearCache::Auto: use_fast_ = linear_eligible; break;
+            case cpi::SchemeConfig::LinearCache::On:
+                if (!linear_eligible)
+                    throw ValidationError(
+                        "linear_cache=on requires time-independent coefficients, a zero source and "
+                        "xi-independent coefficients");
+                use_fast_ = true;
+                break;
+        }
         pd_engine* e = nullptr;
         throw_status(pd_engine_create(&tables_.desc, &e), nullptr);
         eng_.reset(e);
@@ -108,11 +122,35 @@ public:
         }
     }
 
-    // One gap-tooth step t -> t+tau (the direct path; there is no cached
-    // linear-response shortcut on the device, so step == step_direct).
-    CoarseField step(const CoarseField& F, double t) const { return step_direct(F, t); }
+    // One gap-tooth step t -> t+tau (gaptooth.cpp:396-418): the linear-response
+    // 9-point stencil when linear_cache enabled it (row weights built lazily on
+    // the device, as build_row_weights does on first use), else step_direct.
+    CoarseField step(const CoarseField& F, double t) const {
+        if (!use_fast_) return step_direct(F, t);
+        select_step(true);
+        return device_step(F, t);
+    }
 
     CoarseField step_direct(const CoarseField& F, double t) const {
+        select_step(false);
+        return device_step(F, t);
+    }
+
+    bool uses_linear_cache() const { return use_fast_; }
+    // make the device engine's step the one GapToothEngine::step would take
+    void select_step(bool linear) const {
+        if (linear && !weights_ready_) {
+            std::vector<double> w(9 * static_cast<size_t>(grid_.Neta + 1));
+            throw_status(pd_linear_weights(eng_.get(), w.data()), eng_.get());
+            throw_status(pd_engine_set_linear(eng_.get(), w.data()), eng_.get());
+            weights_ready_ = true;
+        }
+        throw_status(pd_engine_set_step_kind(eng_.get(), linear ? PD_STEP_LINEAR : PD_STEP_DIRECT), eng_.get());
+    }
+    void select_default_step() const { select_step(use_fast_); }
+
+private:
+    CoarseField device_step(const CoarseField& F, double t) const {
         CoarseField out{grid_, F.periodic, Field2D(F.U.n1(), F.U.n2())};
         const std::vector<double> bnd = perimeter(t + cfg_.tau);
         const std::vector<double> src = source_factors(t, 0);
@@ -122,6 +160,7 @@ public:
         return out;
     }
 
+public:
     const CoarseGrid& grid() const { return grid_; }
     const cpi::SchemeConfig& config() const { return cfg_; }
     const problems::ProblemSpec& problem() const { return problem_; }
@@ -164,6 +203,8 @@ private:
     CoarseGrid grid_;
     EngineTables tables_;
     std::unique_ptr<pd_engine, EngineDeleter> eng_;
+    bool use_fast_ = false;
+    mutable bool weights_ready_ = false;
 };
 
 } // namespace gaptooth
@@ -183,6 +224,7 @@ inline gaptooth::CoarseField projective_step(const gaptooth::GapToothEngine& eng
     bnd.insert(bnd.end(), last.begin(), last.end());
     const std::vector<double> src = engine.source_factors(t, cfg.k);
     gaptooth::CoarseField out{U.grid, U.periodic, Field2D(U.U.n1(), U.U.n2())};
+    engine.select_default_step(); // cpi.cpp:65 calls engine.step
     throw_status(pd_projective_step(engine.device(), U.U.data(), out.U.data(), t, bnd.data(),
                                     src.empty() ? nullptr : src.data()),
                  engine.device());
@@ -271,6 +313,7 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
         }
         (void)L;
         pd_run_stats st{};
+        engine.select_default_step(); // projective_step -> engine.step  cpi.cpp:65
         const int rc = pd_run(engine.device(), U.U.data(), m, n * dt, bnd.data(), src.empty() ? nullptr : src.data(),
                               &st);
         if (rc == PD_MACRO_INSTABILITY) {

@@ -277,6 +277,7 @@ SchemeConfig scheme_from_desc(const pd_problem_desc& d) {
     s.quadrature = d.quadrature == PD_QUAD_SIMPSON ? SchemeConfig::Quadrature::Simpson
                                                    : SchemeConfig::Quadrature::Trapezoid;
     s.mode = d.mode;
+    s.linear_cache = SchemeConfig::LinearCache::Off; // BASELINE pin: the micro-solve is the hot path
     return s;
 }
 } // namespace cpi

@@ -82,6 +82,10 @@ struct SchemeConfig {
     double robin_w1 = 1.0, robin_w2 = 1.0;
     enum class Quadrature { Trapezoid, Simpson };
     Quadrature quadrature = Quadrature::Trapezoid;
+    // linear-response shortcut of GapToothEngine::step (scheme_config.hpp:30-31);
+    // the reference's default is Auto, the BASELINE configs pin Off
+    enum class LinearCache { Auto, On, Off };
+    LinearCache linear_cache = LinearCache::Auto;
     int mode = PD_MODE_FAST;
     double dt() const { return T / Nt; }
     // SchemeConfig::validate  proj/src/cpi.cpp:11-44

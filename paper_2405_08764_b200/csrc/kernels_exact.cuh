@@ -76,10 +76,15 @@ __global__ void __launch_bounds__(kExactThreads)
 k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
                  const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
                  const double* __restrict__ src_sp, const double* __restrict__ src_time,
-                 const int* __restrict__ fail_flag) {
+                 const int* __restrict__ fail_flag, const double* __restrict__ stencil_in = nullptr,
+                 const int* __restrict__ item_patch = nullptr) {
     extern __shared__ double sm[];
     if (fail_flag && *fail_flag) return;
-    const int patch = blockIdx.x;
+    // item_patch != NULL: evolve_patch of given 3x3 values (stencil_in [items][9])
+    // with patch item_patch[item]'s integrator and centre (build_row_weights,
+    // gaptooth.cpp:377-394); the average goes to out[item].
+    const int item = blockIdx.x;
+    const int patch = item_patch ? item_patch[item] : item;
     PatchSh s = carve(sm, p.N, p.L, p.n1);
     const int i = pij[2 * patch], j = pij[2 * patch + 1];
     int ic = i;
@@ -87,7 +92,8 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
     if (threadIdx.x < 9) {
         const int dp = threadIdx.x / 3 - 1, dq = threadIdx.x % 3 - 1;
         const int ip = p.periodic ? ((ic + dp) % p.Nxi + p.Nxi) % p.Nxi : i + dp;
-        s.stencil[threadIdx.x] = F[(size_t)ip * p.NF2 + j + dq];
+        s.stencil[threadIdx.x] = stencil_in ? stencil_in[(size_t)9 * item + threadIdx.x]
+                                            : F[(size_t)ip * p.NF2 + j + dq];
     }
     const double xi_c = XADD(p.a, XMUL(p.Dxi, (double)ic));
     const double eta_c = XADD(p.c, XMUL(p.Deta, (double)j));
@@ -119,8 +125,38 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
             const double Fd = XDIV(XSUB(avg, U), p.tau); // estimate_derivative  cpi.cpp:54
             out[node] = XADD(U, XMUL(p.dt_macro, Fd));  // cpi.cpp:74 with k = 0
         } else {
-            out[patch] = avg;
+            out[item] = avg;
         }
+    }
+}
+
+// GapToothEngine::step, linear-response path (gaptooth.cpp:396-418): every
+// patch value is the 9-point macro stencil with its row's impulse-response
+// weights, accumulated in the reference's order (p outer, q inner, IEEE
+// add/mul, no contraction).  out_mode as k_gaptooth_exact (FIELD / PROJECTIVE).
+__global__ void k_linear_step(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
+                              const int* __restrict__ pij, const double* __restrict__ row_w,
+                              const int* __restrict__ fail_flag) {
+    if (fail_flag && *fail_flag) return;
+    const int patch = blockIdx.x * blockDim.x + threadIdx.x;
+    if (patch >= p.P) return;
+    const int i = pij[2 * patch], j = pij[2 * patch + 1];
+    const double* w = row_w + (size_t)9 * j;
+    double acc = 0.0;
+#pragma unroll
+    for (int dp = -1; dp <= 1; ++dp) {
+        int ip = i + dp;
+        if (p.periodic) ip = ((ip % p.Nxi) + p.Nxi) % p.Nxi;
+#pragma unroll
+        for (int dq = -1; dq <= 1; ++dq)
+            acc = XADD(acc, XMUL(w[3 * (dp + 1) + dq + 1], F[(size_t)ip * p.NF2 + j + dq]));
+    }
+    const size_t node = (size_t)i * p.NF2 + j;
+    if (out_mode == OUT_PROJECTIVE) {
+        const double U = F[node];
+        out[node] = XADD(U, XMUL(p.dt_macro, XDIV(XSUB(acc, U), p.tau))); // cpi.cpp:54, 74 (k = 0)
+    } else {
+        out[node] = acc;
     }
 }
 

@@ -73,8 +73,10 @@ struct pd_engine {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     std::vector<int32_t> pij, nbr, cset;
-    DevBuf<int32_t> d_pij, d_nbr, d_cset, d_kinds, d_fail;
+    DevBuf<int32_t> d_pij, d_nbr, d_cset, d_kinds, d_fail, d_cset_items;
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
+    DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
+    int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     DevBuf<unsigned long long> d_slot;
     DevBuf<unsigned int> d_counter;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -96,7 +98,9 @@ struct pd_engine {
 
     // ---- one gap-tooth substep F -> out (patch nodes) -------------------
     void launch_step(const double* F, double* out, int out_mode, const double* srct, const int* fail) {
-        if (mode == PD_MODE_FAST && fast.big) {
+        if (step_kind == PD_STEP_LINEAR) {
+            k_linear_step<<<(prm.P + 127) / 128, 128, 0, stream>>>(prm, F, out, out_mode, d_pij.p, d_roww.p, fail);
+        } else if (mode == PD_MODE_FAST && fast.big) {
             launch_big(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
         } else if (mode == PD_MODE_FAST) {
             launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
@@ -651,6 +655,105 @@ pd_status pd_restrict_batch(pd_engine* e, int32_t n, const double* u, double* av
         CUDA_TRY(cudaStreamSynchronize(e->stream));
     });
 }
+
+// ---- linear-response path (GapToothEngine::step, gaptooth.cpp:377-418) ------
+pd_status pd_evolve_batch(pd_engine* e, int32_t n, const int32_t* patch_index, const double* stencils,
+                          double t, double* out) {
+    if (!e || n < 1 || !patch_index || !stencils || !out) return PD_VALIDATION_ERROR;
+    for (int32_t m = 0; m < n; ++m)
+        if (patch_index[m] < 0 || patch_index[m] >= e->prm.P) {
+            e->err = "pd_evolve_batch: patch index " + std::to_string(patch_index[m]) + " outside [0," +
+                     std::to_string(e->prm.P) + ")";
+            return PD_INDEX_OUT_OF_RANGE;
+        }
+    if (e->d.source_kind != PD_SOURCE_ZERO) {
+        e->err = "pd_evolve_batch: needs a zero source";
+        return PD_UNSUPPORTED;
+    }
+    (void)t; // zero source: evolve_patch does not depend on t
+    return guarded(e, [&] {
+        const Params& p = e->prm;
+        e->d_tmp2.alloc((size_t)10 * n);
+        e->d_cset_items.alloc((size_t)n);
+        upload(e->d_tmp2.p, stencils, (size_t)9 * n * 8, e->stream);
+        upload(e->d_cset_items.p, patch_index, (size_t)n * 4, e->stream);
+        double* res = e->d_tmp2.p + (size_t)9 * n;
+        k_gaptooth_exact<<<n, kExactThreads, exact_smem_bytes(p), e->stream>>>(
+            p, nullptr, res, OUT_PATCH, e->d_pij.p, e->d_cset.p, e->d_coeffs.p, nullptr, nullptr, nullptr,
+            e->d_tmp2.p, e->d_cset_items.p);
+        e->check_launch();
+        download(out, res, (size_t)n * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+
+pd_status pd_linear_weights(pd_engine* e, double* row_w) {
+    if (!e || !row_w) return PD_VALIDATION_ERROR;
+    const pd_engine_desc& d = e->d;
+    const int Neta = d.Neta, i0 = d.periodic_xi ? 0 : 1;
+    // eligibility as GapToothEngine's ctor (gaptooth.cpp:213-224): time-independent
+    // coefficients (always, tables), zero source, one coefficient set per eta-row
+    std::vector<int32_t> rowp(Neta + 1, -1), rowset(Neta + 1, -1);
+    bool xi_indep = true;
+    for (int32_t q = 0; q < e->prm.P; ++q) {
+        const int i = e->pij[2 * q], j = e->pij[2 * q + 1];
+        const int set = e->cset.empty() ? q : e->cset[q];
+        if (rowset[j] < 0) rowset[j] = set;
+        else if (rowset[j] != set) xi_indep = false;
+        if (i == i0 && rowp[j] < 0) rowp[j] = q;
+    }
+    if (d.source_kind != PD_SOURCE_ZERO || !xi_indep) {
+        e->err = "linear_cache=on requires time-independent coefficients, a zero source and "
+                 "xi-independent coefficients";
+        return PD_VALIDATION_ERROR;
+    }
+    std::vector<int32_t> items;
+    std::vector<double> st;
+    for (int j = 1; j <= Neta - 1; ++j) {
+        if (rowp[j] < 0) {
+            e->err = "pd_linear_weights: row " + std::to_string(j) + " has no patch at i = " + std::to_string(i0);
+            return PD_VALIDATION_ERROR;
+        }
+        for (int k = 0; k < 9; ++k) {
+            items.push_back(rowp[j]);
+            for (int q = 0; q < 9; ++q) st.push_back(q == k ? 1.0 : 0.0);
+        }
+    }
+    std::vector<double> res(items.size());
+    const pd_status s = pd_evolve_batch(e, (int32_t)items.size(), items.data(), st.data(), 0.0, res.data());
+    if (s != PD_OK) return s;
+    std::fill(row_w, row_w + (size_t)9 * (Neta + 1), 0.0);
+    for (int j = 1; j <= Neta - 1; ++j)
+        for (int k = 0; k < 9; ++k) row_w[(size_t)9 * j + k] = res[(size_t)9 * (j - 1) + k];
+    return PD_OK;
+}
+
+pd_status pd_engine_set_linear(pd_engine* e, const double* row_w) {
+    if (!e) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        if (!row_w) {
+            e->d_roww.free();
+            e->step_kind = PD_STEP_DIRECT;
+            return;
+        }
+        const size_t n = (size_t)9 * (e->d.Neta + 1);
+        e->d_roww.alloc(n);
+        upload(e->d_roww.p, row_w, n * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+
+pd_status pd_engine_set_step_kind(pd_engine* e, int32_t kind) {
+    if (!e || (kind != PD_STEP_DIRECT && kind != PD_STEP_LINEAR)) return PD_VALIDATION_ERROR;
+    if (kind == PD_STEP_LINEAR && !e->d_roww.p) {
+        e->err = "pd_engine_set_step_kind: no linear-response weights (pd_engine_set_linear)";
+        return PD_VALIDATION_ERROR;
+    }
+    e->step_kind = kind;
+    return PD_OK;
+}
+
+int32_t pd_engine_step_kind(const pd_engine* e) { return e ? e->step_kind : -1; }
 
 } // extern "C"
 

@@ -70,6 +70,12 @@ def lib() -> C.CDLL:
     L.pd_integrate_batch.argtypes = [vp, _dp, _ip, _dp, _dp, _dp, C.c_double, _dp, _dp]
     L.pd_lift_batch.argtypes = [vp, C.c_int32, _dp, _dp, _dp, _dp, _dp]
     L.pd_restrict_batch.argtypes = [vp, C.c_int32, _dp, _dp]
+    L.pd_evolve_batch.argtypes = [vp, C.c_int32, _ip, _dp, C.c_double, _dp]
+    L.pd_linear_weights.argtypes = [vp, _dp]
+    L.pd_engine_set_linear.argtypes = [vp, _dp]
+    L.pd_engine_set_step_kind.argtypes = [vp, C.c_int32]
+    L.pd_engine_step_kind.argtypes = [vp]
+    L.pd_engine_step_kind.restype = C.c_int32
     L.pd_problem_create.argtypes = [C.POINTER(ProblemDesc), C.POINTER(vp)]
     L.pd_problem_destroy.argtypes = [vp]
     L.pd_problem_resolved.argtypes = [vp, C.POINTER(ProblemDesc)]
@@ -86,7 +92,8 @@ def lib() -> C.CDLL:
     L.pd_bench_fp64_peak.argtypes = [C.c_double, _dp, _dp]
     for name in ["pd_bench_step_kernel", "pd_bench_fp64_peak", "pd_engine_create", "pd_engine_tables", "pd_engine_set_stream", "pd_gaptooth_step",
                  "pd_projective_step", "pd_projective_step_device", "pd_run", "pd_run_device",
-                 "pd_integrate_batch", "pd_lift_batch", "pd_restrict_batch", "pd_problem_create",
+                 "pd_integrate_batch", "pd_lift_batch", "pd_restrict_batch", "pd_evolve_batch",
+                 "pd_linear_weights", "pd_engine_set_linear", "pd_engine_set_step_kind", "pd_problem_create",
                  "pd_problem_resolved", "pd_problem_engine_desc", "pd_problem_initial_field",
                  "pd_problem_boundary", "pd_problem_boundary_table", "pd_problem_exact",
                  "pd_problem_stability"]:
@@ -324,3 +331,34 @@ class Engine:
         avg = np.empty(len(u))
         _check(lib().pd_restrict_batch(self.h, len(u), _d(u), _d(avg)), self.h)
         return avg
+
+    # ---- linear-response path (GapToothEngine::step with linear_cache) ----
+    def evolve(self, patch_index, stencils, t=0.0):
+        """evolve_patch (gaptooth.cpp:312-353) of given stencils [n][3][3] with
+        the integrators/centres of patches patch_index[n] (EXACT arithmetic)."""
+        idx = np.ascontiguousarray(patch_index, dtype=np.int32).reshape(-1)
+        st = np.ascontiguousarray(stencils, dtype=np.float64).reshape(len(idx), 9)
+        out = np.empty(len(idx))
+        _check(lib().pd_evolve_batch(self.h, len(idx), _i(idx), _d(st), t, _d(out)), self.h)
+        return out
+
+    def linear_weights(self):
+        """build_row_weights (gaptooth.cpp:377-394): [Neta+1][3][3]."""
+        w = np.zeros((self.shape[1], 3, 3))
+        _check(lib().pd_linear_weights(self.h, _d(w)), self.h)
+        return w
+
+    def set_linear(self, row_w=None):
+        """Upload row weights (built here when None) and make every step the
+        linear-response step; set_direct() switches back."""
+        w = self.linear_weights() if row_w is None else np.ascontiguousarray(row_w, dtype=np.float64)
+        _check(lib().pd_engine_set_linear(self.h, _d(w)), self.h)
+        _check(lib().pd_engine_set_step_kind(self.h, abi.PD_STEP_LINEAR), self.h)
+        return w
+
+    def set_direct(self):
+        _check(lib().pd_engine_set_step_kind(self.h, abi.PD_STEP_DIRECT), self.h)
+
+    @property
+    def step_kind(self) -> int:
+        return lib().pd_engine_step_kind(self.h)

@@ -1,7 +1,8 @@
 """Generate the committed golden fixtures (run in the build container, where
 /root/reference and oracle/_ref exist; the GPU box only reads the .npz files).
 
-  python tests/golden/make_golden.py
+  python tests/golden/make_golden.py            (all fixtures)
+  python tests/golden/make_golden.py linear     (ref_linear.npz only)
 
 ref_finals.npz      configs 1-3: initial field, first projective step and the
                     full-run final field computed by the UNMODIFIED reference
@@ -14,6 +15,10 @@ c4_small.npz        config-4 equation on 32x32 patches, 100 macro steps, by the
                     itself rejects b != 0 — parity unpinned by the reference).
 c4_sample.npz       full-size config 4: one gap-tooth substep on 1024 sampled
                     patches by the restated oracle.
+ref_linear.npz      configs 1 and 3 with the reference's DEFAULT linear_cache=auto:
+                    GapToothEngine::step takes the linear-response shortcut
+                    (gaptooth.cpp:377-418); first projective step and final
+                    field of the full run, by the unmodified reference.
 unit_cases.npz      PatchIntegrator::integrate / lift / restrict_average cases
                     run through the reference (known answers of
                     proj/tests/test_microsim.cpp and test_gaptooth.cpp).
@@ -61,6 +66,22 @@ def ref_finals(ref):
         out[f"{name}_maxpct"] = np.array(err)
         print(f"{name}: reference run {sec:.2f} s, max%err {err}")
     np.savez_compressed(OUT / "ref_finals.npz", **out)
+
+
+def ref_linear(ref):
+    out = {}
+    for name in ["c1_diffusion", "c3_annulus"]:
+        d, _ = configs.load(name)
+        prob = Problem(d)
+        R = ref.engine(prob.desc, linear_cache="auto")
+        U0 = R.initial_field()
+        out[f"{name}_U1"] = R.projective_step(U0, 0.0)
+        st, UT, err, sec = R.run()
+        assert st == 0
+        out[f"{name}_final"] = UT
+        out[f"{name}_maxpct"] = np.array(err)
+        print(f"{name}: reference linear-cache run {sec:.3f} s")
+    np.savez_compressed(OUT / "ref_linear.npz", **out)
 
 
 def annulus():
@@ -132,7 +153,11 @@ def unit_cases(ref):
 if __name__ == "__main__":
     ref = Reference()
     O = Restated()
+    if sys.argv[1:] == ["linear"]:
+        ref_linear(ref)
+        sys.exit(0)
     ref_finals(ref)
+    ref_linear(ref)
     annulus()
     c4(O)
     unit_cases(ref)

@@ -336,3 +336,91 @@ def test_config5_shapes_fast_vs_oracle(nodes, restated, gpu):
     assert rel(Ug, Uo) < TOL
     Ux, _ = Engine.from_problem(P, mode=EXACT).run(U0, 6)
     assert np.array_equal(Ux, Uo)
+
+
+# ---------------------------------------------------------------------------
+# linear-response path: GapToothEngine::step with linear_cache (the
+# reference's default for row-shared problems, gaptooth.cpp:213-224, 377-418)
+# ---------------------------------------------------------------------------
+LINEAR = np.load(GOLDEN / "ref_linear.npz")
+
+
+@pytest.mark.parametrize("name", ["c1_diffusion", "c3_annulus"])
+@pytest.mark.parametrize("mode", [EXACT, FAST], ids=["exact", "fast"])
+def test_linear_path_bit_exact_vs_reference(name, mode, restated, gpu):
+    P = load(name)
+    E = Engine.from_problem(P, mode=mode)
+    w = E.set_linear()
+    assert E.step_kind == abi.PD_STEP_LINEAR
+    _, wo = restated.linear_weights(P.engine_desc())
+    assert np.array_equal(w, wo)  # build_row_weights through the EXACT kernel, whatever the family
+    U0 = P.initial_field()
+    Nt = P.desc.Nt
+    U1 = E.projective_step(U0, 0.0, bnd=P.boundary_table(0.0, 1)[0])
+    assert np.array_equal(U1, LINEAR[f"{name}_U1"])
+    UT, stats = E.run(U0, Nt, bnd=P.boundary_table(0.0, Nt))
+    assert stats.steps_done == Nt
+    assert np.array_equal(UT, LINEAR[f"{name}_final"])
+    E.set_direct()
+    U1d = E.projective_step(U0, 0.0, bnd=P.boundary_table(0.0, 1)[0])
+    assert rel(U1d, FINALS[f"{name}_U1"]) < TOL and not np.array_equal(U1d, U1)
+
+
+def test_linear_path_reproduces_shipped_table4_output(gpu):
+    """proj/out/table4/16x10 was written by the reference's linear-response
+    path; the device path reproduces every shipped snapshot bit for bit."""
+    gold = np.load(GOLDEN / "annulus_16x10.npz")
+    P = load("ref_annulus_16x10")
+    E = Engine.from_problem(P)
+    E.set_linear()
+    U, done, Nt = P.initial_field(), 0, P.desc.Nt
+    dt = P.desc.T / Nt
+    for key in ["t_0.25", "t_0.50", "t_0.75", "t_1.00"]:
+        target = int(round(float(key[2:]) * Nt))
+        U, _ = E.run(U, target - done, t0=done * dt, bnd=P.boundary_table(done * dt, target - done))
+        done = target
+        assert np.array_equal(U, gold[key]), key
+
+
+def test_evolve_batch_bit_exact_vs_oracle(restated, gpu):
+    P = load("c2_cdr_tanh")
+    ed = P.engine_desc()
+    E = Engine.from_problem(P, mode=FAST)
+    rng = np.random.default_rng(11)
+    idx = rng.integers(0, E.P, 257).astype(np.int32)
+    sten = rng.uniform(-1, 1, (257, 3, 3))
+    out = E.evolve(idx, sten)
+    st, ref = restated.evolve_batch(ed, idx, sten)
+    assert st == 0 and np.array_equal(out, ref)
+    with pytest.raises(PatchdynError):
+        E.evolve(np.array([E.P], dtype=np.int32), sten[:1])
+
+
+def test_linear_path_rejects_ineligible_problems(gpu):
+    # config 4: coefficients vary along xi (one integrator per patch)
+    P = load("c4_shear", N_xi=9, N_eta=9)
+    E = Engine.from_problem(P)
+    with pytest.raises(PatchdynError, match="xi-independent coefficients"):
+        E.linear_weights()
+    E.set_direct()  # the micro-solve is always available
+    assert E.step_kind == abi.PD_STEP_DIRECT
+    from paper_2405_08764_b200.engine import _check, lib
+
+    with pytest.raises(PatchdynError, match="no linear-response weights"):
+        _check(lib().pd_engine_set_step_kind(E.h, abi.PD_STEP_LINEAR), E.h)
+
+
+def test_cpp_dropin_linear_cache_auto(tmp_path, gpu):
+    """The reference's default linear_cache=auto through the C++ drop-in."""
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = ROOT / "build" / "bin" / "dropin_c1"
+    out = tmp_path / "u.bin"
+    r = subprocess.run([str(exe), "exact", str(out), "auto"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "linear_cache=1" in r.stdout and "steps=200" in r.stdout
+    U = np.fromfile(out, dtype=np.float64).reshape(20, 20)
+    assert np.array_equal(U, LINEAR["c1_diffusion_final"])
+    assert "max_pct_err=%.12f" % float(LINEAR["c1_diffusion_maxpct"]) in r.stdout

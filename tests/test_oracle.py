@@ -354,3 +354,80 @@ def test_config4_small_run_reproduces_committed_oracle_fixture(restated):
     assert np.array_equal(U0, fx["U0"])
     st, UT, _ = restated.run(P.engine_desc(), U0, 100)
     assert st == 0 and np.array_equal(UT, fx["final"])
+
+
+# ---------------------------------------------------------------------------
+# 4. linear-response path (GapToothEngine::step with linear_cache, the
+#    reference's DEFAULT for row-shared problems; gaptooth.cpp:213-224, 377-418)
+# ---------------------------------------------------------------------------
+LINEAR = np.load(GOLDEN / "ref_linear.npz")
+
+
+@pytest.mark.parametrize("name", ["c1_diffusion", "c3_annulus"])
+def test_linear_path_restated_matches_reference_golden(name, restated):
+    P = Problem(configs.load(name)[0])
+    ed = P.engine_desc()
+    st, w = restated.linear_weights(ed)
+    assert st == 0
+    assert np.all(w[0] == 0) and np.all(w[-1] == 0)
+    U0 = P.initial_field()
+    Nt = P.desc.Nt
+    st, U1 = restated.linear_projective_step(ed, w, U0, 0.0, P.boundary_table(0.0, 1)[0])
+    assert st == 0 and np.array_equal(U1, LINEAR[f"{name}_U1"])
+    st, UT, stats = restated.linear_run(ed, w, U0, Nt, 0.0, P.boundary_table(0.0, Nt))
+    assert st == 0 and stats.steps_done == Nt
+    assert np.array_equal(UT, LINEAR[f"{name}_final"])
+    # the shortcut agrees with the micro-solve to ~1e-13 (fast vs direct)
+    assert rel(UT, FINALS[f"{name}_final"]) < 1e-11
+
+
+def test_linear_path_reproduces_shipped_table4_output(restated):
+    """proj/out/table4/16x10 came from the reference's linear-response path:
+    the restated path reproduces every shipped snapshot bit for bit."""
+    gold = np.load(GOLDEN / "annulus_16x10.npz")
+    P = Problem(configs.load("ref_annulus_16x10")[0])
+    ed = P.engine_desc()
+    st, w = restated.linear_weights(ed)
+    assert st == 0
+    U, done, Nt = P.initial_field(), 0, P.desc.Nt
+    dt = P.desc.T / Nt
+    for key in ["t_0.25", "t_0.50", "t_0.75", "t_1.00"]:
+        target = int(round(float(key[2:]) * Nt))
+        st, U, _ = restated.linear_run(ed, w, U, target - done, done * dt, P.boundary_table(done * dt, target - done))
+        assert st == 0
+        done = target
+        assert np.array_equal(U, gold[key]), key
+
+
+def test_evolve_batch_is_one_patch_of_step_direct(restated):
+    """evolve_patch on the gathered stencil == the patch's value after step_direct."""
+    P = Problem(configs.load("c2_cdr_tanh")[0])
+    ed = P.engine_desc()
+    U0 = P.initial_field()
+    st, U1 = restated.gaptooth_step(ed, U0, 0.0)
+    assert st == 0
+    pij = np.ctypeslib.as_array(ed.patch_ij, shape=(ed.npatches, 2))
+    idx = np.array([0, 17, 1000, ed.npatches - 1], dtype=np.int32)
+    sten = np.stack([U0[i - 1:i + 2, j - 1:j + 2] for i, j in pij[idx]])
+    st, avg = restated.evolve_batch(ed, idx, sten)
+    assert st == 0
+    assert np.array_equal(avg, U1[pij[idx, 0], pij[idx, 1]])
+
+
+def test_linear_step_is_linear_and_local(restated):
+    P = Problem(configs.load("c1_diffusion")[0])
+    ed = P.engine_desc()
+    _, w = restated.linear_weights(ed)
+    rng = np.random.default_rng(5)
+    U = rng.uniform(-1, 1, P.shape)
+    _, A = restated.linear_step(ed, w, U)
+    _, B = restated.linear_step(ed, w, 2.0 * U)
+    assert np.array_equal(B, 2.0 * A)
+    # a unit impulse at an interior node reaches exactly its 3x3 neighbourhood
+    E = np.zeros(P.shape)
+    E[9, 9] = 1.0
+    _, R = restated.linear_step(ed, w, E)
+    nz = np.argwhere(R != 0)
+    assert nz.min(0).tolist() == [8, 8] and nz.max(0).tolist() == [10, 10]
+    # and the response of patch (9,9) to it is row 9's centre weight
+    assert R[9, 9] == w[9, 1, 1]
