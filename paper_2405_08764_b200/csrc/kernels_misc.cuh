@@ -9,16 +9,15 @@ namespace pdb200::dev {
 // bnd == nullptr, keep the input field's boundary (copied from F) and apply
 // the periodic seam U(Nxi,j) = U(0,j).  Non-patch nodes are exactly the
 // boundary rows/columns (+ the seam column when periodic).
-__global__ void k_refresh(Params p, double* __restrict__ out, const double* __restrict__ F,
-                          const double* __restrict__ bnd, const int* __restrict__ fail_flag) {
-    if (fail_flag && *fail_flag) return;
+__device__ __forceinline__ void refresh_range(const Params& p, double* __restrict__ out, const double* __restrict__ F,
+                                              const double* __restrict__ bnd, int t0, int stride) {
     const int N1 = p.Nxi, N2 = p.Neta, n2 = p.NF2;
     const int rows = 2 * (N1 + 1), cols = 2 * (N2 + 1);
     const double* S = bnd;
     const double* Nn = bnd ? bnd + (N1 + 1) : nullptr;
     const double* W = bnd ? bnd + 2 * (N1 + 1) : nullptr;
     const double* E = bnd ? W + (N2 + 1) : nullptr;
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < rows + cols; t += gridDim.x * blockDim.x) {
+    for (int t = t0; t < rows + cols; t += stride) {
         if (t < rows) { // S/N rows; corners are owned by the column pass (W/E or seam)
             const int i = t % (N1 + 1), j = t < N1 + 1 ? 0 : N2;
             if (p.periodic ? i == N1 : (i == 0 || i == N1)) continue;
@@ -31,7 +30,7 @@ __global__ void k_refresh(Params p, double* __restrict__ out, const double* __re
                 double v;
                 if (j == 0) v = bnd ? S[0] : F[0];
                 else if (j == N2) v = bnd ? Nn[0] : F[N2];
-                else v = out[j]; // patch (0,j) result, written by the previous kernel
+                else v = out[j]; // patch (0,j) result, written before the refresh
                 out[(size_t)N1 * n2 + j] = v;
             } else {
                 const size_t node = (size_t)(east ? N1 : 0) * n2 + j;
@@ -39,6 +38,12 @@ __global__ void k_refresh(Params p, double* __restrict__ out, const double* __re
             }
         }
     }
+}
+
+__global__ void k_refresh(Params p, double* __restrict__ out, const double* __restrict__ F,
+                          const double* __restrict__ bnd, const int* __restrict__ fail_flag) {
+    if (fail_flag && *fail_flag) return;
+    refresh_range(p, out, F, bnd, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // out(i,j) = Uk + horizon * (Uk1 - Uk)/tau on patch nodes (cpi.cpp:67-74), k > 0.
@@ -81,6 +86,91 @@ __global__ void k_guard(const double* __restrict__ U, size_t n, unsigned long lo
             }
         }
     }
+}
+
+// ---- whole linear-response run in one CTA (fields resident in shared memory) ----
+// pd_run_device with PD_STEP_LINEAR when the macro field fits in shared memory:
+// every macro step (k+1 linear substeps, the projective extrapolation, the
+// boundary refresh and the blow-up guard, cpi.cpp:58-77, 175-202) runs inside
+// one kernel with block barriers instead of four launches per step.  Same
+// arithmetic, in the same order, as k_linear_step / k_extrapolate / k_refresh /
+// k_guard, so results and statistics are identical to the multi-launch loop.
+// Shared layout: A (macro field), B0/B1 (substep ping-pong; B1 only for k > 0).
+__global__ void __launch_bounds__(1024)
+k_linear_run_block(Params p, double* __restrict__ U, const int* __restrict__ pij, const double* __restrict__ row_w,
+                   const double* __restrict__ bnd, size_t perim, int nsteps, double blowup,
+                   unsigned long long* __restrict__ slot, int* __restrict__ fail) {
+    extern __shared__ double sfld[];
+    __shared__ unsigned long long wm[32];
+    __shared__ int s_stop;
+    const size_t NF = (size_t)(p.Nxi + 1) * p.NF2;
+    double* A = sfld;
+    auto B = [&](int b) { return sfld + NF * (size_t)(1 + b); };
+    const int tid = threadIdx.x, nth = blockDim.x;
+    for (size_t q = tid; q < NF; q += nth) A[q] = U[q];
+    if (tid == 0) s_stop = 0;
+    __syncthreads();
+    const int k = p.k;
+    const double horizon = XSUB(p.dt_macro, XMUL((double)k, p.tau)); // as projective_dev computes it
+    for (int n = 0; n < nsteps; ++n) {
+        const double* bn = bnd ? bnd + perim * (size_t)(k + 2) * n : nullptr;
+        const double* src = A;
+        for (int m = 0; m <= k; ++m) {
+            double* dst = B(m & 1);
+            for (int q = tid; q < p.P; q += nth) {
+                const int i = pij[2 * q], j = pij[2 * q + 1];
+                const double* w = row_w + (size_t)9 * j;
+                double acc = 0.0;
+#pragma unroll
+                for (int dp = -1; dp <= 1; ++dp) {
+                    int ip = i + dp;
+                    if (p.periodic) ip = ((ip % p.Nxi) + p.Nxi) % p.Nxi;
+#pragma unroll
+                    for (int dq = -1; dq <= 1; ++dq)
+                        acc = XADD(acc, XMUL(w[3 * (dp + 1) + dq + 1], src[(size_t)ip * p.NF2 + j + dq]));
+                }
+                dst[(size_t)i * p.NF2 + j] = acc;
+            }
+            __syncthreads();
+            if (k > 0) { // the substep field is read by the next substep: refresh its boundary
+                refresh_range(p, dst, src, bn ? bn + perim * m : nullptr, tid, nth);
+                __syncthreads();
+            }
+            src = dst;
+        }
+        // projective extrapolation on patch nodes, in place in A (cpi.cpp:67-74)
+        const double* Uk = k == 0 ? A : B((k - 1) & 1);
+        const double* Uk1 = B(k & 1);
+        for (int q = tid; q < p.P; q += nth) {
+            const size_t node = (size_t)pij[2 * q] * p.NF2 + pij[2 * q + 1];
+            if (k == 0)
+                A[node] = XADD(A[node], XMUL(p.dt_macro, XDIV(XSUB(Uk1[node], A[node]), p.tau)));
+            else
+                A[node] = XADD(Uk[node], XMUL(horizon, XDIV(XSUB(Uk1[node], Uk[node]), p.tau)));
+        }
+        __syncthreads();
+        refresh_range(p, A, A, bn ? bn + perim * (size_t)(k + 1) : nullptr, tid, nth);
+        __syncthreads();
+        // blow-up guard (cpi.cpp:187-202), max |U| as a non-negative bit pattern
+        unsigned long long mx = 0;
+        for (size_t q = tid; q < NF; q += nth) mx = max(mx, (unsigned long long)__double_as_longlong(fabs(A[q])));
+        for (int o = 16; o; o >>= 1) mx = max(mx, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
+        if ((tid & 31) == 0) wm[tid >> 5] = mx;
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < (nth >> 5); ++w) mx = max(mx, wm[w]);
+            slot[n] = mx;
+            const bool nonfinite = mx >= 0x7FF0000000000000ull;
+            if (nonfinite || __longlong_as_double((long long)mx) > blowup) {
+                fail[0] = n + 1;
+                fail[1] = nonfinite ? 1 : 0;
+                s_stop = 1;
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+    }
+    for (size_t q = tid; q < NF; q += nth) U[q] = A[q];
 }
 
 } // namespace pdb200::dev

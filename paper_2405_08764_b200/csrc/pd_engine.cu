@@ -65,6 +65,8 @@ struct DevBuf {
 
 } // namespace
 
+constexpr size_t kLinearBlockSmemMax = 220 * 1024; // dynamic shared memory of k_linear_run_block
+
 struct pd_engine {
     pd_engine_desc d{};
     Params prm{};
@@ -498,16 +500,28 @@ pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps
         const size_t pk = e->perim * (e->prm.k + 2);
         const size_t sk = (size_t)e->prm.nt * (e->prm.k + 1);
         const int64_t l0 = e->launches;
+        // linear-response steps on a field that fits in shared memory: the whole
+        // loop is one single-CTA kernel (k_linear_run_block), same results
+        const size_t block_smem = (e->prm.k == 0 ? 2 : 3) * NF * 8;
+        const bool block_run = e->step_kind == PD_STEP_LINEAR && nsteps > 0 && block_smem <= kLinearBlockSmemMax;
         CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
-        double* cur = U;
-        double* nxt = scratch;
-        for (int n = 0; n < nsteps; ++n) {
-            e->projective_dev(cur, nxt, bnd ? bnd + pk * n : nullptr, (src_time && e->prm.source) ? src_time + sk * n : nullptr,
-                              e->d_fail.p);
-            k_guard<<<gblocks, 256, 0, e->stream>>>(nxt, NF, e->d_slot.p, e->d_counter.p, e->d_fail.p, e->d_fail.p + 1,
-                                                    n, blowup);
+        if (block_run) {
+            CUDA_TRY(cudaFuncSetAttribute(k_linear_run_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)block_smem));
+            k_linear_run_block<<<1, 1024, block_smem, e->stream>>>(e->prm, U, e->d_pij.p, e->d_roww.p, bnd, e->perim,
+                                                                    nsteps, blowup, e->d_slot.p, e->d_fail.p);
             e->check_launch();
-            std::swap(cur, nxt);
+        } else {
+            double* cur = U;
+            double* nxt = scratch;
+            for (int n = 0; n < nsteps; ++n) {
+                e->projective_dev(cur, nxt, bnd ? bnd + pk * n : nullptr,
+                                  (src_time && e->prm.source) ? src_time + sk * n : nullptr, e->d_fail.p);
+                k_guard<<<gblocks, 256, 0, e->stream>>>(nxt, NF, e->d_slot.p, e->d_counter.p, e->d_fail.p,
+                                                        e->d_fail.p + 1, n, blowup);
+                e->check_launch();
+                std::swap(cur, nxt);
+            }
         }
         CUDA_TRY(cudaEventRecord(e->ev1, e->stream));
         int fail[2] = {0, 0};
@@ -519,7 +533,8 @@ pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps
         CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
         // the field after the last executed step lives in buffer (done % 2 == 1 ? scratch : U)
         const int done = fail[0] ? fail[0] : nsteps;
-        if (done % 2 == 1) CUDA_TRY(cudaMemcpyAsync(U, scratch, NF * 8, cudaMemcpyDeviceToDevice, e->stream));
+        if (!block_run && done % 2 == 1)
+            CUDA_TRY(cudaMemcpyAsync(U, scratch, NF * 8, cudaMemcpyDeviceToDevice, e->stream));
         CUDA_TRY(cudaStreamSynchronize(e->stream));
         pd_run_stats s{};
         s.steps_done = fail[0] ? fail[0] - 1 : nsteps;

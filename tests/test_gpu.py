@@ -424,3 +424,38 @@ def test_cpp_dropin_linear_cache_auto(tmp_path, gpu):
     U = np.fromfile(out, dtype=np.float64).reshape(20, 20)
     assert np.array_equal(U, LINEAR["c1_diffusion_final"])
     assert "max_pct_err=%.12f" % float(LINEAR["c1_diffusion_maxpct"]) in r.stdout
+
+
+@pytest.mark.parametrize("N,k", [(19, 0), (19, 1), (127, 0), (127, 1)])
+def test_linear_run_single_cta_and_multilaunch_vs_oracle(N, k, restated, gpu):
+    """pd_run with PD_STEP_LINEAR: a field that fits in shared memory runs the
+    whole loop in one CTA (k_linear_run_block); a larger one uses the
+    per-step launches.  Both equal the restated linear path bit for bit."""
+    P = load("c1_diffusion", N_xi=N, N_eta=N, k=k, Nt=20)
+    ed = P.engine_desc()
+    E = Engine.from_problem(P)
+    w = E.set_linear()
+    U0 = P.initial_field()
+    bnd = P.boundary_table(0.0, 20)
+    U, stats = E.run(U0, 20, bnd=bnd)
+    st, Uo, so = restated.linear_run(ed, w, U0, 20, 0.0, bnd)
+    assert st == 0 and np.array_equal(U, Uo)
+    assert stats.umax_last == so.umax_last and stats.blowup_threshold == so.blowup_threshold
+    block = (2 if k == 0 else 3) * (N + 1) ** 2 * 8 <= 220 * 1024
+    assert stats.kernel_launches == (1 if block else 20 * (3 if k == 0 else 2 * (k + 1) + 3))
+
+
+@pytest.mark.parametrize("N", [19, 127])
+def test_linear_run_guard_trips_like_oracle(N, restated, gpu):
+    P = load("c1_diffusion", N_xi=N, N_eta=N, dt_over_tau=1000, Nt=50)
+    ed = P.engine_desc()
+    E = Engine.from_problem(P)
+    w = E.set_linear()
+    U0 = P.initial_field()
+    bnd = P.boundary_table(0.0, 50)
+    U, stats = E.run(U0, 50, bnd=bnd, raise_on_instability=False)
+    st, Uo, so = restated.linear_run(ed, w, U0, 50, 0.0, bnd)
+    assert st == abi.PD_MACRO_INSTABILITY and so.failed_step > 0
+    assert (stats.failed_step, stats.steps_done, stats.failed_nonfinite) == (so.failed_step, so.steps_done,
+                                                                             so.failed_nonfinite)
+    assert np.array_equal(U, Uo)
