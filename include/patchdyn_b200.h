@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define PD_ABI_VERSION 1
+#define PD_ABI_VERSION 2
 
 /* Status codes map 1:1 onto the reference exception types
  * (proj/include/patchdyn/errors.hpp:9-61). */
@@ -79,6 +79,12 @@ enum { PD_EDGE_E = 0, PD_EDGE_W = 1, PD_EDGE_N = 2, PD_EDGE_S = 3 };
 enum { PD_QUAD_TRAPEZOID = 0, PD_QUAD_SIMPSON = 1 };
 /* source structure  microsim.hpp:58-64 */
 enum { PD_SOURCE_ZERO = 0, PD_SOURCE_SEPARABLE = 1 };
+/* Micro-solver (SchemeConfig::Solver, scheme_config.hpp:19-20; NOTE the C
+ * values differ from the reference's enum order so that a zero-initialised
+ * descriptor selects the explicit scheme of the BASELINE configs) and the ADI
+ * path's upwind convection order (UpwindOrder, microsim.hpp). */
+enum { PD_SOLVER_EXPLICIT = 0, PD_SOLVER_ADI = 1 };
+enum { PD_UPWIND_TWO = 0, PD_UPWIND_THREE = 1, PD_UPWIND_FOUR = 2 };
 /* Kernel family.  EXACT replays the reference's operation order (IEEE, no FMA
  * contraction) and is bit-identical to the reference for b = 0; FAST is the
  * register-blocked folded-weight kernel (FMA), within 1e-11 of it. */
@@ -119,6 +125,12 @@ typedef struct pd_engine_desc {
     const double* source_spatial; /* [ncoeff_sets][nx+1][ny+1] or NULL */
     double l;
     int32_t mode;
+    /* micro-solver: PD_SOLVER_EXPLICIT (microsim.cpp:292-332) or PD_SOLVER_ADI
+     * (Peaceman-Rachford, microsim.cpp:334-507; EXACT family only), with the
+     * ADI upwind order/parameter (UpwindSpec, microsim.hpp) */
+    int32_t solver;
+    int32_t upwind_order;
+    double upwind_r;
 } pd_engine_desc;
 
 typedef struct pd_engine pd_engine;
@@ -200,7 +212,7 @@ pd_status pd_bench_step_kernel(pd_engine* e, const double* in_dev, double* out_d
                                double* ms_per_launch);
 pd_status pd_bench_fp64_peak(double ms_target, double* tflops, double* sm_clock_ghz);
 
-/* Unfused micro-solver, batched: PatchIntegrator::integrate for every patch
+/* Unfused micro-solver, batched (explicit or ADI per desc->solver): PatchIntegrator::integrate for every patch
  * p (coefficient set coeff_set[p]) from u0 [P][n1][n2] over nt steps at t0.
  * edge_kind[4] (E,W,N,S), edge_value/edge_slope [P][4][max(n1,n2)],
  * robin_w[4][2].  Result in uT [P][n1][n2]. */
@@ -256,7 +268,8 @@ enum {
     PD_PROBLEM_ANNULUS_NONAXI = 3,   /* config 3: polar map, non-axisymmetric IC */
     PD_PROBLEM_SHEAR_CDR = 4,        /* configs 4/5: sinusoidal non-orthogonal map */
     PD_PROBLEM_REF_ANNULUS = 10,     /* problems::problem2_annulus  problems.cpp:110-138 */
-    PD_PROBLEM_REF_CDR = 11,         /* problems::problem1_constant(lambda)  problems.cpp:19-69 */
+    PD_PROBLEM_REF_CDR = 11,         /* problems::problem1_constant(lambda)  problems.cpp:19-73 */
+    PD_PROBLEM_REF_CDR_VAR = 13,     /* problems::problem1_variable(lambda)  problems.cpp:19-75 */
     PD_PROBLEM_STEADY = 12           /* harmonic u = x + y (test_gaptooth.cpp:32-49) */
 };
 enum { PD_DT_GIVEN = 0, PD_DT_DIFFUSION = 1, PD_DT_METRIC = 2 };
@@ -284,6 +297,9 @@ typedef struct pd_problem_desc {
     double h_frac;       /* > 0: h = h_frac * macro spacing per direction */
     double dt_over_tau;  /* > 0: T = Nt * dt_over_tau * tau */
     int32_t threads;     /* host threads for coefficient sampling (0 = all) */
+    int32_t solver;      /* PD_SOLVER_* */
+    int32_t upwind_order;/* PD_UPWIND_* (ADI) */
+    double upwind_r;     /* four-point upwind parameter r (ADI) */
 } pd_problem_desc;
 
 typedef struct pd_problem pd_problem;
@@ -302,8 +318,9 @@ pd_status pd_problem_boundary(const pd_problem* p, double t, double* perimeter_h
 pd_status pd_problem_boundary_table(const pd_problem* p, double t0, int32_t nsteps, double* out_host);
 /* Separable-source time factors time(t)/l (microsim.cpp:272-277) for pd_run:
  * [nsteps][k+1][nt], macro step n from t0 + n*dt, substep m from
- * t_n + m*tau (cpi.cpp:65), micro step s at t_m + s*dt_micro
- * (microsim.cpp:536-537).  PD_UNSUPPORTED when the source is zero. */
+ * t_n + m*tau (cpi.cpp:65), micro step s at t_m + s*dt_micro for the
+ * explicit scheme and t_m + (s+1/2)*dt_micro for ADI (microsim.cpp:536-537).
+ * PD_UNSUPPORTED when the source is zero. */
 pd_status pd_problem_source_time(const pd_problem* p, double t0, int32_t nsteps, double* out_host);
 /* Exact solution on the macro grid at t; PD_UNSUPPORTED if none. */
 pd_status pd_problem_exact(const pd_problem* p, double t, double* U_host);

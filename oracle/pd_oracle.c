@@ -247,10 +247,254 @@ static double at_ext(const field_t* f, int p, int q) {
     return U_(f, ii, jj) + ox + oy;
 }
 
+/* ---- ADI micro-solver  microsim.cpp:56-138 (upwind), 334-507 (adi_sweep),
+ *      linalg.cpp:8-61 (line solvers) ------------------------------------- */
+
+typedef struct {
+    int off[4];
+    double w[4];
+    int n;
+} upw_t;
+
+/* make_upwind  microsim.cpp:65-104 (order: PD_UPWIND_*) */
+static upw_t make_upwind(int order, double r, double delta, int vel_sign) {
+    upw_t s;
+    memset(&s, 0, sizeof s);
+    const double s1 = vel_sign >= 0 ? 1.0 : -1.0;
+    if (order == PD_UPWIND_TWO) {
+        s.n = 2;
+        s.off[0] = 0;
+        s.off[1] = vel_sign >= 0 ? -1 : 1;
+        s.w[0] = s1 / delta;
+        s.w[1] = -s1 / delta;
+    } else if (order == PD_UPWIND_THREE) {
+        s.n = 3;
+        s.off[0] = 0;
+        s.off[1] = vel_sign >= 0 ? -1 : 1;
+        s.off[2] = vel_sign >= 0 ? -2 : 2;
+        s.w[0] = 3.0 * s1 / (2 * delta);
+        s.w[1] = -4.0 * s1 / (2 * delta);
+        s.w[2] = s1 / (2 * delta);
+    } else {
+        s.n = 4;
+        if (vel_sign >= 0) {
+            s.off[0] = 1;  s.w[0] = 1.0 / (2 * delta) - r / (3 * delta);
+            s.off[1] = -1; s.w[1] = -1.0 / (2 * delta) - r / delta;
+            s.off[2] = -2; s.w[2] = r / (3 * delta);
+            s.off[3] = 0;  s.w[3] = r / delta;
+        } else {
+            s.off[0] = 1;  s.w[0] = 1.0 / (2 * delta) + r / delta;
+            s.off[1] = -1; s.w[1] = -1.0 / (2 * delta) + r / (3 * delta);
+            s.off[2] = 2;  s.w[2] = -r / (3 * delta);
+            s.off[3] = 0;  s.w[3] = -r / delta;
+        }
+    }
+    return s;
+}
+
+/* upwind_with_fallback  microsim.cpp:107-119 */
+static upw_t upwind_fb(int order, double r, double delta, int vel_sign, int i, int imax) {
+    if (order != PD_UPWIND_TWO) {
+        const upw_t s = make_upwind(order, r, delta, vel_sign);
+        int ok = 1;
+        for (int k = 0; k < s.n; ++k) {
+            const int idx = i + s.off[k];
+            if (idx < 0 || idx > imax) ok = 0;
+        }
+        if (ok) return s;
+    }
+    return make_upwind(PD_UPWIND_TWO, r, delta, vel_sign);
+}
+
+typedef struct {
+    int nx, ny, N, order;
+    double dxi, deta, half, r;
+    const double *A, *C, *Vx, *Vy, *W;
+    const ghost_t *E, *Wg, *Ng, *S;
+} adi_t;
+
+/* cross_term  microsim.cpp:357-395 */
+static double cross_term(const adi_t* a, const double* f, int i, int j, int eta_dir) {
+    const int nx = a->nx, ny = a->ny, n2 = ny + 1, k = i * n2 + j;
+    if (eta_dir) {
+        const double glo = a->S->cIn * f[i * n2 + 1] + a->S->cEdge * f[i * n2] + (a->S->b ? a->S->b[i] : 0.0);
+        const double ghi = a->Ng->cIn * f[i * n2 + ny - 1] + a->Ng->cEdge * f[i * n2 + ny] + (a->Ng->b ? a->Ng->b[i] : 0.0);
+        const double um = j > 0 ? f[k - 1] : glo;
+        const double up = j < ny ? f[k + 1] : ghi;
+        const double uc = f[k];
+        const double uyy = (um - 2.0 * uc + up) / (a->deta * a->deta);
+        const double v = a->Vy[k];
+        const upw_t sw = upwind_fb(a->order, a->r, a->deta, v >= 0 ? 1 : -1, j, ny);
+        double du = 0.0;
+        for (int m = 0; m < sw.n; ++m) {
+            const int jj = j + sw.off[m];
+            const double val = jj < 0 ? glo : (jj > ny ? ghi : f[i * n2 + jj]);
+            du += sw.w[m] * val;
+        }
+        return a->C[k] * uyy - v * du - 0.5 * a->W[k] * uc;
+    }
+    const double glo = a->Wg->cIn * f[n2 + j] + a->Wg->cEdge * f[j] + (a->Wg->b ? a->Wg->b[j] : 0.0);
+    const double ghi = a->E->cIn * f[(nx - 1) * n2 + j] + a->E->cEdge * f[nx * n2 + j] + (a->E->b ? a->E->b[j] : 0.0);
+    const double um = i > 0 ? f[k - n2] : glo;
+    const double up = i < nx ? f[k + n2] : ghi;
+    const double uc = f[k];
+    const double uxx = (um - 2.0 * uc + up) / (a->dxi * a->dxi);
+    const double v = a->Vx[k];
+    const upw_t sw = upwind_fb(a->order, a->r, a->dxi, v >= 0 ? 1 : -1, i, nx);
+    double du = 0.0;
+    for (int m = 0; m < sw.n; ++m) {
+        const int ii = i + sw.off[m];
+        const double val = ii < 0 ? glo : (ii > nx ? ghi : f[ii * n2 + j]);
+        du += sw.w[m] * val;
+    }
+    return a->A[k] * uxx - v * du - 0.5 * a->W[k] * uc;
+}
+
+/* solve_tridiagonal  linalg.cpp:8-25 */
+static void solve_tridiagonal(const double* lo, const double* di, const double* up, double* rhs, double* wk, int n) {
+    double m = di[0];
+    wk[0] = up[0] / m;
+    rhs[0] /= m;
+    for (int k = 1; k < n; ++k) {
+        m = di[k] - lo[k] * wk[k - 1];
+        wk[k] = up[k] / m;
+        rhs[k] = (rhs[k] - lo[k] * rhs[k - 1]) / m;
+    }
+    for (int k = n - 1; k-- > 0;) rhs[k] -= wk[k] * rhs[k + 1];
+}
+
+/* BandedMatrix(n,2,2)::solve  linalg.cpp:43-61; band[r*5 + (c-r) + 2] */
+static void solve_banded(double* band, double* rhs, int n) {
+    for (int k = 0; k < n - 1; ++k) {
+        const double piv = band[k * 5 + 2];
+        const int last = k + 2 < n - 1 ? k + 2 : n - 1;
+        for (int r = k + 1; r <= last; ++r) {
+            const double f = band[r * 5 + (k - r) + 2] / piv;
+            if (f == 0.0) continue;
+            const int cmax = k + 2 < n - 1 ? k + 2 : n - 1;
+            for (int c = k + 1; c <= cmax; ++c) band[r * 5 + (c - r) + 2] -= f * band[k * 5 + (c - k) + 2];
+            rhs[r] -= f * rhs[k];
+        }
+    }
+    for (int r = n - 1; r >= 0; --r) {
+        double s = rhs[r];
+        const int cmax = r + 2 < n - 1 ? r + 2 : n - 1;
+        for (int c = r + 1; c <= cmax; ++c) s -= band[r * 5 + (c - r) + 2] * rhs[c];
+        rhs[r] = s / band[r * 5 + 2];
+    }
+}
+
+/* implicit_sweep  microsim.cpp:402-491: (I - half*L_swept) out = rhs_field */
+static void implicit_sweep(const adi_t* a, const double* rhsf, double* out, int xi_dir, double* sc) {
+    const int nx = a->nx, ny = a->ny, n2 = ny + 1;
+    const int nline = xi_dir ? ny : nx, n = xi_dir ? nx + 1 : ny + 1;
+    const double dd = xi_dir ? a->dxi : a->deta;
+    const ghost_t* glo = xi_dir ? a->Wg : a->S;
+    const ghost_t* ghi = xi_dir ? a->E : a->Ng;
+    const ghost_t* slo = xi_dir ? a->S : a->Wg;
+    const ghost_t* shi = xi_dir ? a->Ng : a->E;
+    const int banded = a->order != PD_UPWIND_TWO;
+    double *lo = sc, *di = sc + n, *up = sc + 2 * n, *rhs = sc + 3 * n, *wk = sc + 4 * n;
+    double* band = sc;
+    double* brhs = sc + 5 * n;
+    for (int line = 0; line <= nline; ++line) {
+        if ((line == 0 && slo->pinned) || (line == nline && shi->pinned)) {
+            const ghost_t* e = line == 0 ? slo : shi;
+            for (int k = 0; k < n; ++k) {
+                if (xi_dir) out[k * n2 + line] = pinned_value(e, k);
+                else out[line * n2 + k] = pinned_value(e, k);
+            }
+            continue;
+        }
+        if (banded) memset(band, 0, sizeof(double) * 5 * n);
+        for (int k = 0; k < n; ++k) {
+            const int pin_lo = k == 0 && glo->pinned, pin_hi = k == n - 1 && ghi->pinned;
+            if (pin_lo || pin_hi) {
+                const double pv = pinned_value(pin_lo ? glo : ghi, line);
+                if (banded) { band[k * 5 + 2] = 1.0; brhs[k] = pv; }
+                else { di[k] = 1.0; lo[k] = 0.0; up[k] = 0.0; rhs[k] = pv; }
+                continue;
+            }
+            const int i = xi_dir ? k : line, j = xi_dir ? line : k, q = i * n2 + j;
+            const double A = xi_dir ? a->A[q] : a->C[q];
+            const double V = xi_dir ? a->Vx[q] : a->Vy[q];
+            const double s = a->half * A / (dd * dd);
+            double diag = 1.0 + 2.0 * s + a->half * 0.5 * a->W[q];
+            double sub = -s, sup = -s, lo2 = 0.0, hi2 = 0.0;
+            double rr = rhsf[q];
+            const upw_t sw = upwind_fb(a->order, a->r, dd, V >= 0 ? 1 : -1, k, n - 1);
+            for (int m = 0; m < sw.n; ++m) {
+                const double wgt = a->half * V * sw.w[m];
+                switch (sw.off[m]) {
+                    case 0: diag += wgt; break;
+                    case -1: sub += wgt; break;
+                    case 1: sup += wgt; break;
+                    case -2: lo2 += wgt; break;
+                    default: hi2 += wgt; break;
+                }
+            }
+            if (k == 0) {
+                rr -= sub * glo->b[line];
+                diag += sub * glo->cEdge;
+                sup += sub * glo->cIn;
+                sub = 0.0;
+            } else if (k == n - 1) {
+                rr -= sup * ghi->b[line];
+                diag += sup * ghi->cEdge;
+                sub += sup * ghi->cIn;
+                sup = 0.0;
+            }
+            if (banded) {
+                brhs[k] = rr;
+                band[k * 5 + 2] = diag;
+                if (k > 0) band[k * 5 + 1] = sub;
+                if (k < n - 1) band[k * 5 + 3] = sup;
+                if (lo2 != 0.0) band[k * 5 + 0] = lo2;
+                if (hi2 != 0.0) band[k * 5 + 4] = hi2;
+            } else {
+                rhs[k] = rr; di[k] = diag; lo[k] = sub; up[k] = sup;
+            }
+        }
+        const double* res = banded ? brhs : rhs;
+        if (banded) solve_banded(band, brhs, n);
+        else solve_tridiagonal(lo, di, up, rhs, wk, n);
+        for (int k = 0; k < n; ++k) {
+            if (xi_dir) out[k * n2 + line] = res[k];
+            else out[line * n2 + k] = res[k];
+        }
+    }
+}
+
+static int node_pinned(const adi_t* a, int i, int j) {
+    return (i == 0 && a->Wg->pinned) || (i == a->nx && a->E->pinned) || (j == 0 && a->S->pinned) ||
+           (j == a->ny && a->Ng->pinned);
+}
+
+/* adi_sweep  microsim.cpp:334-507 (one Peaceman-Rachford step, u in place) */
+static void adi_sweep(const adi_t* a, const double* G, double* u, double* work, double* rhsf, double* sc) {
+    const int nx = a->nx, ny = a->ny, n2 = ny + 1;
+    for (int i = 0; i <= nx; ++i)
+        for (int j = 0; j <= ny; ++j)
+            rhsf[i * n2 + j] = node_pinned(a, i, j) ? 0.0 : u[i * n2 + j] + a->half * (cross_term(a, u, i, j, 1) + G[i * n2 + j]);
+    implicit_sweep(a, rhsf, work, 1, sc);
+    for (int i = 0; i <= nx; ++i)
+        for (int j = 0; j <= ny; ++j)
+            rhsf[i * n2 + j] = node_pinned(a, i, j) ? 0.0 : work[i * n2 + j] + a->half * (cross_term(a, work, i, j, 0) + G[i * n2 + j]);
+    implicit_sweep(a, rhsf, u, 0, sc);
+}
+
 int pdo_integrate(const double* coef, int nx, int ny, int nt, double h_xi, double h_eta,
                   double tau, const int* kinds, const double* values, const double* slopes,
                   const double* robin_w, const double* src_spatial, const double* src_time,
                   double* u) {
+    return pdo_integrate_ex(coef, nx, ny, nt, h_xi, h_eta, tau, kinds, values, slopes, robin_w, src_spatial,
+                            src_time, u, PD_SOLVER_EXPLICIT, PD_UPWIND_TWO, 0.5);
+}
+
+int pdo_integrate_ex(const double* coef, int nx, int ny, int nt, double h_xi, double h_eta,
+                     double tau, const int* kinds, const double* values, const double* slopes,
+                     const double* robin_w, const double* src_spatial, const double* src_time,
+                     double* u, int solver, int upwind_order, double upwind_r) {
     const int n1 = nx + 1, n2 = ny + 1, L = (n1 > n2 ? n1 : n2), N = n1 * n2;
     /* make_micro_grid  microsim.cpp:18-24 */
     const double dxi = h_xi / nx, deta = h_eta / ny, dt = tau / nt;
@@ -289,6 +533,28 @@ int pdo_integrate(const double* coef, int nx, int ny, int nt, double h_xi, doubl
     if (kinds[PD_EDGE_N] == PD_EDGE_DIRICHLET)
         for (int i = 0; i <= nx; ++i) u[i * n2 + ny] = values[PD_EDGE_N * L + i];
 
+    if (solver == PD_SOLVER_ADI) {
+        if (mixed) {
+            snprintf(g_err, sizeof g_err, "mixed-derivative term with the ADI micro-solver is not defined");
+            free(buf);
+            return PD_MIXED_TERM_UNSUPPORTED;
+        }
+        adi_t a = {nx, ny, N, upwind_order, dxi, deta, 0.5 * dt, upwind_r, A, C, Vx, Vy, W, &gE, &gW, &gN, &gS};
+        double* abuf = (double*)malloc(sizeof(double) * (2 * (size_t)N + 6 * (size_t)L));
+        for (int step = 0; step < nt; ++step) {
+            /* sample_source at t0 + (step + 1/2) dt  microsim.cpp:536-537 (src_time carries it) */
+            if (src_spatial && src_time) {
+                const double ft = src_time[step];
+                for (int k = 0; k < N; ++k) G[k] = src_spatial[k] * ft;
+            } else {
+                for (int k = 0; k < N; ++k) G[k] = 0.0;
+            }
+            adi_sweep(&a, G, u, abuf, abuf + N, abuf + 2 * N);
+        }
+        free(abuf);
+        free(buf);
+        return PD_OK;
+    }
     const double idx2 = 1.0 / (dxi * dxi), idy2 = 1.0 / (deta * deta);
     const double idx = 1.0 / (2.0 * dxi), idy = 1.0 / (2.0 * deta);
     const double ixy = 1.0 / (4.0 * dxi * deta); /* extension: u_xi_eta scale */
@@ -452,8 +718,8 @@ static int evolve_patch_vals(const eng_t* e, const double* vals, const double* F
     const double* coef = d->coeffs + (size_t)set * PD_NCOEF * N;
     const double* sp = (d->source_kind == PD_SOURCE_SEPARABLE && d->source_spatial)
                            ? d->source_spatial + (size_t)set * N : NULL;
-    const int st = pdo_integrate(coef, d->nx, d->ny, d->nt, d->h_xi, d->h_eta, d->tau, kinds, values,
-                                 slopes, rw, sp, sp ? src_time : NULL, u);
+    const int st = pdo_integrate_ex(coef, d->nx, d->ny, d->nt, d->h_xi, d->h_eta, d->tau, kinds, values,
+                                    slopes, rw, sp, sp ? src_time : NULL, u, d->solver, d->upwind_order, d->upwind_r);
     if (st != PD_OK) return st;
     *avg = pdo_restrict(u, n1, n2, d->quadrature);
     (void)t;

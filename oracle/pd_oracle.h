@@ -44,6 +44,13 @@ int pdo_integrate(const double* coef, int nx, int ny, int nt, double h_xi, doubl
                   double tau, const int* kinds, const double* values, const double* slopes,
                   const double* robin_w, const double* src_spatial, const double* src_time,
                   double* u);
+/* Same with the micro-solver chosen: PD_SOLVER_ADI runs PatchIntegrator::adi_sweep
+ * (microsim.cpp:334-507) with upwind order PD_UPWIND_* and parameter r; src_time
+ * then holds time(t0 + (s+1/2) dt)/l. */
+int pdo_integrate_ex(const double* coef, int nx, int ny, int nt, double h_xi, double h_eta,
+                     double tau, const int* kinds, const double* values, const double* slopes,
+                     const double* robin_w, const double* src_spatial, const double* src_time,
+                     double* u, int solver, int upwind_order, double upwind_r);
 
 /* Engine-level restatements over the same descriptor as pd_engine_create. */
 int pdo_gaptooth_step(const pd_engine_desc* d, const double* U_in, double* U_out, double t,

@@ -67,7 +67,11 @@ inline cpi::SchemeConfig scheme_from(const pd_problem_desc& d) {
     s.nx = d.nx;
     s.ny = d.ny;
     s.nt = d.nt;
-    s.solver = cpi::SchemeConfig::Solver::Explicit;
+    s.solver = d.solver == PD_SOLVER_ADI ? cpi::SchemeConfig::Solver::ADI : cpi::SchemeConfig::Solver::Explicit;
+    s.upwind.order = d.upwind_order == PD_UPWIND_FOUR    ? microsim::UpwindOrder::Four
+                     : d.upwind_order == PD_UPWIND_THREE ? microsim::UpwindOrder::Three
+                                                         : microsim::UpwindOrder::Two;
+    s.upwind.r = d.upwind_r;
     s.bc_type = d.bc_type == PD_BC_DIRICHLET ? cpi::SchemeConfig::BCType::Dirichlet
               : d.bc_type == PD_BC_ROBIN     ? cpi::SchemeConfig::BCType::Robin
                                              : cpi::SchemeConfig::BCType::Neumann;
@@ -205,6 +209,9 @@ inline Built build(const pd_problem_desc& d) {
             break;
         case PD_PROBLEM_REF_CDR:
             p = problems::problem1_constant(d.lambda);
+            break;
+        case PD_PROBLEM_REF_CDR_VAR:
+            p = problems::problem1_variable(d.lambda);
             break;
         case PD_PROBLEM_STEADY: {
             p.name = "steady";

@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-PD_ABI_VERSION = 1
+PD_ABI_VERSION = 2
 
 # pd_status  (errors.hpp:9-61 mapping)
 PD_OK = 0
@@ -33,6 +33,8 @@ PD_QUAD_TRAPEZOID, PD_QUAD_SIMPSON = 0, 1
 PD_SOURCE_ZERO, PD_SOURCE_SEPARABLE = 0, 1
 PD_MODE_FAST, PD_MODE_EXACT = 0, 1
 PD_STEP_DIRECT, PD_STEP_LINEAR = 0, 1
+PD_SOLVER_EXPLICIT, PD_SOLVER_ADI = 0, 1
+PD_UPWIND_TWO, PD_UPWIND_THREE, PD_UPWIND_FOUR = 0, 1, 2
 PD_COEF_A, PD_COEF_B, PD_COEF_C, PD_COEF_VX, PD_COEF_VY, PD_COEF_W = 0, 1, 2, 3, 4, 5
 PD_NCOEF = 6
 
@@ -42,6 +44,7 @@ PD_PROBLEM_ANNULUS_NONAXI = 3
 PD_PROBLEM_SHEAR_CDR = 4
 PD_PROBLEM_REF_ANNULUS = 10
 PD_PROBLEM_REF_CDR = 11
+PD_PROBLEM_REF_CDR_VAR = 13
 PD_PROBLEM_STEADY = 12
 PD_DT_GIVEN, PD_DT_DIFFUSION, PD_DT_METRIC = 0, 1, 2
 
@@ -61,6 +64,7 @@ class EngineDesc(C.Structure):
         ("ncoeff_sets", C.c_int32), ("coeff_set", _ip), ("coeffs", _dp),
         ("source_kind", C.c_int32), ("source_spatial", _dp), ("l", C.c_double),
         ("mode", C.c_int32),
+        ("solver", C.c_int32), ("upwind_order", C.c_int32), ("upwind_r", C.c_double),
     ]
 
 
@@ -84,6 +88,7 @@ class ProblemDesc(C.Structure):
         ("quadrature", C.c_int32), ("mode", C.c_int32),
         ("dt_rule", C.c_int32), ("h_frac", C.c_double), ("dt_over_tau", C.c_double),
         ("threads", C.c_int32),
+        ("solver", C.c_int32), ("upwind_order", C.c_int32), ("upwind_r", C.c_double),
     ]
 
 

@@ -22,12 +22,15 @@ KINDS = {
     "shear-cdr": abi.PD_PROBLEM_SHEAR_CDR,
     "ref-annulus": abi.PD_PROBLEM_REF_ANNULUS,
     "ref-cdr": abi.PD_PROBLEM_REF_CDR,
+    "ref-cdr-var": abi.PD_PROBLEM_REF_CDR_VAR,
     "steady": abi.PD_PROBLEM_STEADY,
 }
 BC = {"neumann": abi.PD_BC_NEUMANN, "dirichlet": abi.PD_BC_DIRICHLET, "robin": abi.PD_BC_ROBIN}
 QUAD = {"trapezoid": abi.PD_QUAD_TRAPEZOID, "simpson": abi.PD_QUAD_SIMPSON}
 DT = {"given": abi.PD_DT_GIVEN, "diffusion": abi.PD_DT_DIFFUSION, "metric": abi.PD_DT_METRIC}
 MODE = {"fast": abi.PD_MODE_FAST, "exact": abi.PD_MODE_EXACT}
+SOLVER = {"explicit": abi.PD_SOLVER_EXPLICIT, "adi": abi.PD_SOLVER_ADI}  # micro.solver (config.cpp:169-172)
+UPWIND = {"two": abi.PD_UPWIND_TWO, "three": abi.PD_UPWIND_THREE, "four": abi.PD_UPWIND_FOUR}  # config.cpp:173-179
 
 _SCHEMA = {
     "problem": {"kind": str, "lambda": float, "beta": float, "eps": float, "omega": float, "vel": float,
@@ -35,7 +38,8 @@ _SCHEMA = {
     "scheme": {"n_xi": int, "n_eta": int, "nt_macro": int, "k": int, "T": float, "tau": float,
                "h_xi": float, "h_eta": float, "h_frac": float, "dt_over_tau": float},
     "micro": {"nx": int, "ny": int, "nt": int, "dt_rule": str, "bc_type": str, "robin_w1": float,
-              "robin_w2": float, "quadrature": str, "mode": str},
+              "robin_w2": float, "quadrature": str, "mode": str, "solver": str, "upwind": str,
+              "upwind_r": float},
     "sweep": {"log2_patches": str, "micro_nodes": str, "K": str},
 }
 
@@ -56,6 +60,9 @@ def default_desc() -> ProblemDesc:
     d.nt = 2
     d.robin_w1 = d.robin_w2 = 1.0
     d.mode = abi.PD_MODE_FAST
+    d.solver = abi.PD_SOLVER_EXPLICIT  # the BASELINE configs' micro-solver (the reference's default is ADI)
+    d.upwind_order = abi.PD_UPWIND_TWO
+    d.upwind_r = 0.5  # UpwindSpec::r default (microsim.hpp:47)
     return d
 
 
@@ -82,7 +89,7 @@ def parse(text: str, origin: str = "<config>") -> tuple[ProblemDesc, dict]:
               "scheme.nt_macro": "Nt", "scheme.k": "k", "scheme.T": "T", "scheme.tau": "tau",
               "scheme.h_xi": "h_xi", "scheme.h_eta": "h_eta", "scheme.h_frac": "h_frac",
               "scheme.dt_over_tau": "dt_over_tau", "micro.nx": "nx", "micro.ny": "ny", "micro.nt": "nt",
-              "micro.robin_w1": "robin_w1", "micro.robin_w2": "robin_w2"}
+              "micro.robin_w1": "robin_w1", "micro.robin_w2": "robin_w2", "micro.upwind_r": "upwind_r"}
     for k, f in simple.items():
         if k in vals:
             setattr(d, f, vals[k])
@@ -94,6 +101,10 @@ def parse(text: str, origin: str = "<config>") -> tuple[ProblemDesc, dict]:
         d.quadrature = QUAD[vals["micro.quadrature"]]
     if "micro.mode" in vals:
         d.mode = MODE[vals["micro.mode"]]
+    if "micro.solver" in vals:
+        d.solver = SOLVER[vals["micro.solver"]]
+    if "micro.upwind" in vals:
+        d.upwind_order = UPWIND[vals["micro.upwind"]]
     return d, vals
 
 

@@ -145,11 +145,14 @@ pd_status pd_problem_source_time(const pd_problem* p, double t0, int32_t nsteps,
     if (s.source_zero || !s.source_time) return PD_UNSUPPORTED;
     const int k = p->cfg.k, nt = p->cfg.nt;
     const double dt = p->cfg.dt(), tau = p->cfg.tau, mdt = tau / nt, l = s.physical.l;
+    const bool adi = p->cfg.solver == pdb200::cpi::SchemeConfig::Solver::ADI;
     for (int n = 0; n < nsteps; ++n) {
         const double t = t0 + n * dt;
         for (int m = 0; m <= k; ++m) {
             const double tm = t + m * tau;
-            for (int q = 0; q < nt; ++q) out[(static_cast<size_t>(n) * (k + 1) + m) * nt + q] = s.source_time(tm + q * mdt) / l;
+            for (int q = 0; q < nt; ++q) // coefficient/source time of micro step q  microsim.cpp:536-537
+                out[(static_cast<size_t>(n) * (k + 1) + m) * nt + q] =
+                    s.source_time(adi ? tm + (q + 0.5) * mdt : tm + q * mdt) / l;
         }
     }
     return PD_OK;

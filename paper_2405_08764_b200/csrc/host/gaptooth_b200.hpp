@@ -190,7 +190,10 @@ public:
         std::vector<double> f(static_cast<size_t>(k + 1) * cfg_.nt);
         for (int m = 0; m <= k; ++m)
             for (int s = 0; s < cfg_.nt; ++s)
-                f[static_cast<size_t>(m) * cfg_.nt + s] = problem_.source_time((t + m * cfg_.tau) + s * mdt) / problem_.physical.l;
+                f[static_cast<size_t>(m) * cfg_.nt + s] =
+                    problem_.source_time(cfg_.solver == cpi::SchemeConfig::Solver::ADI ? (t + m * cfg_.tau) + (s + 0.5) * mdt
+                                                                                       : (t + m * cfg_.tau) + s * mdt) /
+                    problem_.physical.l;
         return f;
     }
 

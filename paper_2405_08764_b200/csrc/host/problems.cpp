@@ -45,16 +45,23 @@ using geometry::SecondDerivs;
 auto zero3 = [](double, double, double) { return 0.0; };
 auto zero2 = [](double, double) { return 0.0; };
 
-ProblemSpec ref_cdr(double lambda) {
-    // problems::problem1_constant  proj/src/problems.cpp:19-69 (lambda-stretched CDR,
-    // exact e^{x+y+t}, separable source (10x + 10y - 1) e^{x+y} * e^t)
+ProblemSpec ref_cdr(double lambda, bool variable) {
+    // problems::problem1_constant / problem1_variable  proj/src/problems.cpp:19-75
+    // (lambda-stretched CDR, exact e^{x+y+t}, separable source
+    // (c0 x + 10y - 1) e^{x+y} * e^t; variable: D = 1 + x, c0 = 8)
+    if (!(lambda >= 0.0 && lambda < 1.0)) {
+        std::ostringstream os;
+        os << "stretching parameter must lie in [0,1), got " << lambda;
+        throw InvalidStretch(os.str());
+    }
     ProblemSpec p;
-    p.name = "cdr-const";
+    p.name = variable ? "cdr-var" : "cdr-const";
     p.mapping = lambda == 0.0 ? geometry::identity_map() : geometry::stretched_map(lambda);
-    auto Dx = [](double, double, double) { return 1.0; };
+    auto Dx = [variable](double x, double, double) { return variable ? 1.0 + x : 1.0; };
     auto vx = [](double x, double, double) { return 10.0 * x; };
     auto vy = [](double, double y, double) { return 10.0 * y; };
-    auto src = [](double x, double y, double t) { return (10.0 * x + 10.0 * y - 1.0) * std::exp(x + y + t); };
+    const double c0 = variable ? 8.0 : 10.0;
+    auto src = [c0](double x, double y, double t) { return (c0 * x + 10.0 * y - 1.0) * std::exp(x + y + t); };
     p.physical = geometry::cdr_coefficients(Dx, Dx, vx, vy, src);
     const geometry::Mapping m = p.mapping;
     p.initial = [m](double xi, double eta) {
@@ -72,9 +79,9 @@ ProblemSpec ref_cdr(double lambda) {
     p.coeffs_time_independent = true;
     p.source_zero = false;
     p.source_separable = true;
-    p.source_spatial = [m](double xi, double eta) {
+    p.source_spatial = [m, c0](double xi, double eta) {
         const PhysPoint q = m.forward(xi, eta);
-        return (10.0 * q.x + 10.0 * q.y - 1.0) * std::exp(q.x + q.y);
+        return (c0 * q.x + 10.0 * q.y - 1.0) * std::exp(q.x + q.y);
     };
     p.source_time = [](double t) { return std::exp(t); };
     p.coeffs_xi_independent = false;
@@ -204,7 +211,9 @@ ProblemSpec from_desc(const pd_problem_desc& d) {
             return p;
         }
         case PD_PROBLEM_REF_CDR:
-            return ref_cdr(d.lambda);
+            return ref_cdr(d.lambda, false);
+        case PD_PROBLEM_REF_CDR_VAR:
+            return ref_cdr(d.lambda, true);
         case PD_PROBLEM_STEADY: { // harmonic u = x + y  (proj/tests/test_gaptooth.cpp:32-49)
             p.name = "steady";
             p.mapping = geometry::identity_map();
@@ -252,7 +261,6 @@ void SchemeConfig::validate(double xi_extent, double eta_extent) const {
         fail("Simpson restriction needs even nx and ny");
     if (bc_type == BCType::Robin && robin_w1 == 0.0 && robin_w2 == 0.0)
         fail("robin patch conditions need nonzero weights");
-    if (solver == Solver::ADI) throw Unsupported("the B200 path implements the explicit micro-solver only");
 }
 
 SchemeConfig scheme_from_desc(const pd_problem_desc& d) {
@@ -268,7 +276,11 @@ SchemeConfig scheme_from_desc(const pd_problem_desc& d) {
     s.nx = d.nx;
     s.ny = d.ny;
     s.nt = d.nt;
-    s.solver = SchemeConfig::Solver::Explicit;
+    s.solver = d.solver == PD_SOLVER_ADI ? SchemeConfig::Solver::ADI : SchemeConfig::Solver::Explicit;
+    s.upwind.order = d.upwind_order == PD_UPWIND_FOUR    ? microsim::UpwindOrder::Four
+                     : d.upwind_order == PD_UPWIND_THREE ? microsim::UpwindOrder::Three
+                                                         : microsim::UpwindOrder::Two;
+    s.upwind.r = d.upwind_r;
     s.bc_type = d.bc_type == PD_BC_DIRICHLET ? SchemeConfig::BCType::Dirichlet
               : d.bc_type == PD_BC_ROBIN     ? SchemeConfig::BCType::Robin
                                              : SchemeConfig::BCType::Neumann;
@@ -324,6 +336,11 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
     d.source_kind = p.source_zero ? PD_SOURCE_ZERO : PD_SOURCE_SEPARABLE;
     d.l = p.physical.l;
     d.mode = cfg.mode;
+    d.solver = cfg.solver == cpi::SchemeConfig::Solver::ADI ? PD_SOLVER_ADI : PD_SOLVER_EXPLICIT;
+    d.upwind_order = cfg.upwind.order == microsim::UpwindOrder::Four    ? PD_UPWIND_FOUR
+                     : cfg.upwind.order == microsim::UpwindOrder::Three ? PD_UPWIND_THREE
+                                                                        : PD_UPWIND_TWO;
+    d.upwind_r = cfg.upwind.r;
     if (d.l == 0.0) throw ValidationError("time-derivative multiplier l must be nonzero");
 
     // patch list: j outer, i inner (gaptooth.cpp:251-280)
@@ -421,6 +438,7 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
 }
 
 void check_stability(const EngineTables& t, const cpi::SchemeConfig& cfg) {
+    if (cfg.solver != cpi::SchemeConfig::Solver::Explicit) return; // guard of the explicit scheme only
     const double mdxi = cfg.h_xi / cfg.nx, mdeta = cfg.h_eta / cfg.ny;
     const double dt = cfg.tau / cfg.nt;
     const double dmin = std::min(mdxi, mdeta);

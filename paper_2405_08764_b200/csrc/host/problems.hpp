@@ -66,6 +66,15 @@ ProblemSpec from_desc(const pd_problem_desc& d);
 std::vector<double> seeded_field(int Nxi, int Neta, uint64_t seed, int sweeps);
 } // namespace problems
 
+namespace microsim {
+// UpwindSpec  proj/include/patchdyn/microsim.hpp:43-48 (ADI convection stencils)
+enum class UpwindOrder { Two, Three, Four };
+struct UpwindSpec {
+    UpwindOrder order = UpwindOrder::Two;
+    double r = 0.5; // modification weight of the four-point scheme
+};
+} // namespace microsim
+
 namespace cpi {
 struct SchemeConfig {
     int N_xi = 10, N_eta = 10;
@@ -76,7 +85,8 @@ struct SchemeConfig {
     double h_xi = 1e-3, h_eta = 1e-3;
     int nx = 10, ny = 10, nt = 2;
     enum class Solver { ADI, Explicit };
-    Solver solver = Solver::Explicit;
+    Solver solver = Solver::ADI; // the reference's default (scheme_config.hpp:19-20)
+    microsim::UpwindSpec upwind{};
     enum class BCType { Neumann, Dirichlet, Robin };
     BCType bc_type = BCType::Neumann;
     double robin_w1 = 1.0, robin_w2 = 1.0;

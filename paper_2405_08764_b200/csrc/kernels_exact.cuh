@@ -11,7 +11,14 @@ namespace pdb200::dev {
 constexpr int kExactThreads = 128;
 
 inline size_t exact_smem_bytes(const Params& p) {
-    return sizeof(double) * (2 * (size_t)p.N + 3 * 4 * (size_t)p.L + p.n1 + 11 + 4 * 6);
+    size_t d = 2 * (size_t)p.N + 3 * 4 * (size_t)p.L + p.n1 + 11 + 4 * 6;
+    if (p.solver == PD_SOLVER_ADI) d += (size_t)p.N + 6 * (size_t)p.L * p.L; // rhs field + line scratch
+    return sizeof(double) * d;
+}
+
+// ADI scratch behind the PatchSh region: rhs field [N], line scratch [L][6L]
+__device__ inline double* adi_scratch(double* sm, const Params& p) {
+    return sm + patch_smem_doubles(p.N, p.L, p.n1);
 }
 
 // Dirichlet edges pin their nodes from the start (microsim.cpp:521-530; W, E, S, N order)
@@ -114,7 +121,13 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
     const int set = cset ? cset[patch] : patch;
     const double* coef = coeffs + (size_t)set * PD_NCOEF * p.N;
     const double* sp = src_sp ? src_sp + (size_t)set * p.N : nullptr;
-    double* res = micro_loop_x(p, s, eg, coef, sp, src_time, p.mixed != 0);
+    double* res;
+    if (p.solver == PD_SOLVER_ADI) {
+        double* xs = adi_scratch(sm, p);
+        res = micro_loop_adi(p, s, eg, coef, sp, src_time, xs, xs + p.N);
+    } else {
+        res = micro_loop_x(p, s, eg, coef, sp, src_time, p.mixed != 0);
+    }
     const double avg = restrict_x(res, p.nx, p.ny, p.quad, s.row);
     if (threadIdx.x == 0) {
         const size_t node = (size_t)i * p.NF2 + j;
@@ -186,7 +199,13 @@ k_integrate_exact(Params p, const double* __restrict__ u0, const double* __restr
     const int set = cset ? cset[patch] : patch;
     const double* coef = coeffs + (size_t)set * PD_NCOEF * p.N;
     const double* sp = src_sp ? src_sp + (size_t)set * p.N : nullptr;
-    double* res = micro_loop_x(p, s, eg, coef, sp, src_time, p.mixed != 0);
+    double* res;
+    if (p.solver == PD_SOLVER_ADI) {
+        double* xs = adi_scratch(sm, p);
+        res = micro_loop_adi(p, s, eg, coef, sp, src_time, xs, xs + p.N);
+    } else {
+        res = micro_loop_x(p, s, eg, coef, sp, src_time, p.mixed != 0);
+    }
     for (int t = threadIdx.x; t < p.N; t += blockDim.x) uT[(size_t)patch * p.N + t] = res[t];
 }
 

@@ -33,6 +33,8 @@ struct Params {
     int P, nsets;
     int mixed;  // any B != 0
     int source; // PD_SOURCE_*
+    int solver, upwind_order; // PD_SOLVER_*, PD_UPWIND_* (ADI)
+    double upwind_r;
     // FAST-mode constants, computed once on the host (no divisions on the device)
     double i2Dxi, i2Deta, iDxi2, iDeta2, i4DD; // 1/(2D), 1/D^2, 1/(4 Dxi Deta)
     double c24x, c24y;                          // h^2/24 (box-average constant of the lift)

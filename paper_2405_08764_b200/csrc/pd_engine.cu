@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "kernels_adi.cuh"
 #include "kernels_exact.cuh"
 #include "kernels_fast.cuh"
 #include "kernels_fast_big.cuh"
@@ -174,6 +175,14 @@ void validate_desc(const pd_engine_desc* d) {
     if (d->bc_type == PD_BC_ROBIN && d->robin_w1 == 0.0 && d->robin_w2 == 0.0)
         bad("robin patch conditions need nonzero weights");
     if (d->source_kind == PD_SOURCE_SEPARABLE && !d->source_spatial) bad("separable source needs a spatial table");
+    if (d->solver != PD_SOLVER_EXPLICIT && d->solver != PD_SOLVER_ADI) bad("unknown micro-solver");
+    if (d->upwind_order < PD_UPWIND_TWO || d->upwind_order > PD_UPWIND_FOUR) bad("upwind order must be two, three or four");
+    // the reference sizes its banded line matrix once per ADI step for the xi
+    // lines (microsim.cpp:400, 431-432) and reuses it for the eta lines: only
+    // square micro grids are well defined with the wide upwind stencils
+    if (d->solver == PD_SOLVER_ADI && d->upwind_order != PD_UPWIND_TWO && d->nx != d->ny)
+        throw Status{PD_UNSUPPORTED, "ADI with three/four-point upwinding needs nx == ny (the reference's banded "
+                                     "line matrix is sized for the xi lines only)"};
 }
 
 Params make_params(const pd_engine_desc& d, int P) {
@@ -238,6 +247,9 @@ Params make_params(const pd_engine_desc& d, int P) {
     p.gsc[PD_EDGE_W] = -2.0 * p.mdxi;
     p.gsc[PD_EDGE_N] = 2.0 * p.mdeta;
     p.gsc[PD_EDGE_S] = -2.0 * p.mdeta;
+    p.solver = d.solver;
+    p.upwind_order = d.upwind_order;
+    p.upwind_r = d.upwind_r;
     return p;
 }
 
@@ -329,11 +341,13 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             }
         }
         p.mixed = mixed ? 1 : 0;
+        if (mixed && d.solver == PD_SOLVER_ADI)
+            throw Status{PD_MIXED_TERM_UNSUPPORTED, "mixed-derivative term with the ADI micro-solver is not defined"};
         if (mixed && d.bc_type == PD_BC_ROBIN)
             throw Status{PD_MIXED_TERM_UNSUPPORTED, "mixed-derivative term with Robin patch conditions is not defined"};
         const double dmin = std::min(p.mdxi, p.mdeta);
         const double number = max_ac * p.mdt / (dmin * dmin);
-        if (number > 0.5 + 1e-12) {
+        if (d.solver == PD_SOLVER_EXPLICIT && number > 0.5 + 1e-12) { // the guard is the explicit scheme's
             std::ostringstream m;
             m << "explicit micro scheme diffusive stability number " << number << " exceeds 0.5";
             throw Status{PD_STABILITY_VIOLATION, m.str()};
@@ -364,7 +378,13 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
         e->device_bytes = Ncoef * 8 + e->pij.size() * 4 + e->nbr.size() * 4 + 2 * e->NF * 8;
         // kernel family
         e->mode = PD_MODE_EXACT;
-        if (d.mode == PD_MODE_FAST && d.source_kind == PD_SOURCE_ZERO) {
+        if (exact_smem_bytes(p) > 48 * 1024) {
+            CUDA_TRY(cudaFuncSetAttribute(k_gaptooth_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)exact_smem_bytes(p)));
+            CUDA_TRY(cudaFuncSetAttribute(k_integrate_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)exact_smem_bytes(p)));
+        }
+        if (d.mode == PD_MODE_FAST && d.source_kind == PD_SOURCE_ZERO && d.solver == PD_SOLVER_EXPLICIT) {
             if (plan_big(p, e->fast)) {
                 const size_t wcount = fast_weights_count(e->fast, p);
                 e->d_weights.alloc(wcount);

@@ -3,6 +3,7 @@
 
   python tests/golden/make_golden.py            (all fixtures)
   python tests/golden/make_golden.py linear     (ref_linear.npz only)
+  python tests/golden/make_golden.py adi        (table1_cdr.npz, ref_adi.npz only)
 
 ref_finals.npz      configs 1-3: initial field, first projective step and the
                     full-run final field computed by the UNMODIFIED reference
@@ -15,6 +16,11 @@ c4_small.npz        config-4 equation on 32x32 patches, 100 macro steps, by the
                     itself rejects b != 0 — parity unpinned by the reference).
 c4_sample.npz       full-size config 4: one gap-tooth substep on 1024 sampled
                     patches by the restated oracle.
+table1_cdr.npz      the reference's shipped Table-1 output (proj/out/table1/snapshots,
+                    problem1_constant(0) with the ADI micro-solver) as arrays.
+ref_adi.npz         ADI micro-solver variants (upwind two/three/four, Neumann/
+                    Dirichlet/Robin patch conditions, k = 1, nx != ny) run by
+                    the unmodified reference: 40 macro steps each.
 ref_linear.npz      configs 1 and 3 with the reference's DEFAULT linear_cache=auto:
                     GapToothEngine::step takes the linear-response shortcut
                     (gaptooth.cpp:377-418); first projective step and final
@@ -82,6 +88,42 @@ def ref_linear(ref):
         out[f"{name}_maxpct"] = np.array(err)
         print(f"{name}: reference linear-cache run {sec:.3f} s")
     np.savez_compressed(OUT / "ref_linear.npz", **out)
+
+
+ADI_CASES = {
+    # name: config overrides of configs/ref_table1_cdr_const.cfg
+    "const_two": {},
+    "const_l03_three": {"lambda_": 0.3, "upwind_order": 1},
+    "var_l03_four": {"problem": 13, "lambda_": 0.3, "upwind_order": 2, "upwind_r": 0.3},
+    "var_dirichlet_two": {"problem": 13, "bc_type": 1},
+    "const_robin_three": {"bc_type": 2, "robin_w1": 2.0, "robin_w2": 1.0, "upwind_order": 1},
+    "var_k1_two": {"problem": 13, "k": 1},
+    "const_nx10_ny14_two": {"ny": 14, "lambda_": 0.2},
+}
+ADI_STEPS = 40
+
+
+def table1():
+    arrs = {}
+    for p in sorted(Path("/root/reference/proj/out/table1/snapshots").glob("t_*.snap")):
+        t, U = read_snap(p)
+        arrs[f"t_{t:.6f}"] = U
+    np.savez_compressed(OUT / "table1_cdr.npz", **arrs)
+    print("table1 snapshots:", list(arrs))
+
+
+def ref_adi(ref):
+    base, _ = configs.load("ref_table1_cdr_const")
+    out = {}
+    for name, over in ADI_CASES.items():
+        prob = Problem(configs.copy_desc(base, **over))
+        R = ref.engine(prob.desc)
+        U0 = R.initial_field()
+        U, sec = R.steps(U0, 0, ADI_STEPS)
+        out[f"{name}_U0"] = U0
+        out[f"{name}_final"] = U
+        print(f"adi {name}: {sec * 1e3:.1f} ms")
+    np.savez_compressed(OUT / "ref_adi.npz", **out)
 
 
 def annulus():
@@ -156,8 +198,14 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["linear"]:
         ref_linear(ref)
         sys.exit(0)
+    if sys.argv[1:] == ["adi"]:
+        table1()
+        ref_adi(ref)
+        sys.exit(0)
     ref_finals(ref)
     ref_linear(ref)
+    table1()
+    ref_adi(ref)
     annulus()
     c4(O)
     unit_cases(ref)

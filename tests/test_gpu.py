@@ -459,3 +459,55 @@ def test_linear_run_guard_trips_like_oracle(N, restated, gpu):
     assert (stats.failed_step, stats.steps_done, stats.failed_nonfinite) == (so.failed_step, so.steps_done,
                                                                              so.failed_nonfinite)
     assert np.array_equal(U, Uo)
+
+
+# ---------------------------------------------------------------------------
+# ADI micro-solver (the reference's default solver, behind its Tables 1-3)
+# ---------------------------------------------------------------------------
+ADI = np.load(GOLDEN / "ref_adi.npz")
+ADI_CASES = {
+    "const_two": {},
+    "const_l03_three": {"lambda_": 0.3, "upwind_order": abi.PD_UPWIND_THREE},
+    "var_l03_four": {"problem": abi.PD_PROBLEM_REF_CDR_VAR, "lambda_": 0.3, "upwind_order": abi.PD_UPWIND_FOUR,
+                     "upwind_r": 0.3},
+    "var_dirichlet_two": {"problem": abi.PD_PROBLEM_REF_CDR_VAR, "bc_type": abi.PD_BC_DIRICHLET},
+    "const_robin_three": {"bc_type": abi.PD_BC_ROBIN, "robin_w1": 2.0, "robin_w2": 1.0,
+                          "upwind_order": abi.PD_UPWIND_THREE},
+    "var_k1_two": {"problem": abi.PD_PROBLEM_REF_CDR_VAR, "k": 1},
+    "const_nx10_ny14_two": {"ny": 14, "lambda_": 0.2},
+}
+
+
+@pytest.mark.parametrize("name", list(ADI_CASES))
+def test_adi_bit_exact_vs_reference(name, gpu):
+    P = load("ref_table1_cdr_const", **ADI_CASES[name])
+    E = Engine.from_problem(P, mode=FAST)  # ADI runs on the EXACT family whatever is asked
+    assert E.mode == EXACT
+    U0 = ADI[f"{name}_U0"]
+    n = 40
+    U, stats = E.run(U0, n, bnd=P.boundary_table(0.0, n), src_time=P.source_time(0.0, n))
+    assert stats.steps_done == n
+    assert np.array_equal(U, ADI[f"{name}_final"])
+
+
+def test_adi_reproduces_shipped_table1_output(gpu):
+    """proj/out/table1: problem1_constant(0), ADI, nt = 2, 1001 macro steps —
+    every shipped snapshot reproduced bit for bit."""
+    gold = np.load(GOLDEN / "table1_cdr.npz")
+    P = load("ref_table1_cdr_const")
+    E = Engine.from_problem(P)
+    U, done, Nt = P.initial_field(), 0, P.desc.Nt
+    dt = P.desc.T / Nt
+    # tables for the whole run: macro step n at t = n*dt exactly as cpi::run (cpi.cpp:176)
+    bnd, src = P.boundary_table(0.0, Nt), P.source_time(0.0, Nt)
+    for key in sorted(gold.files):
+        target = int(round(float(key[2:]) / dt))
+        U, _ = E.run(U, target - done, t0=done * dt, bnd=bnd[done:target], src_time=src[done:target])
+        done = target
+        assert np.array_equal(U, gold[key]), key
+
+
+def test_adi_rejects_wide_upwind_on_rectangular_patches(gpu):
+    P = load("ref_table1_cdr_const", ny=12, upwind_order=abi.PD_UPWIND_THREE)
+    with pytest.raises(PatchdynError, match="nx == ny"):
+        Engine.from_problem(P)
