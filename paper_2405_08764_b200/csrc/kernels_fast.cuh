@@ -187,9 +187,29 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     const double* gN = sg[gs][PD_EDGE_N];
     const double* gS = sg[gs][PD_EDGE_S];
     if constexpr (MIXED) {
-        for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
-            int e, k;
-            sg[gs][4 + e_of_ring<N1, N2>(t, e, k)][k] = ring_offset<N1, N2>(gE, gW, gN, gS, t);
+        if constexpr (LP == 32) { // one patch per warp: closed form (measured faster at 16x16)
+            for (int t = r; t < 2 * N2 + 2 * N1; t += LP) {
+                int e, k;
+                sg[gs][4 + e_of_ring<N1, N2>(t, e, k)][k] = ring_offset<N1, N2>(gE, gW, gN, gS, t);
+            }
+        } else { // several patches per warp: generic corner rule (measured faster at 8x8)
+            auto off = [&](int pp, int qq) {
+                const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
+                const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
+                double o = 0.0;
+                if (pp < 0) o += gW[qc];
+                if (pp > N1 - 1) o += gE[qc];
+                if (qq < 0) o += gS[pc];
+                if (qq > N2 - 1) o += gN[pc];
+                return o;
+            };
+            for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
+                int e, k;
+                e_of_ring<N1, N2>(t, e, k);
+                const int i = e == PD_EDGE_E ? N1 - 1 : e == PD_EDGE_W ? 0 : k;
+                const int j = e == PD_EDGE_N ? N2 - 1 : e == PD_EDGE_S ? 0 : k;
+                sg[gs][4 + e][k] = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
+            }
         }
         __syncwarp();
     }
