@@ -1,0 +1,223 @@
+"""Multi-process slab decomposition of the macro loop.
+
+Within one gap-tooth substep the patches are independent; across substeps each
+patch needs its 3x3 macro stencil (gaptooth.cpp:74-104).  So the patch columns
+i in [i_lo, Nxi-1] are split into contiguous xi-slabs, one per rank; every rank
+keeps a full-size macro field buffer but only its own columns (plus one halo
+column on each side, and the global boundary) are ever current.  Per substep:
+
+  1. the rank's engine advances its own patches (the fused device step);
+  2. the two edge columns go to the neighbouring ranks and the two halo columns
+     come back (one macro column = Neta+1 contiguous doubles in the i-major
+     Field2D layout, field.hpp:20-27; periodic xi wraps rank 0 <-> rank N-1);
+  3. the blow-up guard (cpi.cpp:187-202) reduces max |U| over ranks (one
+     all-reduce of a single double).
+
+Results do not depend on the decomposition: every patch value is computed from
+the same stencil values in the same arithmetic, so the sharded run equals the
+single-engine run bit for bit (tests/test_dist.py).  The exchange uses
+torch.distributed point-to-point ops — NCCL over NVLink on GPUs, gloo on CPU.
+
+The compute is injected (``step_fn``): the product wiring (``device_step_fn``)
+runs the engine's fused projective step on device buffers; the CPU tests pass
+the restated oracle.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .abi import EngineDesc
+
+
+@dataclass
+class Slab:
+    rank: int
+    world: int
+    i0: int  # first owned patch column
+    i1: int  # one past the last owned patch column
+    periodic: bool
+    Nxi: int
+
+    def left(self) -> int | None:
+        """Rank owning column i0-1 (None: the global boundary)."""
+        if self.rank > 0:
+            return self.rank - 1
+        return self.world - 1 if self.periodic and self.world > 1 else None
+
+    def right(self) -> int | None:
+        if self.rank < self.world - 1:
+            return self.rank + 1
+        return 0 if self.periodic and self.world > 1 else None
+
+
+def slabs(Nxi: int, periodic: bool, world: int) -> list[Slab]:
+    """Contiguous, balanced xi-slabs of the patch columns (gaptooth.cpp:251-280)."""
+    i_lo, i_hi = (0 if periodic else 1), Nxi - 1
+    ncol = i_hi - i_lo + 1
+    if world > ncol:
+        raise ValueError(f"{world} ranks for {ncol} patch columns")
+    out, start = [], i_lo
+    for r in range(world):
+        n = ncol // world + (1 if r < ncol % world else 0)
+        out.append(Slab(r, world, start, start + n, periodic, Nxi))
+        start += n
+    return out
+
+
+def subset_desc(ed: EngineDesc, slab: Slab) -> EngineDesc:
+    """pd_engine_desc restricted to the slab's patches (reference order kept),
+    with only the coefficient sets those patches use."""
+    P = ed.npatches
+    pij = np.ctypeslib.as_array(ed.patch_ij, shape=(P, 2)).copy()
+    sel = np.nonzero((pij[:, 0] >= slab.i0) & (pij[:, 0] < slab.i1))[0]
+    cset = np.ctypeslib.as_array(ed.coeff_set, shape=(P,)).copy() if ed.coeff_set else np.arange(P, dtype=np.int32)
+    used, remap = np.unique(cset[sel], return_inverse=True)
+    n1, n2 = ed.nx + 1, ed.ny + 1
+    per_set = abi.PD_NCOEF * n1 * n2
+    coeffs = np.ctypeslib.as_array(ed.coeffs, shape=(ed.ncoeff_sets * per_set,))
+    sub_coef = np.ascontiguousarray(coeffs.reshape(ed.ncoeff_sets, per_set)[used])
+    sub_pij = np.ascontiguousarray(pij[sel].astype(np.int32))
+    sub_cset = np.ascontiguousarray(remap.astype(np.int32))
+    d = EngineDesc()
+    for f, _ in EngineDesc._fields_:
+        setattr(d, f, getattr(ed, f))
+    d.npatches = len(sel)
+    d.patch_ij = sub_pij.ctypes.data_as(abi._ip)
+    d.ncoeff_sets = len(used)
+    d.coeff_set = sub_cset.ctypes.data_as(abi._ip)
+    d.coeffs = sub_coef.ctypes.data_as(abi._dp)
+    if ed.source_kind == abi.PD_SOURCE_SEPARABLE and ed.source_spatial:
+        sp = np.ctypeslib.as_array(ed.source_spatial, shape=(ed.ncoeff_sets * n1 * n2,))
+        sub_sp = np.ascontiguousarray(sp.reshape(ed.ncoeff_sets, n1 * n2)[used])
+        d.source_spatial = sub_sp.ctypes.data_as(abi._dp)
+        d._keep_sp = sub_sp
+    d._keep = (sub_pij, sub_cset, sub_coef, ed)
+    return d
+
+
+class ShardedRun:
+    """The cpi::run macro loop (cpi.cpp:175-202) over xi-slabs.
+
+    step_fn(U_in, U_out, t, bnd) -> None advances the rank's own patches by one
+    projective step (k+1 substeps + extrapolation + boundary refresh) on
+    full-size field buffers (numpy arrays or torch tensors, 1-D, length NF).
+    """
+
+    def __init__(self, slab: Slab, Neta: int, step_fn, dist, group=None, stage_cpu: bool = False):
+        self.s = slab
+        self.n2 = Neta + 1
+        self.step_fn = step_fn
+        self.dist = dist
+        self.group = group
+        self.stage_cpu = stage_cpu  # device buffers over a CPU-only transport (gloo): copy columns through the host
+
+    def _col(self, U, i):
+        return U[i * self.n2:(i + 1) * self.n2]
+
+    def exchange(self, U):
+        """Own edge columns out, halo columns in.  Per neighbour pair the
+        messages are ordered (rightward first, then leftward) on both sides,
+        so the exchange is unambiguous even when left == right (2 ranks,
+        periodic) and with NCCL, whose point-to-point ops carry no tags."""
+        import torch
+
+        s, d = self.s, self.dist
+        Nxi = s.Nxi
+        left, right = s.left(), s.right()
+        ops, recv = [], []
+        stage = (lambda x: x.cpu()) if self.stage_cpu else (lambda x: x.contiguous())
+        if right is not None:  # my last column is my right neighbour's left halo
+            ops.append(d.P2POp(d.isend, stage(self._col(U, s.i1 - 1)), right, self.group))
+        if left is not None:  # my first column is my left neighbour's right halo
+            ops.append(d.P2POp(d.isend, stage(self._col(U, s.i0)), left, self.group))
+        if left is not None:
+            buf = stage(torch.empty_like(self._col(U, s.i0)))
+            ops.append(d.P2POp(d.irecv, buf, left, self.group))
+            recv.append(((s.i0 - 1) % Nxi if s.periodic else s.i0 - 1, buf))
+        if right is not None:
+            buf = stage(torch.empty_like(self._col(U, s.i0)))
+            ops.append(d.P2POp(d.irecv, buf, right, self.group))
+            recv.append((s.i1 % Nxi if s.periodic else s.i1, buf))
+        if ops:
+            for r in d.batch_isend_irecv(ops):
+                r.wait()
+        for i, buf in recv:
+            buf = buf.to(U.device)
+            U[i * self.n2:(i + 1) * self.n2] = buf
+            if s.periodic and i == 0:  # the seam column mirrors column 0
+                U[s.Nxi * self.n2:(s.Nxi + 1) * self.n2] = buf
+
+    def owned_max(self, U):
+        """max |U| over the rank's patch columns and the global boundary: over
+        all ranks this covers every node once (the guard's scope, cpi.cpp:187-202)."""
+        import torch
+
+        s = self.s
+        V = U.view(-1, self.n2)
+        parts = [V[s.i0:s.i1].abs().max(), V[:, 0].abs().max(), V[:, -1].abs().max()]
+        if not s.periodic:  # W/E boundary columns (periodic: column 0 is a patch column, Nxi its seam copy)
+            parts += [V[0].abs().max(), V[-1].abs().max()]
+        return torch.stack(parts).max()
+
+    def run(self, U, nsteps: int, dt: float, t0: float = 0.0, bnd_table=None):
+        """U: this rank's full-size field (halo columns current).  Returns
+        (U, steps_done, failed_step) with cpi.cpp:187-202's guard over all ranks."""
+        import torch
+
+        d = self.dist
+        red = (lambda x: x.cpu()) if self.stage_cpu else (lambda x: x)
+        m0 = red(self.owned_max(U).reshape(1).clone())
+        d.all_reduce(m0, op=d.ReduceOp.MAX, group=self.group)
+        blowup = 10.0 * max(float(m0.item()), 1e-12)
+        nxt = U.clone()  # columns a rank never computes stay finite
+        for n in range(nsteps):
+            self.step_fn(U, nxt, t0 + n * dt, None if bnd_table is None else bnd_table[n])
+            self.exchange(nxt)
+            m = red(self.owned_max(nxt).reshape(1).clone())
+            d.all_reduce(m, op=d.ReduceOp.MAX, group=self.group)
+            U, nxt = nxt, U
+            mv = float(m.item())
+            if not np.isfinite(mv) or mv > blowup:
+                return U, n, n + 1
+        return U, nsteps, 0
+
+    def gather(self, U):
+        """Assemble the full field on every rank from each rank's own columns."""
+        import torch
+
+        d, s = self.dist, self.s
+        V = U.view(-1, self.n2)
+        mine = torch.zeros(s.Nxi + 1, dtype=torch.bool, device=U.device)
+        mine[s.i0:s.i1] = True
+        part = torch.where(mine[:, None], V, torch.zeros_like(V))
+        if self.stage_cpu:
+            part = part.cpu()
+        d.all_reduce(part, op=d.ReduceOp.SUM, group=self.group)
+        part = part.to(U.device)
+        owned = torch.zeros_like(mine)
+        for sl in slabs(s.Nxi, s.periodic, s.world):
+            owned[sl.i0:sl.i1] = True
+        out = torch.where(owned[:, None], part, V)  # boundary columns are identical on every rank
+        if s.periodic:
+            out[s.Nxi] = out[0]
+        return out.reshape(-1)
+
+
+def device_step_fn(engine, k: int, perim: int, device):
+    """The product step: the engine's fused projective step on device buffers
+    (pd_projective_step_device); the boundary table row is uploaded per step."""
+    import torch
+
+    def step(U_in, U_out, t, bnd):
+        b = None
+        if bnd is not None:
+            b = torch.as_tensor(np.ascontiguousarray(bnd).reshape(-1), device=device)
+        from .engine import _check, lib
+
+        _check(lib().pd_projective_step_device(engine.h, U_in.data_ptr(), U_out.data_ptr(), t,
+                                               None if b is None else b.data_ptr(), None), engine.h)
+
+    return step

@@ -41,3 +41,66 @@ def test_replica_value_uses_max_over_ranks():
         vals = dict(out)
     expect = world * 1_000_000 / (15.0e-3)
     assert vals[0] == pytest.approx(expect) and vals[1] == pytest.approx(expect)
+
+
+# ---------------------------------------------------------------------------
+# xi-slab decomposition of the macro loop (paper_2405_08764_b200/sharded.py):
+# the sharded run equals the single-engine run bit for bit (restated oracle as
+# the per-rank compute, gloo point-to-point for the halo columns).
+# ---------------------------------------------------------------------------
+def _shard_worker(rank, world, port, name, over, nsteps, out):
+    import numpy as np
+    import torch
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.pyoracle import Restated
+    from paper_2405_08764_b200 import configs, sharded
+    from paper_2405_08764_b200.engine import Problem
+
+    O = Restated(threads=1)
+    P = Problem(configs.copy_desc(configs.load(name)[0], **over))
+    ed = P.engine_desc()
+    sl = sharded.slabs(ed.Nxi, bool(ed.periodic_xi), world)[rank]
+    sub = sharded.subset_desc(ed, sl)
+
+    def step(U_in, U_out, t, bnd):
+        st, o = O.projective_step(sub, U_in.numpy(), t, bnd)
+        assert st == 0
+        U_out.copy_(torch.from_numpy(o))
+
+    runner = sharded.ShardedRun(sl, ed.Neta, step, dist)
+    U0 = torch.from_numpy(P.initial_field().reshape(-1).copy())
+    dt = P.desc.T / P.desc.Nt
+    U, done, failed = runner.run(U0, nsteps, dt, 0.0, P.boundary_table(0.0, nsteps))
+    full = runner.gather(U)
+    out[rank] = (full.numpy().copy(), done, failed)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,over,world", [("c1_diffusion", {}, 2), ("c1_diffusion", {}, 3),
+                                             ("c3_annulus", {}, 2), ("c3_annulus", {}, 3),
+                                             ("c1_diffusion", {"dt_over_tau": 1000, "Nt": 50}, 2)])
+def test_sharded_run_equals_single_engine(name, over, world):
+    import numpy as np
+
+    from oracle.pyoracle import Restated
+    from paper_2405_08764_b200 import configs
+    from paper_2405_08764_b200.engine import Problem
+
+    nsteps = 20 if "Nt" not in over else 50
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_shard_worker, args=(world, port, name, over, nsteps, out), nprocs=world, join=True)
+        res = dict(out)
+    P = Problem(configs.copy_desc(configs.load(name)[0], **over))
+    ed = P.engine_desc()
+    st, Uref, stats = Restated(threads=1).run(ed, P.initial_field(), nsteps, 0.0, P.boundary_table(0.0, nsteps))
+    for r in range(world):
+        U, done, failed = res[r]
+        if st == 0:
+            assert failed == 0 and done == nsteps
+            assert np.array_equal(U.reshape(P.shape), Uref)
+        else:  # the guard trips at the same macro step on every rank
+            assert failed == stats.failed_step and done == stats.steps_done

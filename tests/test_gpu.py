@@ -511,3 +511,62 @@ def test_adi_rejects_wide_upwind_on_rectangular_patches(gpu):
     P = load("ref_table1_cdr_const", ny=12, upwind_order=abi.PD_UPWIND_THREE)
     with pytest.raises(PatchdynError, match="nx == ny"):
         Engine.from_problem(P)
+
+
+# ---------------------------------------------------------------------------
+# xi-slab decomposition with device engines (sharded.py): two ranks sharing the
+# one GPU, gloo transport with host-staged halo columns; the kernels never wait
+# on each other, each rank advances its own patches.
+# ---------------------------------------------------------------------------
+def _gpu_shard_worker(rank, world, port, name, mode, nsteps, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_08764_b200 import configs, sharded
+    from paper_2405_08764_b200.engine import Engine, Problem
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    P = Problem(configs.load(name)[0])
+    ed = P.engine_desc()
+    sl = sharded.slabs(ed.Nxi, bool(ed.periodic_xi), world)[rank]
+    E = Engine(sharded.subset_desc(ed, sl), mode)
+    dev = torch.device("cuda", 0)
+    step = sharded.device_step_fn(E, P.desc.k, E.perim, dev)
+
+    def step_sync(U_in, U_out, t, bnd):
+        step(U_in, U_out, t, bnd)
+        torch.cuda.synchronize()
+
+    runner = sharded.ShardedRun(sl, ed.Neta, step_sync, dist, stage_cpu=True)
+    U0 = torch.from_numpy(P.initial_field().reshape(-1).copy()).to(dev)
+    U, done, failed = runner.run(U0, nsteps, P.desc.T / P.desc.Nt, 0.0, P.boundary_table(0.0, nsteps))
+    out[rank] = (runner.gather(U).cpu().numpy(), done, failed, E.P)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["c1_diffusion", "c3_annulus"])
+@pytest.mark.parametrize("mode", [EXACT, FAST], ids=["exact", "fast"])
+def test_sharded_device_run_equals_single_engine(name, mode, gpu):
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    nsteps, world = 20, 2
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_gpu_shard_worker, args=(world, port, name, mode, nsteps, out), nprocs=world, join=True)
+        res = dict(out)
+    P = load(name)
+    E = Engine.from_problem(P, mode=mode)
+    Uref, _ = E.run(P.initial_field(), nsteps, bnd=P.boundary_table(0.0, nsteps))
+    assert sum(res[r][3] for r in range(world)) == E.P  # the slabs partition the patches
+    for r in range(world):
+        U, done, failed, _ = res[r]
+        assert failed == 0 and done == nsteps
+        assert np.array_equal(U.reshape(P.shape), Uref)
