@@ -80,6 +80,7 @@ struct pd_engine {
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
     DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
+    bool subset = false;                // the patch list covers only part of the interior
     DevBuf<unsigned long long> d_slot;
     DevBuf<unsigned int> d_counter;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -120,7 +121,14 @@ struct pd_engine {
     }
 
     // gap-tooth step (step_direct, gaptooth.cpp:360-375)
+    // A patch subset (one slab of a decomposed run) leaves other patch nodes
+    // untouched by the kernels: copy them through so out = in outside the
+    // subset (CoarseField out = F, gaptooth.cpp:361).
+    void copy_through(const double* in, double* out) {
+        if (subset && in != out) CUDA_TRY(cudaMemcpyAsync(out, in, NF * 8, cudaMemcpyDeviceToDevice, stream));
+    }
     void gaptooth_step_dev(const double* in, double* out, const double* bnd, const double* srct, const int* fail) {
+        copy_through(in, out);
         launch_step(in, out, OUT_FIELD, srct, fail);
         launch_refresh(out, in, bnd, fail);
     }
@@ -128,6 +136,7 @@ struct pd_engine {
     // projective step (cpi.cpp:58-77).  bnd: [k+2][perim] or null; srct [k+1][nt] or null.
     void projective_dev(const double* in, double* out, const double* bnd, const double* srct, const int* fail) {
         const int k = prm.k;
+        copy_through(in, out);
         if (k == 0) {
             launch_step(in, out, OUT_PROJECTIVE, srct, fail);
             launch_refresh(out, in, bnd ? bnd + perim : nullptr, fail);
@@ -137,6 +146,7 @@ struct pd_engine {
         const double* prev = in;
         for (int m = 0; m <= k; ++m) {
             double* nxt = d_chain.p + NF * m;
+            copy_through(prev, nxt);
             launch_step(prev, nxt, OUT_FIELD, srct ? srct + (size_t)prm.nt * m : nullptr, fail);
             launch_refresh(nxt, prev, bnd ? bnd + perim * m : nullptr, fail);
             prev = nxt;
@@ -353,6 +363,7 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             throw Status{PD_STABILITY_VIOLATION, m.str()};
         }
         e->NF = (size_t)(d.Nxi + 1) * (d.Neta + 1);
+        e->subset = P < (d.Nxi - (d.periodic_xi ? 0 : 1)) * (d.Neta - 1);
         e->perim = pd_perimeter_len(d.Nxi, d.Neta);
         // device
         CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));

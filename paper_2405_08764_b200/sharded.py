@@ -106,7 +106,11 @@ class ShardedRun:
     full-size field buffers (numpy arrays or torch tensors, 1-D, length NF).
     """
 
-    def __init__(self, slab: Slab, Neta: int, step_fn, dist, group=None, stage_cpu: bool = False):
+    def __init__(self, slab: Slab, Neta: int, step_fn, dist, group=None, stage_cpu: bool = False, k: int = 0):
+        if k != 0:
+            # k > 0 chains substeps inside one projective step; their halo
+            # columns would have to be exchanged after every substep
+            raise NotImplementedError("the xi-slab runner exchanges halos once per projective step (k = 0 only)")
         self.s = slab
         self.n2 = Neta + 1
         self.step_fn = step_fn

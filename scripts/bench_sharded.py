@@ -35,7 +35,7 @@ E = Engine(sharded.subset_desc(ed, sl))
 stream = torch.cuda.current_stream(dev)
 _check(lib().pd_engine_set_stream(E.h, stream.cuda_stream), E.h)  # engine kernels ordered with NCCL on this stream
 step = sharded.device_step_fn(E, P.desc.k, E.perim, dev)
-runner = sharded.ShardedRun(sl, ed.Neta, step, dist)
+runner = sharded.ShardedRun(sl, ed.Neta, step, dist, k=P.desc.k)
 U0 = torch.from_numpy(P.initial_field().reshape(-1).copy()).to(dev)
 dt = P.desc.T / P.desc.Nt
 runner.run(U0.clone(), a.warmup, dt)

@@ -69,7 +69,7 @@ def _shard_worker(rank, world, port, name, over, nsteps, out):
         assert st == 0
         U_out.copy_(torch.from_numpy(o))
 
-    runner = sharded.ShardedRun(sl, ed.Neta, step, dist)
+    runner = sharded.ShardedRun(sl, ed.Neta, step, dist, k=P.desc.k)
     U0 = torch.from_numpy(P.initial_field().reshape(-1).copy())
     dt = P.desc.T / P.desc.Nt
     U, done, failed = runner.run(U0, nsteps, dt, 0.0, P.boundary_table(0.0, nsteps))

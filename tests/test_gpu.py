@@ -540,7 +540,7 @@ def _gpu_shard_worker(rank, world, port, name, mode, nsteps, out):
         step(U_in, U_out, t, bnd)
         torch.cuda.synchronize()
 
-    runner = sharded.ShardedRun(sl, ed.Neta, step_sync, dist, stage_cpu=True)
+    runner = sharded.ShardedRun(sl, ed.Neta, step_sync, dist, stage_cpu=True, k=P.desc.k)
     U0 = torch.from_numpy(P.initial_field().reshape(-1).copy()).to(dev)
     U, done, failed = runner.run(U0, nsteps, P.desc.T / P.desc.Nt, 0.0, P.boundary_table(0.0, nsteps))
     out[rank] = (runner.gather(U).cpu().numpy(), done, failed, E.P)
