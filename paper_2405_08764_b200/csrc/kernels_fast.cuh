@@ -88,17 +88,38 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
             // inward weight absorbs the outward one; the outward slot keeps the
             // original weight for the per-patch ghost constant (zeroed in k_fast).
             const bool Wb = i == 0, Eb = i == Cfg::N1 - 1, Sb = j == 0, Nb = j == Cfg::N2 - 1;
-            switch (kind) {
-                case WE: val = Wb ? wE + wW : wE; break;
-                case WW: val = Eb ? wW + wE : wW; break;
-                case WN: val = Sb ? wN + wS : wN; break;
-                case WS: val = Nb ? wS + wN : wS; break;
-                case WD: val = dt * (B * ixy); break;
-                default: val = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr); break;
+            if (p.pinned && (Wb || Eb || Sb || Nb)) {
+                val = 0.0; // pinned edge node: u' = its pinned value, set as the node constant
+            } else {
+                switch (kind) {
+                    case WE: val = Wb ? wE + wW : wE; break;
+                    case WW: val = Eb ? wW + wE : wW; break;
+                    case WN: val = Sb ? wN + wS : wN; break;
+                    case WS: val = Nb ? wS + wN : wS; break;
+                    case WD: val = dt * (B * ixy); break;
+                    default: { // Robin ghosts also carry cEdge * u(edge) (microsim.cpp:178-183)
+                        double wc = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr);
+                        if (Wb) wc += wW * p.cedge[PD_EDGE_W];
+                        if (Eb) wc += wE * p.cedge[PD_EDGE_E];
+                        if (Sb) wc += wS * p.cedge[PD_EDGE_S];
+                        if (Nb) wc += wN * p.cedge[PD_EDGE_N];
+                        val = wc;
+                        break;
+                    }
+                }
             }
         }
         W[((unit * Cfg::S + s) * 32 + lane) * 2 + half] = val;
     }
+}
+
+// Per-edge-node constant of the boundary fold-in: Robin ghost offset
+// b = sign 2 delta (w1 value + w2 slope) / w2 (make_ghost, microsim.cpp:176-183)
+// or, on a pinned edge, the pinned value (pinned_value, microsim.cpp:189-192).
+__device__ __forceinline__ double edge_constant(const Params& p, int e, double value, double slope) {
+    if (p.bc_type == PD_BC_DIRICHLET) return value;
+    if (p.pinned) return value + p.w2 / p.w1 * slope; // Robin with w2 ~ 0 behaves as Dirichlet
+    return p.gsc[e] * ((p.w1 * value + p.w2 * slope) / p.w2);
 }
 
 // ---- mixed-term ring offsets ------------------------------------------------
@@ -170,7 +191,16 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
             const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
             const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
-            sg[gs][e][j] = p.gsc[e] * (p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2);
+            const double sl = p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2;
+            if (p.bc_type == PD_BC_NEUMANN) {
+                sg[gs][e][j] = p.gsc[e] * sl;
+            } else { // Robin / Dirichlet need the edge value too (dirichlet_edge_values, gaptooth.cpp:110-130)
+                const double* w = p.vlag[e];
+                const double V0 = w[0] * v[0] + w[1] * v[3] + w[2] * v[6];
+                const double V1 = w[0] * v[1] + w[1] * v[4] + w[2] * v[7];
+                const double V2 = w[0] * v[2] + w[1] * v[5] + w[2] * v[8];
+                sg[gs][e][j] = edge_constant(p, e, p.lagq[j][0] * V0 + p.lagq[j][1] * V1 + p.lagq[j][2] * V2, sl);
+            }
         } else {
             const int u = t - 2 * N2;
             const int e = u < N1 ? PD_EDGE_N : PD_EDGE_S, i = u < N1 ? u : u - N1;
@@ -178,7 +208,16 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
             const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
             const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
-            sg[gs][e][i] = p.gsc[e] * (p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2);
+            const double sl = p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2;
+            if (p.bc_type == PD_BC_NEUMANN) {
+                sg[gs][e][i] = p.gsc[e] * sl;
+            } else {
+                const double* w = p.vlag[e];
+                const double V0 = w[0] * v[0] + w[1] * v[1] + w[2] * v[2];
+                const double V1 = w[0] * v[3] + w[1] * v[4] + w[2] * v[5];
+                const double V2 = w[0] * v[6] + w[1] * v[7] + w[2] * v[8];
+                sg[gs][e][i] = edge_constant(p, e, p.lagp[i][0] * V0 + p.lagp[i][1] * V1 + p.lagp[i][2] * V2, sl);
+            }
         }
     }
     __syncwarp();
@@ -187,7 +226,9 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     const double* gN = sg[gs][PD_EDGE_N];
     const double* gS = sg[gs][PD_EDGE_S];
     if constexpr (MIXED) {
-        if constexpr (LP == 32) { // one patch per warp: closed form (measured faster at 16x16)
+        if (p.pinned) {
+            // pinned ring nodes do not update; the interior reads real nodes only
+        } else if constexpr (LP == 32) { // one patch per warp: closed form (measured faster at 16x16)
             for (int t = r; t < 2 * N2 + 2 * N1; t += LP) {
                 int e, k;
                 sg[gs][4 + e_of_ring<N1, N2>(t, e, k)][k] = ring_offset<N1, N2>(gE, gW, gN, gS, t);
@@ -234,7 +275,25 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
             const bool Sb = jj == 0 && bj == 0, Nb = jj == BJ - 1 && bj == Cfg::LJ - 1;
             double cc = 0.0;
-            // single-edge reflections u_ghost = u_inner + g (microsim.cpp:314-323)
+            if (p.pinned) {
+                // pinned edge nodes keep their value (all their weights are zero): the
+                // sweep's priority W, E, S, N for the value (microsim.cpp:306-311); a
+                // Dirichlet edge also pins the initial field, in W, E, S, N order with
+                // the later edge winning at corners (microsim.cpp:521-530)
+                if (Wb) cc = gW[j];
+                else if (Eb) cc = gE[j];
+                else if (Sb) cc = gS[i];
+                else if (Nb) cc = gN[i];
+                if (p.bc_type == PD_BC_DIRICHLET) {
+                    if (Wb) u[ii][jj] = gW[j];
+                    if (Eb) u[ii][jj] = gE[j];
+                    if (Sb) u[ii][jj] = gS[i];
+                    if (Nb) u[ii][jj] = gN[i];
+                }
+                c[ii][jj] = cc;
+                continue;
+            }
+            // single-edge reflections u_ghost = u_inner + cEdge u_edge + b (microsim.cpp:314-323)
             if (Wb) { cc = fma(WT(WW, ii, jj), gW[j], cc); WT(WW, ii, jj) = 0.0; }
             if (Eb) { cc = fma(WT(WE, ii, jj), gE[j], cc); WT(WE, ii, jj) = 0.0; }
             if (Sb) { cc = fma(WT(WS, ii, jj), gS[i], cc); WT(WS, ii, jj) = 0.0; }
@@ -424,8 +483,9 @@ using FC16M = FastCfg<16, 16, 2, 4, true>;
 #define PD_FAST_CONFIGS(X) X(0, FC7) X(1, FC7M) X(2, FC8) X(3, FC8M) X(4, FC9) X(5, FC9M) X(6, FC16) X(7, FC16M)
 
 inline bool plan_fast(const Params& p, FastPlan& plan) {
-    // only the Neumann patch conditions of every BASELINE config are folded
-    if (p.bc_type != PD_BC_NEUMANN || p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
+    // Neumann (every BASELINE config), Robin and Dirichlet patch conditions are
+    // folded into the weights / node constants; Simpson and sources stay EXACT
+    if (p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
     int id = -1;
 #define PD_MATCH(ID, CFG) \
     if (id < 0 && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;

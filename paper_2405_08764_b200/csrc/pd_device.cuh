@@ -42,6 +42,9 @@ struct Params {
     double lagq[33][3];  // Lagrange value weights at the E/W edge nodes Y_j (j < n2)
     double lagp[33][3];  // Lagrange value weights at the N/S edge nodes X_i (i < n1)
     double gsc[4];       // ghost scale +-2 delta per edge (microsim.cpp:166)
+    double vlag[4][3];   // Lagrange value weights at +-h/2 across each edge (E, W, N, S): edge values
+    double cedge[4];     // Robin ghost coefficient cEdge = -sign 2 delta w1/w2 per edge (microsim.cpp:180)
+    int pinned;          // the patch edges pin their nodes (Dirichlet, or Robin with w2 ~ 0)
 };
 
 // One micro edge condition in shared memory (EdgeCondition + Ghost,

@@ -247,6 +247,16 @@ Params make_params(const pd_engine_desc& d, int P) {
         o[1] = -2.0 * X / (D * D);
         o[2] = (X + 0.5 * D) / (D * D);
     };
+    lag(0.5 * d.h_xi, p.Dxi, p.vlag[0]);
+    lag(-0.5 * d.h_xi, p.Dxi, p.vlag[1]);
+    lag(0.5 * d.h_eta, p.Deta, p.vlag[2]);
+    lag(-0.5 * d.h_eta, p.Deta, p.vlag[3]);
+    p.pinned = d.bc_type == PD_BC_DIRICHLET || (d.bc_type == PD_BC_ROBIN && std::fabs(d.robin_w2) < 1e-300);
+    for (int e = 0; e < 4; ++e) {
+        const double sign = (e == PD_EDGE_E || e == PD_EDGE_N) ? 1.0 : -1.0;
+        const double delta = (e == PD_EDGE_E || e == PD_EDGE_W) ? p.mdxi : p.mdeta;
+        p.cedge[e] = (d.bc_type == PD_BC_ROBIN && !p.pinned) ? -sign * 2.0 * delta * d.robin_w1 / d.robin_w2 : 0.0;
+    }
     dlag(0.5 * d.h_xi, p.Dxi, p.dlag[0]);
     dlag(-0.5 * d.h_xi, p.Dxi, p.dlag[1]);
     dlag(0.5 * d.h_eta, p.Deta, p.dlag[2]);
