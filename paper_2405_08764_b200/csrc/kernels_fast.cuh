@@ -113,6 +113,17 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
     }
 }
 
+// restrict_average weight of node k of n+1 (gaptooth.cpp:172-185): trapezoid
+// 1/n (1/2n at the ends) or Simpson (1, 4, 2, ..., 4, 1)/(3n)
+template <int n>
+__device__ __forceinline__ double quad_weight(int k, int quad) {
+    constexpr double tr = 1.0 / n, te = 0.5 / n;
+    constexpr double s1 = 1.0 / (3.0 * n), s2 = 2.0 / (3.0 * n), s4 = 4.0 / (3.0 * n);
+    const bool end = k == 0 || k == n;
+    if (quad == PD_QUAD_SIMPSON) return end ? s1 : ((k & 1) ? s4 : s2);
+    return end ? te : tr;
+}
+
 // Per-edge-node constant of the boundary fold-in: Robin ghost offset
 // b = sign 2 delta (w1 value + w2 slope) / w2 (make_ghost, microsim.cpp:176-183)
 // or, on a pinned edge, the pinned value (pinned_value, microsim.cpp:189-192).
@@ -392,9 +403,19 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             for (int jj = 0; jj < BJ; ++jj) u[ii][jj] = nu[ii][jj];
     }
 
-    // ---- trapezoid restriction (gaptooth.cpp:170-194) ----------------------
+    // ---- trapezoid / Simpson restriction (gaptooth.cpp:170-194) -------------
     double part = 0.0;
-    {
+    // Simpson needs even nx, ny (odd node counts): compiled only for those shapes
+    constexpr bool kSimpsonShape = (N1 - 1) % 2 == 0 && (N2 - 1) % 2 == 0;
+    if (kSimpsonShape && p.quad == PD_QUAD_SIMPSON) {
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            double row = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) row += quad_weight<N2 - 1>(bj * BJ + jj, PD_QUAD_SIMPSON) * u[ii][jj];
+            part += quad_weight<N1 - 1>(bi * BI + ii, PD_QUAD_SIMPSON) * row;
+        }
+    } else {
         const double ox = 1.0 / (N1 - 1), oy = 1.0 / (N2 - 1);
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
@@ -484,8 +505,10 @@ using FC16M = FastCfg<16, 16, 2, 4, true>;
 
 inline bool plan_fast(const Params& p, FastPlan& plan) {
     // Neumann (every BASELINE config), Robin and Dirichlet patch conditions are
-    // folded into the weights / node constants; Simpson and sources stay EXACT
-    if (p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
+    // folded into the weights / node constants, both quadratures into the
+    // restriction (Simpson exists only for odd node counts); sources stay EXACT
+    if (p.source != PD_SOURCE_ZERO) return false;
+    if (p.quad == PD_QUAD_SIMPSON && ((p.n1 - 1) % 2 || (p.n2 - 1) % 2)) return false;
     int id = -1;
 #define PD_MATCH(ID, CFG) \
     if (id < 0 && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
