@@ -66,13 +66,25 @@ __global__ void k_fold_big(Params p, const double* __restrict__ coeffs, const in
             const double ax = A * idx2, vx = Vx * idx, cy = C * idy2, vy = Vy * idy;
             const double wE = dt * (ax - vx), wW = dt * (ax + vx), wN = dt * (cy - vy), wS = dt * (cy + vy);
             const bool Wb = i == 0, Eb = i == Cfg::N1 - 1, Sb = j == 0, Nb = j == Cfg::N2 - 1;
-            switch (kind) { // same static Neumann reflection as k_fold
-                case WE: val = Wb ? wE + wW : wE; break;
-                case WW: val = Eb ? wW + wE : wW; break;
-                case WN: val = Sb ? wN + wS : wN; break;
-                case WS: val = Nb ? wS + wN : wS; break;
-                case WD: val = flip ? -(dt * (B * ixy)) : dt * (B * ixy); break;
-                default: val = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr); break;
+            if (p.pinned && (Wb || Eb || Sb || Nb)) {
+                val = 0.0; // pinned edge node (as k_fold)
+            } else {
+                switch (kind) { // same static reflections as k_fold
+                    case WE: val = Wb ? wE + wW : wE; break;
+                    case WW: val = Eb ? wW + wE : wW; break;
+                    case WN: val = Sb ? wN + wS : wN; break;
+                    case WS: val = Nb ? wS + wN : wS; break;
+                    case WD: val = flip ? -(dt * (B * ixy)) : dt * (B * ixy); break;
+                    default: {
+                        double wc = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr);
+                        if (Wb) wc += wW * p.cedge[PD_EDGE_W];
+                        if (Eb) wc += wE * p.cedge[PD_EDGE_E];
+                        if (Sb) wc += wS * p.cedge[PD_EDGE_S];
+                        if (Nb) wc += wN * p.cedge[PD_EDGE_N];
+                        val = wc;
+                        break;
+                    }
+                }
             }
         }
         W[((unit * Cfg::S + s) * 32 + lane) * 2 + half] = val;
@@ -135,7 +147,16 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
             const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
             const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
-            s_g[e][j] = p.gsc[e] * (p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2);
+            const double sl = p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2;
+            if (p.bc_type == PD_BC_NEUMANN) {
+                s_g[e][j] = p.gsc[e] * sl;
+            } else {
+                const double* w = p.vlag[e];
+                const double V0 = w[0] * v[0] + w[1] * v[3] + w[2] * v[6];
+                const double V1 = w[0] * v[1] + w[1] * v[4] + w[2] * v[7];
+                const double V2 = w[0] * v[2] + w[1] * v[5] + w[2] * v[8];
+                s_g[e][j] = edge_constant(p, e, p.lagq[j][0] * V0 + p.lagq[j][1] * V1 + p.lagq[j][2] * V2, sl);
+            }
         } else {
             const int u = t - 2 * N2;
             const int e = u < N1 ? PD_EDGE_N : PD_EDGE_S, i = u < N1 ? u : u - N1;
@@ -143,7 +164,16 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
             const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
             const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
-            s_g[e][i] = p.gsc[e] * (p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2);
+            const double sl = p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2;
+            if (p.bc_type == PD_BC_NEUMANN) {
+                s_g[e][i] = p.gsc[e] * sl;
+            } else {
+                const double* w = p.vlag[e];
+                const double V0 = w[0] * v[0] + w[1] * v[1] + w[2] * v[2];
+                const double V1 = w[0] * v[3] + w[1] * v[4] + w[2] * v[5];
+                const double V2 = w[0] * v[6] + w[1] * v[7] + w[2] * v[8];
+                s_g[e][i] = edge_constant(p, e, p.lagp[i][0] * V0 + p.lagp[i][1] * V1 + p.lagp[i][2] * V2, sl);
+            }
         }
     }
     __syncthreads();
@@ -151,7 +181,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     const double* gW = s_g[PD_EDGE_W];
     const double* gN = s_g[PD_EDGE_N];
     const double* gS = s_g[PD_EDGE_S];
-    if constexpr (MIXED) {
+    if constexpr (MIXED) if (!p.pinned) { // pinned ring nodes do not update
         auto off = [&](int pp, int qq) {
             const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
             const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
@@ -198,6 +228,18 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
             const bool Hb = jj == 0 && etaEdge; // physical S (unmirrored) or N (mirrored) edge
             double cc = 0.0;
+            if (p.pinned) { // as patch_body: sweep priority W, E, S|N; Dirichlet pins u0 in W, E, S|N order
+                if (Wb) cc = gW[j];
+                else if (Eb) cc = gE[j];
+                else if (Hb) cc = gEta[i];
+                if (p.bc_type == PD_BC_DIRICHLET) {
+                    if (Wb) u[ii][jj] = gW[j];
+                    if (Eb) u[ii][jj] = gE[j];
+                    if (Hb) u[ii][jj] = gEta[i];
+                }
+                c[ii][jj] = cc;
+                continue;
+            }
             if (Wb) { cc = fma(WT(WW, ii, jj), gW[j], cc); WT(WW, ii, jj) = 0.0; }
             if (Eb) { cc = fma(WT(WE, ii, jj), gE[j], cc); WT(WE, ii, jj) = 0.0; }
             if (Hb) { cc = fma(WT(WS, ii, jj), gEta[i], cc); WT(WS, ii, jj) = 0.0; }
@@ -339,7 +381,7 @@ using BC32M = BigCfg<32, true>;
 namespace pdb200::dev {
 
 inline bool plan_big(const Params& p, FastPlan& plan) {
-    if (p.bc_type != PD_BC_NEUMANN || p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
+    if (p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
     if (!(p.n1 == 32 && p.n2 == 32)) return false;
     plan.big = 1;
     plan.mixed = p.mixed;
