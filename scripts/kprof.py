@@ -16,8 +16,8 @@ elif which == 'k1':
     d = configs.copy_desc(d, nt=1)
 elif which == 'k10':
     d = configs.sweep_desc(d, 18, 16, 10)
-P = Problem(d)
-E = Engine.from_problem(P)
+P = Problem(configs.copy_desc(d, N_xi=129, N_eta=129) if which == 'c4exact' else d)
+E = Engine.from_problem(P, mode=1 if which == 'c4exact' else None)
 U0 = P.initial_field()
 dU = torch.from_numpy(U0.ravel()).cuda(); dS = torch.empty_like(dU)
 ms = E.bench_step_kernel(dU.data_ptr(), dS.data_ptr(), 3)
