@@ -604,3 +604,25 @@ def test_sharded_device_run_equals_single_engine(name, mode, gpu):
         U, done, failed, _ = res[r]
         assert failed == 0 and done == nsteps
         assert np.array_equal(U.reshape(P.shape), Uref)
+
+
+# ---------------------------------------------------------------------------
+# maximum size: the largest config-5 patch count (2^20 patches of 32x32 micro
+# nodes, 103 GB of device tables) — size-independent properties on the device,
+# a sampled substep against the oracle
+# ---------------------------------------------------------------------------
+def test_config5_maximum_size(restated, gpu):
+    base, _ = configs.load("c5_sweep")
+    P = Problem(configs.sweep_desc(base, 20, 32, 10))
+    ed = P.engine_desc()
+    E = Engine.from_problem(P, mode=FAST)
+    assert E.mode == FAST and E.P == 2 ** 20
+    U0 = P.initial_field()
+    S = E.step_direct(U0, 0.0)
+    assert np.isfinite(S).all()
+    assert np.array_equal(E.step_direct(2.0 * U0, 0.0), 2.0 * S)  # linear, power-of-two scaling exact
+    rng = np.random.default_rng(3)
+    idx = np.sort(rng.choice(E.P, 64, replace=False)).astype(np.int32)
+    avg, _ = restated.patch_subset(ed, U0, 0.0, idx)
+    pij = np.ctypeslib.as_array(ed.patch_ij, shape=(E.P, 2))[idx]
+    assert rel(S[pij[:, 0], pij[:, 1]], avg) < 1e-13
