@@ -34,10 +34,13 @@ struct FastPlan {
     int big = 0; // 32x32 patches: kernels_fast_big.cuh (one CTA of 4 warps per patch)
 };
 
-template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
+template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_, bool PAD_ = false>
 struct FastCfg {
     static constexpr int N1 = N1_, N2 = N2_, BI = BI_, BJ = BJ_;
     static constexpr bool MIXED = MIXED_;
+    // PAD: the patch (p.n1 x p.n2, runtime) is smaller than the N1 x N2 tile;
+    // the extra "phantom" nodes carry zero weights and stay out of the restriction
+    static constexpr bool PAD = PAD_;
     static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, G = 32 / LP;
     static constexpr int NPL = BI * BJ;          // nodes per lane
     static constexpr int NW = MIXED ? 6 : 5;     // weights per node: C,E,W,N,S,(D)
@@ -77,6 +80,11 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
             const int ii = node / Cfg::BJ, jj = node % Cfg::BJ;
             const int bi = r % Cfg::LI, bj = r / Cfg::LI;
             const int i = bi * Cfg::BI + ii, j = bj * Cfg::BJ + jj;
+            const int n1 = Cfg::PAD ? p.n1 : Cfg::N1, n2 = Cfg::PAD ? p.n2 : Cfg::N2;
+            if (Cfg::PAD && (i >= n1 || j >= n2)) { // phantom node of a padded tile
+                W[((unit * Cfg::S + s) * 32 + lane) * 2 + half] = 0.0;
+                continue;
+            }
             const int set = cset ? cset[patch] : (int)patch;
             const double* c = coeffs + (size_t)set * PD_NCOEF * p.N;
             const int k = i * p.n2 + j;
@@ -87,7 +95,7 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
             // Neumann reflection u_ghost = u_inner + g (microsim.cpp:314-323): the
             // inward weight absorbs the outward one; the outward slot keeps the
             // original weight for the per-patch ghost constant (zeroed in k_fast).
-            const bool Wb = i == 0, Eb = i == Cfg::N1 - 1, Sb = j == 0, Nb = j == Cfg::N2 - 1;
+            const bool Wb = i == 0, Eb = i == n1 - 1, Sb = j == 0, Nb = j == n2 - 1;
             if (p.pinned && (Wb || Eb || Sb || Nb)) {
                 val = 0.0; // pinned edge node: u' = its pinned value, set as the node constant
             } else {
@@ -124,6 +132,12 @@ __device__ __forceinline__ double quad_weight(int k, int quad) {
     return end ? te : tr;
 }
 
+__device__ __forceinline__ double quad_weight_rt(int k, int n, int quad) {
+    const bool end = k == 0 || k == n;
+    if (quad == PD_QUAD_SIMPSON) return (end ? 1.0 : ((k & 1) ? 4.0 : 2.0)) / (3.0 * n);
+    return (end ? 0.5 : 1.0) / n;
+}
+
 // Per-edge-node constant of the boundary fold-in: Robin ghost offset
 // b = sign 2 delta (w1 value + w2 slope) / w2 (make_ghost, microsim.cpp:176-183)
 // or, on a pinned edge, the pinned value (pinned_value, microsim.cpp:189-192).
@@ -139,8 +153,7 @@ __device__ __forceinline__ double edge_constant(const Params& p, int e, double v
 // ghosts carry both edges' offsets); what remains is a signed difference of
 // the node's own edge offsets plus, at the two ends of the edge, the
 // neighbouring edges' offsets.  Ring entry t: E (j = t), W, N (i), S order.
-template <int N1, int N2>
-__device__ __forceinline__ int e_of_ring(int t, int& e, int& k) {
+__device__ __forceinline__ int e_of_ring(int N1, int N2, int t, int& e, int& k) {
     const bool xi_edge = t < 2 * N2;
     const int L = xi_edge ? N2 : N1, u = xi_edge ? t : t - 2 * N2;
     const bool first = u < L;
@@ -148,9 +161,8 @@ __device__ __forceinline__ int e_of_ring(int t, int& e, int& k) {
     e = xi_edge ? (first ? PD_EDGE_E : PD_EDGE_W) : (first ? PD_EDGE_N : PD_EDGE_S);
     return e;
 }
-template <int N1, int N2>
-__device__ __forceinline__ double ring_offset(const double* gE, const double* gW, const double* gN, const double* gS,
-                                              int t) {
+__device__ __forceinline__ double ring_offset(int N1, int N2, const double* gE, const double* gW, const double* gN,
+                                              const double* gS, int t) {
     const bool xi_edge = t < 2 * N2;
     const int L = xi_edge ? N2 : N1, M = xi_edge ? N1 : N2, u = xi_edge ? t : t - 2 * N2;
     const bool first = u < L; // E or N: +, W or S: -
@@ -176,6 +188,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LP = Cfg::LP, G = Cfg::G, NPL = Cfg::NPL;
     constexpr int N1 = Cfg::N1, N2 = Cfg::N2;
     constexpr bool MIXED = Cfg::MIXED;
+    const int n1 = Cfg::PAD ? p.n1 : N1, n2 = Cfg::PAD ? p.n2 : N2; // the patch's real extent
     const int g = lane / LP, r = lane % LP;
     const int bi = r % LI, bj = r / LI;
     const int gs = g < G ? g : 0;
@@ -195,9 +208,9 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     // 2*N1 + 2*N2 entries; then, for the mixed term, the boundary-ring offsets
     // Doff (the reflected node values cancel in (uNE+uSW)-(uNW+uSE); what
     // remains is a signed sum of ghost offsets, SURVEY B.4 corners).
-    for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
-        if (t < 2 * N2) {
-            const int e = t < N2 ? PD_EDGE_E : PD_EDGE_W, j = t < N2 ? t : t - N2;
+    for (int t = r; g < G && t < 2 * n2 + 2 * n1; t += LP) {
+        if (t < 2 * n2) {
+            const int e = t < n2 ? PD_EDGE_E : PD_EDGE_W, j = t < n2 ? t : t - n2;
             const double* d = p.dlag[e];
             const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
             const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
@@ -213,8 +226,8 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
                 sg[gs][e][j] = edge_constant(p, e, p.lagq[j][0] * V0 + p.lagq[j][1] * V1 + p.lagq[j][2] * V2, sl);
             }
         } else {
-            const int u = t - 2 * N2;
-            const int e = u < N1 ? PD_EDGE_N : PD_EDGE_S, i = u < N1 ? u : u - N1;
+            const int u = t - 2 * n2;
+            const int e = u < n1 ? PD_EDGE_N : PD_EDGE_S, i = u < n1 ? u : u - n1;
             const double* d = p.dlag[e];
             const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
             const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
@@ -240,26 +253,26 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
         if (p.pinned) {
             // pinned ring nodes do not update; the interior reads real nodes only
         } else if constexpr (LP == 32) { // one patch per warp: closed form (measured faster at 16x16)
-            for (int t = r; t < 2 * N2 + 2 * N1; t += LP) {
+            for (int t = r; t < 2 * n2 + 2 * n1; t += LP) {
                 int e, k;
-                sg[gs][4 + e_of_ring<N1, N2>(t, e, k)][k] = ring_offset<N1, N2>(gE, gW, gN, gS, t);
+                sg[gs][4 + e_of_ring(n1, n2, t, e, k)][k] = ring_offset(n1, n2, gE, gW, gN, gS, t);
             }
         } else { // several patches per warp: generic corner rule (measured faster at 8x8)
             auto off = [&](int pp, int qq) {
-                const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
-                const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
+                const int qc = qq < 0 ? 0 : (qq > n2 - 1 ? n2 - 1 : qq);
+                const int pc = pp < 0 ? 0 : (pp > n1 - 1 ? n1 - 1 : pp);
                 double o = 0.0;
                 if (pp < 0) o += gW[qc];
-                if (pp > N1 - 1) o += gE[qc];
+                if (pp > n1 - 1) o += gE[qc];
                 if (qq < 0) o += gS[pc];
-                if (qq > N2 - 1) o += gN[pc];
+                if (qq > n2 - 1) o += gN[pc];
                 return o;
             };
-            for (int t = r; g < G && t < 2 * N2 + 2 * N1; t += LP) {
+            for (int t = r; g < G && t < 2 * n2 + 2 * n1; t += LP) {
                 int e, k;
-                e_of_ring<N1, N2>(t, e, k);
-                const int i = e == PD_EDGE_E ? N1 - 1 : e == PD_EDGE_W ? 0 : k;
-                const int j = e == PD_EDGE_N ? N2 - 1 : e == PD_EDGE_S ? 0 : k;
+                e_of_ring(n1, n2, t, e, k);
+                const int i = e == PD_EDGE_E ? n1 - 1 : e == PD_EDGE_W ? 0 : k;
+                const int j = e == PD_EDGE_N ? n2 - 1 : e == PD_EDGE_S ? 0 : k;
                 sg[gs][4 + e][k] = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
             }
         }
@@ -281,10 +294,17 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const int j = bj * BJ + jj;
             const double Y = -0.5 * p.h_eta + p.mdeta * j;
             u[ii][jj] = Ai + Y * (Bi + Y * hUyy); // quadratic lift (gaptooth.cpp:154-168)
-            // only block-edge nodes can be patch-edge nodes: written so the
-            // compiler drops the impossible cases at compile time
-            const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
-            const bool Sb = jj == 0 && bj == 0, Nb = jj == BJ - 1 && bj == Cfg::LJ - 1;
+            if (Cfg::PAD && (i >= n1 || j >= n2)) { // phantom node: zero weights, zero state
+                u[ii][jj] = 0.0;
+                c[ii][jj] = 0.0;
+                continue;
+            }
+            // only block-edge nodes can be patch-edge nodes of an exact-fit tile:
+            // written so the compiler drops the impossible cases at compile time
+            const bool Wb = ii == 0 && bi == 0;
+            const bool Eb = Cfg::PAD ? i == n1 - 1 : (ii == BI - 1 && bi == LI - 1);
+            const bool Sb = jj == 0 && bj == 0;
+            const bool Nb = Cfg::PAD ? j == n2 - 1 : (jj == BJ - 1 && bj == Cfg::LJ - 1);
             double cc = 0.0;
             if (p.pinned) {
                 // pinned edge nodes keep their value (all their weights are zero): the
@@ -407,7 +427,19 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     double part = 0.0;
     // Simpson needs even nx, ny (odd node counts): compiled only for those shapes
     constexpr bool kSimpsonShape = (N1 - 1) % 2 == 0 && (N2 - 1) % 2 == 0;
-    if (kSimpsonShape && p.quad == PD_QUAD_SIMPSON) {
+    if constexpr (Cfg::PAD) { // real extent at run time, phantom nodes weigh nothing
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            const int i = bi * BI + ii;
+            double row = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+                const int j = bj * BJ + jj;
+                row += (j < n2 ? quad_weight_rt(j, n2 - 1, p.quad) : 0.0) * u[ii][jj];
+            }
+            part += (i < n1 ? quad_weight_rt(i, n1 - 1, p.quad) : 0.0) * row;
+        }
+    } else if (kSimpsonShape && p.quad == PD_QUAD_SIMPSON) {
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
             double row = 0.0;
@@ -500,8 +532,19 @@ using FC9 = FastCfg<9, 9, 3, 3, false>;
 using FC9M = FastCfg<9, 9, 3, 3, true>;
 using FC16 = FastCfg<16, 16, 2, 4, false>;
 using FC16M = FastCfg<16, 16, 2, 4, true>;
+// padded tiles: any patch up to 16 x 16 micro nodes (phantom nodes fill the tile)
+using FC7P = FastCfg<7, 7, 1, 7, false, true>;
+using FC7MP = FastCfg<7, 7, 1, 7, true, true>;
+using FC8P = FastCfg<8, 8, 2, 4, false, true>;
+using FC8MP = FastCfg<8, 8, 2, 4, true, true>;
+using FC9P = FastCfg<9, 9, 3, 3, false, true>;
+using FC9MP = FastCfg<9, 9, 3, 3, true, true>;
+using FC16P = FastCfg<16, 16, 2, 4, false, true>;
+using FC16MP = FastCfg<16, 16, 2, 4, true, true>;
 
-#define PD_FAST_CONFIGS(X) X(0, FC7) X(1, FC7M) X(2, FC8) X(3, FC8M) X(4, FC9) X(5, FC9M) X(6, FC16) X(7, FC16M)
+#define PD_FAST_CONFIGS(X)                                                                                       \
+    X(0, FC7) X(1, FC7M) X(2, FC8) X(3, FC8M) X(4, FC9) X(5, FC9M) X(6, FC16) X(7, FC16M) X(8, FC7P) X(9, FC7MP) \
+        X(10, FC8P) X(11, FC8MP) X(12, FC9P) X(13, FC9MP) X(14, FC16P) X(15, FC16MP)
 
 inline bool plan_fast(const Params& p, FastPlan& plan) {
     // Neumann (every BASELINE config), Robin and Dirichlet patch conditions are
@@ -510,10 +553,15 @@ inline bool plan_fast(const Params& p, FastPlan& plan) {
     if (p.source != PD_SOURCE_ZERO) return false;
     if (p.quad == PD_QUAD_SIMPSON && ((p.n1 - 1) % 2 || (p.n2 - 1) % 2)) return false;
     int id = -1;
+    // an exact-fit tile first (compile-time extents), else the smallest padded tile
 #define PD_MATCH(ID, CFG) \
-    if (id < 0 && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
+    if (id < 0 && !CFG::PAD && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
     PD_FAST_CONFIGS(PD_MATCH)
 #undef PD_MATCH
+#define PD_MATCH_PAD(ID, CFG) \
+    if (id < 0 && CFG::PAD && p.n1 <= CFG::N1 && p.n2 <= CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
+    PD_FAST_CONFIGS(PD_MATCH_PAD)
+#undef PD_MATCH_PAD
     if (id < 0) return false;
     plan.id = id;
     plan.mixed = p.mixed;

@@ -19,10 +19,11 @@
 
 namespace pdb200::dev {
 
-template <int N_, bool MIXED_>
+template <int N_, bool MIXED_, bool PAD_ = false>
 struct BigCfg {
     static constexpr int N1 = N_, N2 = N_, BI = 2, BJ = 4;
     static constexpr bool MIXED = MIXED_;
+    static constexpr bool PAD = PAD_; // patch smaller than the tile: phantom nodes (as FastCfg)
     static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, WPP = LP / 32;
     static constexpr int NPL = BI * BJ, NW = MIXED ? 6 : 5, NWL = NW * NPL, S = (NWL + 1) / 2;
     static constexpr int L = N_;
@@ -58,6 +59,11 @@ __global__ void k_fold_big(Params p, const double* __restrict__ coeffs, const in
             const bool flip = bj & 1; // mirrored block row: local N/S = physical S/N
             const int i = bi * Cfg::BI + ii, j = bj * Cfg::BJ + (flip ? Cfg::BJ - 1 - jj : jj);
             const int kind = flip && lkind == WN ? WS : flip && lkind == WS ? WN : lkind;
+            const int n1 = Cfg::PAD ? p.n1 : Cfg::N1, n2 = Cfg::PAD ? p.n2 : Cfg::N2;
+            if (Cfg::PAD && (i >= n1 || j >= n2)) { // phantom node
+                W[((unit * Cfg::S + s) * 32 + lane) * 2 + half] = 0.0;
+                continue;
+            }
             const int set = cset ? cset[patch] : (int)patch;
             const double* c = coeffs + (size_t)set * PD_NCOEF * p.N;
             const int k = i * p.n2 + j;
@@ -65,7 +71,7 @@ __global__ void k_fold_big(Params p, const double* __restrict__ coeffs, const in
             const double Vx = c[PD_COEF_VX * p.N + k], Vy = c[PD_COEF_VY * p.N + k], Wr = c[PD_COEF_W * p.N + k];
             const double ax = A * idx2, vx = Vx * idx, cy = C * idy2, vy = Vy * idy;
             const double wE = dt * (ax - vx), wW = dt * (ax + vx), wN = dt * (cy - vy), wS = dt * (cy + vy);
-            const bool Wb = i == 0, Eb = i == Cfg::N1 - 1, Sb = j == 0, Nb = j == Cfg::N2 - 1;
+            const bool Wb = i == 0, Eb = i == n1 - 1, Sb = j == 0, Nb = j == n2 - 1;
             if (p.pinned && (Wb || Eb || Sb || Nb)) {
                 val = 0.0; // pinned edge node (as k_fold)
             } else {
@@ -98,6 +104,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LJ = Cfg::LJ, NPL = Cfg::NPL, S = Cfg::S;
     constexpr int N1 = Cfg::N1, N2 = Cfg::N2, ROW = Cfg::ROW, WPP = Cfg::WPP;
     constexpr bool MIXED = Cfg::MIXED;
+    const int n1 = Cfg::PAD ? p.n1 : N1, n2 = Cfg::PAD ? p.n2 : N2; // the patch's real extent
     __shared__ double s_g[8][Cfg::L];                   // ghost offsets + mixed ring offsets
     __shared__ __align__(16) double s_row[2][LJ][ROW]; // [parity][block row][padded column]: local row jj = 0
     __shared__ double s_red[WPP];
@@ -140,9 +147,9 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     const double hUyy = 0.5 * ((v[5] - 2.0 * v[4] + v[3]) * p.iDeta2);
     const double Uxy = (v[8] - v[6] - v[2] + v[0]) * p.i4DD;
     const double C0 = v[4] - p.c24x * (2.0 * hUxx) - p.c24y * (2.0 * hUyy);
-    for (int t = r; t < 2 * N2 + 2 * N1; t += 32 * WPP) {
-        if (t < 2 * N2) {
-            const int e = t < N2 ? PD_EDGE_E : PD_EDGE_W, j = t < N2 ? t : t - N2;
+    for (int t = r; t < 2 * n2 + 2 * n1; t += 32 * WPP) {
+        if (t < 2 * n2) {
+            const int e = t < n2 ? PD_EDGE_E : PD_EDGE_W, j = t < n2 ? t : t - n2;
             const double* d = p.dlag[e];
             const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
             const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
@@ -158,8 +165,8 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
                 s_g[e][j] = edge_constant(p, e, p.lagq[j][0] * V0 + p.lagq[j][1] * V1 + p.lagq[j][2] * V2, sl);
             }
         } else {
-            const int u = t - 2 * N2;
-            const int e = u < N1 ? PD_EDGE_N : PD_EDGE_S, i = u < N1 ? u : u - N1;
+            const int u = t - 2 * n2;
+            const int e = u < n1 ? PD_EDGE_N : PD_EDGE_S, i = u < n1 ? u : u - n1;
             const double* d = p.dlag[e];
             const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
             const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
@@ -183,26 +190,26 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     const double* gS = s_g[PD_EDGE_S];
     if constexpr (MIXED) if (!p.pinned) { // pinned ring nodes do not update
         auto off = [&](int pp, int qq) {
-            const int qc = qq < 0 ? 0 : (qq > N2 - 1 ? N2 - 1 : qq);
-            const int pc = pp < 0 ? 0 : (pp > N1 - 1 ? N1 - 1 : pp);
+            const int qc = qq < 0 ? 0 : (qq > n2 - 1 ? n2 - 1 : qq);
+            const int pc = pp < 0 ? 0 : (pp > n1 - 1 ? n1 - 1 : pp);
             double o = 0.0;
             if (pp < 0) o += gW[qc];
-            if (pp > N1 - 1) o += gE[qc];
+            if (pp > n1 - 1) o += gE[qc];
             if (qq < 0) o += gS[pc];
-            if (qq > N2 - 1) o += gN[pc];
+            if (qq > n2 - 1) o += gN[pc];
             return o;
         };
-        for (int t = r; t < 2 * N2 + 2 * N1; t += 32 * WPP) {
+        for (int t = r; t < 2 * n2 + 2 * n1; t += 32 * WPP) {
             int e, i, j, k;
-            if (t < 2 * N2) {
-                e = t < N2 ? PD_EDGE_E : PD_EDGE_W;
-                k = j = t < N2 ? t : t - N2;
-                i = e == PD_EDGE_E ? N1 - 1 : 0;
+            if (t < 2 * n2) {
+                e = t < n2 ? PD_EDGE_E : PD_EDGE_W;
+                k = j = t < n2 ? t : t - n2;
+                i = e == PD_EDGE_E ? n1 - 1 : 0;
             } else {
-                const int u = t - 2 * N2;
-                e = u < N1 ? PD_EDGE_N : PD_EDGE_S;
-                k = i = u < N1 ? u : u - N1;
-                j = e == PD_EDGE_N ? N2 - 1 : 0;
+                const int u = t - 2 * n2;
+                e = u < n1 ? PD_EDGE_N : PD_EDGE_S;
+                k = i = u < n1 ? u : u - n1;
+                j = e == PD_EDGE_N ? n2 - 1 : 0;
             }
             s_g[4 + e][k] = (off(i + 1, j + 1) + off(i - 1, j - 1)) - (off(i - 1, j + 1) + off(i + 1, j - 1));
         }
@@ -225,6 +232,49 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const int j = flip ? j0 + BJ - 1 - jj : j0 + jj;
             const double Y = -0.5 * p.h_eta + p.mdeta * j;
             u[ii][jj] = Ai + Y * (Bi + Y * hUyy);
+            if constexpr (Cfg::PAD) {
+                // padded tile: the physical N edge (j = n2-1) can sit in any block row;
+                // its outward neighbour is local N in an unmirrored row, local S in a
+                // mirrored one (compile-time slots in each branch)
+                if (i >= n1 || j >= n2) { // phantom node
+                    u[ii][jj] = 0.0;
+                    c[ii][jj] = 0.0;
+                    continue;
+                }
+                const bool Wb = i == 0, Eb = i == n1 - 1, Sb = j == 0, Nb = j == n2 - 1;
+                double cc = 0.0;
+                if (p.pinned) {
+                    if (Wb) cc = gW[j];
+                    else if (Eb) cc = gE[j];
+                    else if (Sb) cc = gS[i];
+                    else if (Nb) cc = gN[i];
+                    if (p.bc_type == PD_BC_DIRICHLET) {
+                        if (Wb) u[ii][jj] = gW[j];
+                        if (Eb) u[ii][jj] = gE[j];
+                        if (Sb) u[ii][jj] = gS[i];
+                        if (Nb) u[ii][jj] = gN[i];
+                    }
+                    c[ii][jj] = cc;
+                    continue;
+                }
+                if (Wb) { cc = fma(WT(WW, ii, jj), gW[j], cc); WT(WW, ii, jj) = 0.0; }
+                if (Eb) { cc = fma(WT(WE, ii, jj), gE[j], cc); WT(WE, ii, jj) = 0.0; }
+                if (Sb) { cc = fma(WT(WS, ii, jj), gS[i], cc); WT(WS, ii, jj) = 0.0; } // row 0 is never mirrored
+                if (Nb) {
+                    if (flip) { cc = fma(WT(WS, ii, jj), gN[i], cc); WT(WS, ii, jj) = 0.0; }
+                    else { cc = fma(WT(WN, ii, jj), gN[i], cc); WT(WN, ii, jj) = 0.0; }
+                }
+                if constexpr (MIXED) {
+                    if (Wb || Eb || Sb || Nb) {
+                        const double* dd = s_g[4 + (Wb ? PD_EDGE_W : Eb ? PD_EDGE_E : Sb ? PD_EDGE_S : PD_EDGE_N)];
+                        const double o = dd[(Wb || Eb) ? j : i];
+                        cc = fma(WT(WD, ii, jj), flip ? -o : o, cc);
+                        WT(WD, ii, jj) = 0.0;
+                    }
+                }
+                c[ii][jj] = cc;
+                continue;
+            }
             const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
             const bool Hb = jj == 0 && etaEdge; // physical S (unmirrored) or N (mirrored) edge
             double cc = 0.0;
@@ -339,7 +389,19 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
 
     // ---- trapezoid restriction: lane partials, warp reduce, CTA reduce -------
     double part = 0.0;
-    {
+    if constexpr (Cfg::PAD) { // real extent at run time, phantom nodes weigh nothing
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            const int i = i0 + ii;
+            double row = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+                const int j = flip ? j0 + BJ - 1 - jj : j0 + jj;
+                row += (j < n2 ? quad_weight_rt(j, n2 - 1, p.quad) : 0.0) * u[ii][jj];
+            }
+            part += (i < n1 ? quad_weight_rt(i, n1 - 1, p.quad) : 0.0) * row;
+        }
+    } else {
         const double ox = 1.0 / (N1 - 1), oy = 1.0 / (N2 - 1);
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
@@ -375,17 +437,23 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
 
 using BC32 = BigCfg<32, false>;
 using BC32M = BigCfg<32, true>;
+using BC32P = BigCfg<32, false, true>;  // padded: any patch of 17..32 micro nodes per side
+using BC32MP = BigCfg<32, true, true>;
 
 } // namespace pdb200::dev
 
 namespace pdb200::dev {
 
 inline bool plan_big(const Params& p, FastPlan& plan) {
-    if (p.quad != PD_QUAD_TRAPEZOID || p.source != PD_SOURCE_ZERO) return false;
-    if (!(p.n1 == 32 && p.n2 == 32)) return false;
+    if (p.source != PD_SOURCE_ZERO) return false;
+    // exact 32 x 32 tiles, or padded ones for patches of up to 32 nodes per side
+    // that do not fit the one-warp 16 x 16 tile
+    const bool exact = p.n1 == 32 && p.n2 == 32;
+    const bool pad = !exact && p.n1 <= 32 && p.n2 <= 32 && (p.n1 > 16 || p.n2 > 16);
+    if (!exact && !pad) return false;
     plan.big = 1;
     plan.mixed = p.mixed;
-    plan.id = p.mixed ? 101 : 100;
+    plan.id = (p.mixed ? 101 : 100) + (pad ? 2 : 0);
     plan.LP = BC32::LP;
     plan.G = 1;
     plan.S = p.mixed ? BC32M::S : BC32::S;
@@ -393,18 +461,24 @@ inline bool plan_big(const Params& p, FastPlan& plan) {
     return true;
 }
 
+#define PD_BIG_CONFIGS(X) X(100, BC32) X(101, BC32M) X(102, BC32P) X(103, BC32MP)
+
 inline void fold_big(const FastPlan& plan, const Params& p, const double* coeffs, const int* cset, double* W,
                      cudaStream_t s) {
     const size_t total = (size_t)plan.nunits * plan.S * 64;
     const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
-    if (plan.mixed) k_fold_big<BC32M><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits);
-    else k_fold_big<BC32><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits);
+#define PD_BIG_FOLD(ID, CFG) \
+    if (plan.id == ID) k_fold_big<CFG><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits);
+    PD_BIG_CONFIGS(PD_BIG_FOLD)
+#undef PD_BIG_FOLD
 }
 
 inline void launch_big(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
                        const int* nbr, const double* W, const int* fail, cudaStream_t s) {
-    if (plan.mixed) k_fast_big<BC32M><<<p.P, 32 * BC32M::WPP, 0, s>>>(p, F, out, out_mode, nbr, W, fail);
-    else k_fast_big<BC32><<<p.P, 32 * BC32::WPP, 0, s>>>(p, F, out, out_mode, nbr, W, fail);
+#define PD_BIG_LAUNCH(ID, CFG) \
+    if (plan.id == ID) k_fast_big<CFG><<<p.P, 32 * CFG::WPP, 0, s>>>(p, F, out, out_mode, nbr, W, fail);
+    PD_BIG_CONFIGS(PD_BIG_LAUNCH)
+#undef PD_BIG_LAUNCH
 }
 
 } // namespace pdb200::dev

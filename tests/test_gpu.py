@@ -227,7 +227,7 @@ def test_macro_instability_guard(restated, gpu):
     d.nx = d.ny = 10
     d.nt = 400
     P = Problem(d)
-    E = Engine.from_problem(P)
+    E = Engine.from_problem(P, mode=EXACT)
     U0 = P.initial_field()
     bt = P.boundary_table(0.0, 5)
     st, Uo, so = restated.run(P.engine_desc(), U0, 5, bnd=bt)
@@ -237,6 +237,11 @@ def test_macro_instability_guard(restated, gpu):
     assert e.value.status == abi.PD_MACRO_INSTABILITY and f"macro step {so.failed_step}" in str(e.value)
     Ug, sg = E.run(U0, 5, bnd=bt, raise_on_instability=False)
     assert sg.failed_step == so.failed_step and np.array_equal(Ug, Uo)
+    # the FAST family (an 11x11 patch in the padded 16x16 tile) trips at the same step
+    F = Engine.from_problem(P, mode=FAST)
+    assert F.mode == FAST
+    _, sf = F.run(U0, 5, bnd=bt, raise_on_instability=False)
+    assert sf.failed_step == so.failed_step
 
 
 def test_error_paths(gpu):
@@ -626,3 +631,42 @@ def test_config5_maximum_size(restated, gpu):
     avg, _ = restated.patch_subset(ed, U0, 0.0, idx)
     pij = np.ctypeslib.as_array(ed.patch_ij, shape=(E.P, 2))[idx]
     assert rel(S[pij[:, 0], pij[:, 1]], avg) < 1e-13
+
+
+# ---------------------------------------------------------------------------
+# padded FAST tiles: any patch up to 16x16 micro nodes runs on the FAST path
+# (phantom nodes fill the 7/8/9/16 tile); full runs vs the oracle
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("nx,ny", [(4, 4), (5, 5), (9, 9), (10, 10), (12, 12), (14, 14), (10, 13), (6, 11),
+                                   (16, 16), (20, 20), (23, 23), (27, 19), (9, 24), (31, 20)])
+@pytest.mark.parametrize("name", ["c1_diffusion", "c4_shear"], ids=["5pt", "mixed"])
+def test_fast_padded_tiles_vs_oracle(nx, ny, name, restated, gpu):
+    over = dict(nx=nx, ny=ny, Nt=10) if name == "c1_diffusion" else dict(nx=nx, ny=ny, N_xi=9, N_eta=9, nt=20, Nt=5)
+    P = load(name, **over)
+    ed = P.engine_desc()
+    U0 = P.initial_field()
+    n = P.desc.Nt
+    bt = P.boundary_table(0.0, n)
+    st, Uo, _ = restated.run(ed, U0, n, bnd=bt)
+    assert st == 0
+    E = Engine.from_problem(P, mode=FAST)
+    assert E.mode == FAST
+    Ug, stats = E.run(U0, n, bnd=bt)
+    assert stats.steps_done == n
+    assert rel(Ug, Uo) < TOL
+
+
+@pytest.mark.parametrize("bc", ["dirichlet", "robin", "simpson"])
+@pytest.mark.parametrize("nx,ny", [(10, 12), (20, 22)], ids=["one-warp-tile", "32x32-tile"])
+def test_fast_padded_tiles_patch_conditions(bc, nx, ny, restated, gpu):
+    over = dict(nx=nx, ny=ny, Nt=10, **BC_CASES[bc])
+    P = load("c1_diffusion", **over)
+    ed = P.engine_desc()
+    U0 = P.initial_field()
+    bt = P.boundary_table(0.0, 10)
+    st, Uo, _ = restated.run(ed, U0, 10, bnd=bt)
+    assert st == 0
+    E = Engine.from_problem(P, mode=FAST)
+    assert E.mode == FAST
+    Ug, _ = E.run(U0, 10, bnd=bt)
+    assert rel(Ug, Uo) < TOL
