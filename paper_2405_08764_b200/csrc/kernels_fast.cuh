@@ -34,10 +34,13 @@ struct FastPlan {
     int big = 0; // 32x32 patches: kernels_fast_big.cuh (one CTA of 4 warps per patch)
 };
 
-template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_, bool PAD_ = false>
+template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_, bool PAD_ = false, bool GEN_ = false>
 struct FastCfg {
     static constexpr int N1 = N1_, N2 = N2_, BI = BI_, BJ = BJ_;
     static constexpr bool MIXED = MIXED_;
+    // GEN: Robin / Dirichlet patch conditions compiled in (the Neumann-only
+    // instantiation keeps the BASELINE kernels free of their branches)
+    static constexpr bool GEN = GEN_;
     // PAD: the patch (p.n1 x p.n2, runtime) is smaller than the N1 x N2 tile;
     // the extra "phantom" nodes carry zero weights and stay out of the restriction
     static constexpr bool PAD = PAD_;
@@ -96,7 +99,7 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
             // inward weight absorbs the outward one; the outward slot keeps the
             // original weight for the per-patch ghost constant (zeroed in k_fast).
             const bool Wb = i == 0, Eb = i == n1 - 1, Sb = j == 0, Nb = j == n2 - 1;
-            if (p.pinned && (Wb || Eb || Sb || Nb)) {
+            if (Cfg::GEN && p.pinned && (Wb || Eb || Sb || Nb)) {
                 val = 0.0; // pinned edge node: u' = its pinned value, set as the node constant
             } else {
                 switch (kind) {
@@ -216,7 +219,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
             const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
             const double sl = p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2;
-            if (p.bc_type == PD_BC_NEUMANN) {
+            if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 sg[gs][e][j] = p.gsc[e] * sl;
             } else { // Robin / Dirichlet need the edge value too (dirichlet_edge_values, gaptooth.cpp:110-130)
                 const double* w = p.vlag[e];
@@ -233,7 +236,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
             const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
             const double sl = p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2;
-            if (p.bc_type == PD_BC_NEUMANN) {
+            if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 sg[gs][e][i] = p.gsc[e] * sl;
             } else {
                 const double* w = p.vlag[e];
@@ -250,7 +253,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
     const double* gN = sg[gs][PD_EDGE_N];
     const double* gS = sg[gs][PD_EDGE_S];
     if constexpr (MIXED) {
-        if (p.pinned) {
+        if (Cfg::GEN && p.pinned) {
             // pinned ring nodes do not update; the interior reads real nodes only
         } else if constexpr (LP == 32) { // one patch per warp: closed form (measured faster at 16x16)
             for (int t = r; t < 2 * n2 + 2 * n1; t += LP) {
@@ -306,7 +309,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
             const bool Sb = jj == 0 && bj == 0;
             const bool Nb = Cfg::PAD ? j == n2 - 1 : (jj == BJ - 1 && bj == Cfg::LJ - 1);
             double cc = 0.0;
-            if (p.pinned) {
+            if (Cfg::GEN && p.pinned) {
                 // pinned edge nodes keep their value (all their weights are zero): the
                 // sweep's priority W, E, S, N for the value (microsim.cpp:306-311); a
                 // Dirichlet edge also pins the initial field, in W, E, S, N order with
@@ -524,27 +527,29 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
 }
 
 // ---- instantiations --------------------------------------------------------
-using FC7 = FastCfg<7, 7, 1, 7, false>;
-using FC7M = FastCfg<7, 7, 1, 7, true>;
-using FC8 = FastCfg<8, 8, 2, 4, false>;
-using FC8M = FastCfg<8, 8, 2, 4, true>;
-using FC9 = FastCfg<9, 9, 3, 3, false>;
-using FC9M = FastCfg<9, 9, 3, 3, true>;
-using FC16 = FastCfg<16, 16, 2, 4, false>;
-using FC16M = FastCfg<16, 16, 2, 4, true>;
-// padded tiles: any patch up to 16 x 16 micro nodes (phantom nodes fill the tile)
-using FC7P = FastCfg<7, 7, 1, 7, false, true>;
-using FC7MP = FastCfg<7, 7, 1, 7, true, true>;
-using FC8P = FastCfg<8, 8, 2, 4, false, true>;
-using FC8MP = FastCfg<8, 8, 2, 4, true, true>;
-using FC9P = FastCfg<9, 9, 3, 3, false, true>;
-using FC9MP = FastCfg<9, 9, 3, 3, true, true>;
-using FC16P = FastCfg<16, 16, 2, 4, false, true>;
-using FC16MP = FastCfg<16, 16, 2, 4, true, true>;
+// tiles: 7x7 (1x7 blocks, four patches per warp), 8x8 (2x4, four), 9x9 (3x3,
+// three), 16x16 (2x4, one); each with/without the mixed term, exact-fit or
+// padded (PAD), Neumann-only or with Robin/Dirichlet compiled in (GEN)
+#define PD_FAST_TILE(NAME, N, BI, BJ)                                                          \
+    using NAME = FastCfg<N, N, BI, BJ, false>;                                                 \
+    using NAME##M = FastCfg<N, N, BI, BJ, true>;                                               \
+    using NAME##P = FastCfg<N, N, BI, BJ, false, true>;                                        \
+    using NAME##MP = FastCfg<N, N, BI, BJ, true, true>;                                        \
+    using NAME##G = FastCfg<N, N, BI, BJ, false, false, true>;                                 \
+    using NAME##MG = FastCfg<N, N, BI, BJ, true, false, true>;                                 \
+    using NAME##PG = FastCfg<N, N, BI, BJ, false, true, true>;                                 \
+    using NAME##MPG = FastCfg<N, N, BI, BJ, true, true, true>;
+PD_FAST_TILE(FC7, 7, 1, 7)
+PD_FAST_TILE(FC8, 8, 2, 4)
+PD_FAST_TILE(FC9, 9, 3, 3)
+PD_FAST_TILE(FC16, 16, 2, 4)
+#undef PD_FAST_TILE
 
-#define PD_FAST_CONFIGS(X)                                                                                       \
-    X(0, FC7) X(1, FC7M) X(2, FC8) X(3, FC8M) X(4, FC9) X(5, FC9M) X(6, FC16) X(7, FC16M) X(8, FC7P) X(9, FC7MP) \
-        X(10, FC8P) X(11, FC8MP) X(12, FC9P) X(13, FC9MP) X(14, FC16P) X(15, FC16MP)
+#define PD_FAST_TILE_IDS(X, B, NAME) \
+    X(B + 0, NAME) X(B + 1, NAME##M) X(B + 2, NAME##P) X(B + 3, NAME##MP) X(B + 4, NAME##G) X(B + 5, NAME##MG) \
+        X(B + 6, NAME##PG) X(B + 7, NAME##MPG)
+#define PD_FAST_CONFIGS(X) \
+    PD_FAST_TILE_IDS(X, 0, FC7) PD_FAST_TILE_IDS(X, 8, FC8) PD_FAST_TILE_IDS(X, 16, FC9) PD_FAST_TILE_IDS(X, 24, FC16)
 
 inline bool plan_fast(const Params& p, FastPlan& plan) {
     // Neumann (every BASELINE config), Robin and Dirichlet patch conditions are
@@ -554,12 +559,14 @@ inline bool plan_fast(const Params& p, FastPlan& plan) {
     if (p.quad == PD_QUAD_SIMPSON && ((p.n1 - 1) % 2 || (p.n2 - 1) % 2)) return false;
     int id = -1;
     // an exact-fit tile first (compile-time extents), else the smallest padded tile
+    const bool gen = p.bc_type != PD_BC_NEUMANN;
 #define PD_MATCH(ID, CFG) \
-    if (id < 0 && !CFG::PAD && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
+    if (id < 0 && !CFG::PAD && CFG::GEN == gen && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
     PD_FAST_CONFIGS(PD_MATCH)
 #undef PD_MATCH
 #define PD_MATCH_PAD(ID, CFG) \
-    if (id < 0 && CFG::PAD && p.n1 <= CFG::N1 && p.n2 <= CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
+    if (id < 0 && CFG::PAD && CFG::GEN == gen && p.n1 <= CFG::N1 && p.n2 <= CFG::N2 && (p.mixed != 0) == CFG::MIXED) \
+        id = ID;
     PD_FAST_CONFIGS(PD_MATCH_PAD)
 #undef PD_MATCH_PAD
     if (id < 0) return false;

@@ -19,10 +19,11 @@
 
 namespace pdb200::dev {
 
-template <int N_, bool MIXED_, bool PAD_ = false>
+template <int N_, bool MIXED_, bool PAD_ = false, bool GEN_ = false>
 struct BigCfg {
     static constexpr int N1 = N_, N2 = N_, BI = 2, BJ = 4;
     static constexpr bool MIXED = MIXED_;
+    static constexpr bool GEN = GEN_; // Robin / Dirichlet patch conditions compiled in (as FastCfg)
     static constexpr bool PAD = PAD_; // patch smaller than the tile: phantom nodes (as FastCfg)
     static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, WPP = LP / 32;
     static constexpr int NPL = BI * BJ, NW = MIXED ? 6 : 5, NWL = NW * NPL, S = (NWL + 1) / 2;
@@ -72,7 +73,7 @@ __global__ void k_fold_big(Params p, const double* __restrict__ coeffs, const in
             const double ax = A * idx2, vx = Vx * idx, cy = C * idy2, vy = Vy * idy;
             const double wE = dt * (ax - vx), wW = dt * (ax + vx), wN = dt * (cy - vy), wS = dt * (cy + vy);
             const bool Wb = i == 0, Eb = i == n1 - 1, Sb = j == 0, Nb = j == n2 - 1;
-            if (p.pinned && (Wb || Eb || Sb || Nb)) {
+            if (Cfg::GEN && p.pinned && (Wb || Eb || Sb || Nb)) {
                 val = 0.0; // pinned edge node (as k_fold)
             } else {
                 switch (kind) { // same static reflections as k_fold
@@ -155,7 +156,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
             const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
             const double sl = p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2;
-            if (p.bc_type == PD_BC_NEUMANN) {
+            if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 s_g[e][j] = p.gsc[e] * sl;
             } else {
                 const double* w = p.vlag[e];
@@ -172,7 +173,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
             const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
             const double sl = p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2;
-            if (p.bc_type == PD_BC_NEUMANN) {
+            if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 s_g[e][i] = p.gsc[e] * sl;
             } else {
                 const double* w = p.vlag[e];
@@ -188,7 +189,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     const double* gW = s_g[PD_EDGE_W];
     const double* gN = s_g[PD_EDGE_N];
     const double* gS = s_g[PD_EDGE_S];
-    if constexpr (MIXED) if (!p.pinned) { // pinned ring nodes do not update
+    if constexpr (MIXED) if (!(Cfg::GEN && p.pinned)) { // pinned ring nodes do not update
         auto off = [&](int pp, int qq) {
             const int qc = qq < 0 ? 0 : (qq > n2 - 1 ? n2 - 1 : qq);
             const int pc = pp < 0 ? 0 : (pp > n1 - 1 ? n1 - 1 : pp);
@@ -243,7 +244,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
                 }
                 const bool Wb = i == 0, Eb = i == n1 - 1, Sb = j == 0, Nb = j == n2 - 1;
                 double cc = 0.0;
-                if (p.pinned) {
+                if (Cfg::GEN && p.pinned) {
                     if (Wb) cc = gW[j];
                     else if (Eb) cc = gE[j];
                     else if (Sb) cc = gS[i];
@@ -278,7 +279,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const bool Wb = ii == 0 && bi == 0, Eb = ii == BI - 1 && bi == LI - 1;
             const bool Hb = jj == 0 && etaEdge; // physical S (unmirrored) or N (mirrored) edge
             double cc = 0.0;
-            if (p.pinned) { // as patch_body: sweep priority W, E, S|N; Dirichlet pins u0 in W, E, S|N order
+            if (Cfg::GEN && p.pinned) { // as patch_body: sweep priority W, E, S|N; Dirichlet pins u0 in W, E, S|N order
                 if (Wb) cc = gW[j];
                 else if (Eb) cc = gE[j];
                 else if (Hb) cc = gEta[i];
@@ -439,6 +440,10 @@ using BC32 = BigCfg<32, false>;
 using BC32M = BigCfg<32, true>;
 using BC32P = BigCfg<32, false, true>;  // padded: any patch of 17..32 micro nodes per side
 using BC32MP = BigCfg<32, true, true>;
+using BC32G = BigCfg<32, false, false, true>; // with Robin / Dirichlet patch conditions
+using BC32MG = BigCfg<32, true, false, true>;
+using BC32PG = BigCfg<32, false, true, true>;
+using BC32MPG = BigCfg<32, true, true, true>;
 
 } // namespace pdb200::dev
 
@@ -453,7 +458,7 @@ inline bool plan_big(const Params& p, FastPlan& plan) {
     if (!exact && !pad) return false;
     plan.big = 1;
     plan.mixed = p.mixed;
-    plan.id = (p.mixed ? 101 : 100) + (pad ? 2 : 0);
+    plan.id = (p.mixed ? 101 : 100) + (pad ? 2 : 0) + (p.bc_type != PD_BC_NEUMANN ? 4 : 0);
     plan.LP = BC32::LP;
     plan.G = 1;
     plan.S = p.mixed ? BC32M::S : BC32::S;
@@ -461,7 +466,9 @@ inline bool plan_big(const Params& p, FastPlan& plan) {
     return true;
 }
 
-#define PD_BIG_CONFIGS(X) X(100, BC32) X(101, BC32M) X(102, BC32P) X(103, BC32MP)
+#define PD_BIG_CONFIGS(X)                                                                                  \
+    X(100, BC32) X(101, BC32M) X(102, BC32P) X(103, BC32MP) X(104, BC32G) X(105, BC32MG) X(106, BC32PG) \
+        X(107, BC32MPG)
 
 inline void fold_big(const FastPlan& plan, const Params& p, const double* coeffs, const int* cset, double* W,
                      cudaStream_t s) {
