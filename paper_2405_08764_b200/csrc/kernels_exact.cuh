@@ -9,6 +9,15 @@
 namespace pdb200::dev {
 
 constexpr int kExactThreads = 128;
+// threads per CTA of the fused EXACT step.  The ADI solver keeps only one
+// thread per micro line busy in its solves: with enough patches to fill the
+// chip, smaller CTAs (more of them per SM) win — measured on B200
+// (profiles/r01_adi.jsonl): 16 129 patches of 11^2 nodes 1.84 -> 0.83 ms with
+// 32 threads, of 21^2 nodes 7.62 -> 6.33 ms with 64; 81 patches prefer 128.
+inline int exact_threads(const Params& p) {
+    if (p.solver != PD_SOLVER_ADI || p.P < 8 * 148) return kExactThreads;
+    return p.L <= 16 ? 32 : 64;
+}
 
 inline size_t exact_smem_bytes(const Params& p) {
     size_t d = 2 * (size_t)p.N + 3 * 4 * (size_t)p.L + p.n1 + 11 + 4 * 6;

@@ -109,7 +109,7 @@ struct pd_engine {
         } else if (mode == PD_MODE_FAST) {
             launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
         } else {
-            k_gaptooth_exact<<<prm.P, kExactThreads, exact_smem_bytes(prm), stream>>>(
+            k_gaptooth_exact<<<prm.P, exact_threads(prm), exact_smem_bytes(prm), stream>>>(
                 prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail);
         }
         check_launch();
@@ -666,7 +666,7 @@ pd_status pd_integrate_batch(pd_engine* e, const double* u0, const int32_t* edge
             upload(e->d_srct.p, src_time, (size_t)p.nt * 8, e->stream);
             dsrc = e->d_srct.p;
         }
-        k_integrate_exact<<<p.P, kExactThreads, exact_smem_bytes(p), e->stream>>>(
+        k_integrate_exact<<<p.P, exact_threads(p), exact_smem_bytes(p), e->stream>>>(
             p, du0, dev_, des, e->d_kinds.p, e->d_rw.p, e->d_cset.p, e->d_coeffs.p, e->d_src.p, dsrc, duT);
         e->check_launch();
         download(uT, duT, nu * 8, e->stream);
