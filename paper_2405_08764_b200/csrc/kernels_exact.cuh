@@ -15,7 +15,9 @@ constexpr int kExactThreads = 128;
 // (profiles/r01_adi.jsonl): 16 129 patches of 11^2 nodes 1.84 -> 0.83 ms with
 // 32 threads, of 21^2 nodes 7.62 -> 6.33 ms with 64; 81 patches prefer 128.
 inline int exact_threads(const Params& p) {
-    if (p.solver != PD_SOLVER_ADI || p.P < 8 * 148) return kExactThreads;
+    // explicit: two-warp CTAs for many small patches (16 384 patches of 16^2: 3.52 -> 3.27 ms)
+    if (p.solver != PD_SOLVER_ADI) return (p.P >= 8 * 148 && p.N <= 256) ? 64 : kExactThreads;
+    if (p.P < 8 * 148) return kExactThreads;
     return p.L <= 16 ? 32 : 64;
 }
 
