@@ -34,19 +34,23 @@ struct FastPlan {
     int big = 0; // 32x32 patches: kernels_fast_big.cuh (one CTA of 4 warps per patch)
 };
 
-template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_, bool PAD_ = false, bool GEN_ = false>
+template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_, bool PAD_ = false, bool GEN_ = false, bool SRC_ = false>
 struct FastCfg {
     static constexpr int N1 = N1_, N2 = N2_, BI = BI_, BJ = BJ_;
     static constexpr bool MIXED = MIXED_;
     // GEN: Robin / Dirichlet patch conditions compiled in (the Neumann-only
     // instantiation keeps the BASELINE kernels free of their branches)
     static constexpr bool GEN = GEN_;
+    // SRC: separable source g = spatial * time(t)/l (microsim.cpp:272-277); the
+    // sixth weight slot (the mixed term's, unused without it) holds dt * spatial
+    static constexpr bool SRC = SRC_;
+    static_assert(!(MIXED_ && SRC_), "the source variant is compiled for the 5-point operator only");
     // PAD: the patch (p.n1 x p.n2, runtime) is smaller than the N1 x N2 tile;
     // the extra "phantom" nodes carry zero weights and stay out of the restriction
     static constexpr bool PAD = PAD_;
     static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, G = 32 / LP;
     static constexpr int NPL = BI * BJ;          // nodes per lane
-    static constexpr int NW = MIXED ? 6 : 5;     // weights per node: C,E,W,N,S,(D)
+    static constexpr int NW = (MIXED || SRC) ? 6 : 5; // weights per node: C,E,W,N,S,(D | source)
     static constexpr int NWL = NW * NPL;         // weight doubles per lane
     static constexpr int S = (NWL + 1) / 2;      // 16-byte slots per lane
     static constexpr int L = N1 > N2 ? N1 : N2;
@@ -61,7 +65,7 @@ constexpr int kFastWarps = 1; // one warp per CTA: warps retire and are replaced
 // of lane l is at ((u*S + s)*32 + l); lane-local weight index f = k*NPL + ii*BJ + jj.
 template <class Cfg>
 __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* __restrict__ cset,
-                       double* __restrict__ W, int nunits) {
+                       double* __restrict__ W, int nunits, const double* __restrict__ src_sp) {
     const size_t total = (size_t)nunits * 32 * (2 * Cfg::S);
     const double idx2 = 1.0 / (p.mdxi * p.mdxi), idy2 = 1.0 / (p.mdeta * p.mdeta);
     const double idx = 1.0 / (2.0 * p.mdxi), idy = 1.0 / (2.0 * p.mdeta);
@@ -107,7 +111,7 @@ __global__ void k_fold(Params p, const double* __restrict__ coeffs, const int* _
                     case WW: val = Eb ? wW + wE : wW; break;
                     case WN: val = Sb ? wN + wS : wN; break;
                     case WS: val = Nb ? wS + wN : wS; break;
-                    case WD: val = dt * (B * ixy); break;
+                    case WD: val = Cfg::SRC ? dt * src_sp[(size_t)set * p.N + k] : dt * (B * ixy); break;
                     default: { // Robin ghosts also carry cEdge * u(edge) (microsim.cpp:178-183)
                         double wc = 1.0 - dt * (2.0 * ax + 2.0 * cy + Wr);
                         if (Wb) wc += wW * p.cedge[PD_EDGE_W];
@@ -187,7 +191,8 @@ __device__ __forceinline__ double ring_offset(int N1, int N2, const double* gE, 
 template <class Cfg>
 __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg::S], const double (&v)[9], int lane,
                                            bool valid, int patch, double (*sg)[8][Cfg::L], double* sred,
-                                           const int* __restrict__ nbr, double* __restrict__ out, int out_mode) {
+                                           const int* __restrict__ nbr, double* __restrict__ out, int out_mode,
+                                           const double* __restrict__ srct) {
     constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LP = Cfg::LP, G = Cfg::G, NPL = Cfg::NPL;
     constexpr int N1 = Cfg::N1, N2 = Cfg::N2;
     constexpr bool MIXED = Cfg::MIXED;
@@ -420,6 +425,13 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
                     nu[ii][jj] = fma(WT(WD, ii, jj), up - dn, nu[ii][jj]);
                 }
         }
+        if constexpr (Cfg::SRC) { // + dt * spatial * time(t0 + step dt)/l  (microsim.cpp:272-277, 329)
+            const double ft = srct ? __ldg(srct + step) : 0.0; // no factors given: g = 0, as EXACT
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WD, ii, jj), ft, nu[ii][jj]);
+        }
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
@@ -494,7 +506,7 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 template <class Cfg>
 __global__ void __launch_bounds__(32 * kFastWarps)
 k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
-       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag) {
+       const double* __restrict__ Wt, int nunits, const int* __restrict__ fail_flag, const double* __restrict__ srct) {
     constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
     __shared__ double s_g[kFastWarps][G][8][L]; // ghost offsets + mixed-term ring offsets per edge
     __shared__ double s_red[kFastWarps][32];
@@ -523,7 +535,7 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
     double v[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + idx[q]) : 0.0;
-    patch_body<Cfg>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, out_mode);
+    patch_body<Cfg>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, out_mode, srct);
 }
 
 // ---- instantiations --------------------------------------------------------
@@ -544,28 +556,45 @@ PD_FAST_TILE(FC8, 8, 2, 4)
 PD_FAST_TILE(FC9, 9, 3, 3)
 PD_FAST_TILE(FC16, 16, 2, 4)
 #undef PD_FAST_TILE
+// separable-source variants (5-point operator): exact / padded x Neumann / general
+#define PD_FAST_SRC_TILE(NAME, N, BI, BJ)                                           \
+    using NAME##S = FastCfg<N, N, BI, BJ, false, false, false, true>;               \
+    using NAME##SP = FastCfg<N, N, BI, BJ, false, true, false, true>;               \
+    using NAME##SG = FastCfg<N, N, BI, BJ, false, false, true, true>;               \
+    using NAME##SPG = FastCfg<N, N, BI, BJ, false, true, true, true>;
+PD_FAST_SRC_TILE(FC7, 7, 1, 7)
+PD_FAST_SRC_TILE(FC8, 8, 2, 4)
+PD_FAST_SRC_TILE(FC9, 9, 3, 3)
+PD_FAST_SRC_TILE(FC16, 16, 2, 4)
+#undef PD_FAST_SRC_TILE
 
 #define PD_FAST_TILE_IDS(X, B, NAME) \
     X(B + 0, NAME) X(B + 1, NAME##M) X(B + 2, NAME##P) X(B + 3, NAME##MP) X(B + 4, NAME##G) X(B + 5, NAME##MG) \
         X(B + 6, NAME##PG) X(B + 7, NAME##MPG)
-#define PD_FAST_CONFIGS(X) \
-    PD_FAST_TILE_IDS(X, 0, FC7) PD_FAST_TILE_IDS(X, 8, FC8) PD_FAST_TILE_IDS(X, 16, FC9) PD_FAST_TILE_IDS(X, 24, FC16)
+#define PD_FAST_SRC_IDS(X, B, NAME) X(B + 0, NAME##S) X(B + 1, NAME##SP) X(B + 2, NAME##SG) X(B + 3, NAME##SPG)
+#define PD_FAST_CONFIGS(X)                                                                                         \
+    PD_FAST_TILE_IDS(X, 0, FC7) PD_FAST_TILE_IDS(X, 8, FC8) PD_FAST_TILE_IDS(X, 16, FC9) PD_FAST_TILE_IDS(X, 24, FC16) \
+        PD_FAST_SRC_IDS(X, 32, FC7) PD_FAST_SRC_IDS(X, 36, FC8) PD_FAST_SRC_IDS(X, 40, FC9) PD_FAST_SRC_IDS(X, 44, FC16)
 
 inline bool plan_fast(const Params& p, FastPlan& plan) {
     // Neumann (every BASELINE config), Robin and Dirichlet patch conditions are
     // folded into the weights / node constants, both quadratures into the
     // restriction (Simpson exists only for odd node counts); sources stay EXACT
-    if (p.source != PD_SOURCE_ZERO) return false;
+    const bool src = p.source == PD_SOURCE_SEPARABLE;
+    if (p.source != PD_SOURCE_ZERO && !(src && !p.mixed)) return false; // sources: 5-point variant only
     if (p.quad == PD_QUAD_SIMPSON && ((p.n1 - 1) % 2 || (p.n2 - 1) % 2)) return false;
     int id = -1;
     // an exact-fit tile first (compile-time extents), else the smallest padded tile
     const bool gen = p.bc_type != PD_BC_NEUMANN;
-#define PD_MATCH(ID, CFG) \
-    if (id < 0 && !CFG::PAD && CFG::GEN == gen && p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
+#define PD_MATCH(ID, CFG)                                                                                       \
+    if (id < 0 && !CFG::PAD && CFG::GEN == gen && CFG::SRC == src && p.n1 == CFG::N1 && p.n2 == CFG::N2 &&        \
+        (p.mixed != 0) == CFG::MIXED)                                                                               \
+        id = ID;
     PD_FAST_CONFIGS(PD_MATCH)
 #undef PD_MATCH
-#define PD_MATCH_PAD(ID, CFG) \
-    if (id < 0 && CFG::PAD && CFG::GEN == gen && p.n1 <= CFG::N1 && p.n2 <= CFG::N2 && (p.mixed != 0) == CFG::MIXED) \
+#define PD_MATCH_PAD(ID, CFG)                                                                                   \
+    if (id < 0 && CFG::PAD && CFG::GEN == gen && CFG::SRC == src && p.n1 <= CFG::N1 && p.n2 <= CFG::N2 &&         \
+        (p.mixed != 0) == CFG::MIXED)                                                                               \
         id = ID;
     PD_FAST_CONFIGS(PD_MATCH_PAD)
 #undef PD_MATCH_PAD
@@ -589,20 +618,21 @@ inline size_t fast_weights_count(const FastPlan& plan, const Params&) {
 }
 
 inline void fold_weights(const FastPlan& plan, const Params& p, const double* coeffs, const int* cset, double* W,
-                         cudaStream_t s) {
+                         cudaStream_t s, const double* src_sp) {
     const size_t total = fast_weights_count(plan, p);
     const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
 #define PD_FOLD(ID, CFG) \
-    if (plan.id == ID) k_fold<CFG><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits);
+    if (plan.id == ID) k_fold<CFG><<<blocks, 256, 0, s>>>(p, coeffs, cset, W, plan.nunits, src_sp);
     PD_FAST_CONFIGS(PD_FOLD)
 #undef PD_FOLD
 }
 
 inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, double* out, int out_mode,
-                        const int* nbr, const double* W, const int* fail, cudaStream_t s) {
+                        const int* nbr, const double* W, const int* fail, cudaStream_t s, const double* srct) {
     const int blocks = (plan.nunits + kFastWarps - 1) / kFastWarps;
 #define PD_LAUNCH(ID, CFG) \
-    if (plan.id == ID) k_fast<CFG><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail);
+    if (plan.id == ID)     \
+        k_fast<CFG><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail, srct);
     PD_FAST_CONFIGS(PD_LAUNCH)
 #undef PD_LAUNCH
 }

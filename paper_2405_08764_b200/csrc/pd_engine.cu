@@ -107,7 +107,7 @@ struct pd_engine {
         } else if (mode == PD_MODE_FAST && fast.big) {
             launch_big(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
         } else if (mode == PD_MODE_FAST) {
-            launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
+            launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream, srct);
         } else {
             k_gaptooth_exact<<<prm.P, exact_threads(prm), exact_smem_bytes(prm), stream>>>(
                 prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail);
@@ -405,7 +405,7 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             CUDA_TRY(cudaFuncSetAttribute(k_integrate_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)exact_smem_bytes(p)));
         }
-        if (d.mode == PD_MODE_FAST && d.source_kind == PD_SOURCE_ZERO && d.solver == PD_SOLVER_EXPLICIT) {
+        if (d.mode == PD_MODE_FAST && d.solver == PD_SOLVER_EXPLICIT) { // the plans decide on sources
             if (plan_big(p, e->fast)) {
                 const size_t wcount = fast_weights_count(e->fast, p);
                 e->d_weights.alloc(wcount);
@@ -416,7 +416,7 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             } else if (plan_fast(p, e->fast)) {
                 const size_t wcount = fast_weights_count(e->fast, p);
                 e->d_weights.alloc(wcount);
-                fold_weights(e->fast, p, e->d_coeffs.p, e->d_cset.p, e->d_weights.p, e->stream);
+                fold_weights(e->fast, p, e->d_coeffs.p, e->d_cset.p, e->d_weights.p, e->stream, e->d_src.p);
                 e->check_launch();
                 e->device_bytes += wcount * 8;
                 e->mode = PD_MODE_FAST;
