@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define PD_ABI_VERSION 2
+#define PD_ABI_VERSION 3
 
 /* Status codes map 1:1 onto the reference exception types
  * (proj/include/patchdyn/errors.hpp:9-61). */
@@ -131,6 +131,13 @@ typedef struct pd_engine_desc {
     int32_t solver;
     int32_t upwind_order;
     double upwind_r;
+    /* On-device mesh/metric generation: when coeffs == NULL and
+     * this points at a built-in problem (pd_problem_desc, PD_PROBLEM_*), the
+     * engine computes the coefficient table (and a separable source's spatial
+     * table) on the GPU instead of copying host tables, sampling each set at
+     * the first patch that uses it.  Agrees with the host table to a few ulp
+     * (the transcendental library differs).  NULL otherwise. */
+    const struct pd_problem_desc* coeff_generator;
 } pd_engine_desc;
 
 typedef struct pd_engine pd_engine;
@@ -273,6 +280,7 @@ enum {
     PD_PROBLEM_STEADY = 12           /* harmonic u = x + y (test_gaptooth.cpp:32-49) */
 };
 enum { PD_DT_GIVEN = 0, PD_DT_DIFFUSION = 1, PD_DT_METRIC = 2 };
+enum { PD_COEFF_HOST = 0, PD_COEFF_DEVICE = 1 };
 
 typedef struct pd_problem_desc {
     int32_t problem;
@@ -300,6 +308,8 @@ typedef struct pd_problem_desc {
     int32_t solver;      /* PD_SOLVER_* */
     int32_t upwind_order;/* PD_UPWIND_* (ADI) */
     double upwind_r;     /* four-point upwind parameter r (ADI) */
+    int32_t coeff_gen;   /* PD_COEFF_HOST: host tables (bit-identical to the reference's sampling);
+                            PD_COEFF_DEVICE: no host tables, engines generate them on the GPU */
 } pd_problem_desc;
 
 typedef struct pd_problem pd_problem;
@@ -327,6 +337,15 @@ pd_status pd_problem_exact(const pd_problem* p, double t, double* U_host);
 /* max |A|+|C| over all sampled nodes (the dt pin's denominator) and the
  * reference's single-direction stability number (microsim.cpp:253-262). */
 pd_status pd_problem_stability(const pd_problem* p, double* max_a_plus_c, double* ref_number);
+
+/* The device generator on its own (desc->coeff_generator must be set): the
+ * table into coeffs_host [ncoeff_sets][PD_NCOEF][n1][n2] and the source's
+ * spatial table into source_spatial_host [ncoeff_sets][n1][n2] (either may be
+ * NULL); stats[5] = max(|A|,|C|), max(|A|+|C|), max|B|, generator kernel ms
+ * (CUDA events), micro nodes generated.  PD_NON_POSITIVE_JACOBIAN as
+ * geometry.cpp:80-91 when J <= 1e-14 at some node. */
+pd_status pd_coeffs_generate(const pd_engine_desc* desc, double* coeffs_host, double* source_spatial_host,
+                             double* stats);
 
 #ifdef __cplusplus
 }

@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-PD_ABI_VERSION = 2
+PD_ABI_VERSION = 3
 
 # pd_status  (errors.hpp:9-61 mapping)
 PD_OK = 0
@@ -47,6 +47,7 @@ PD_PROBLEM_REF_CDR = 11
 PD_PROBLEM_REF_CDR_VAR = 13
 PD_PROBLEM_STEADY = 12
 PD_DT_GIVEN, PD_DT_DIFFUSION, PD_DT_METRIC = 0, 1, 2
+PD_COEFF_HOST, PD_COEFF_DEVICE = 0, 1
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -65,6 +66,7 @@ class EngineDesc(C.Structure):
         ("source_kind", C.c_int32), ("source_spatial", _dp), ("l", C.c_double),
         ("mode", C.c_int32),
         ("solver", C.c_int32), ("upwind_order", C.c_int32), ("upwind_r", C.c_double),
+        ("coeff_generator", C.c_void_p),  # const pd_problem_desc* (on-device table generation)
     ]
 
 
@@ -89,6 +91,7 @@ class ProblemDesc(C.Structure):
         ("dt_rule", C.c_int32), ("h_frac", C.c_double), ("dt_over_tau", C.c_double),
         ("threads", C.c_int32),
         ("solver", C.c_int32), ("upwind_order", C.c_int32), ("upwind_r", C.c_double),
+        ("coeff_gen", C.c_int32),
     ]
 
 

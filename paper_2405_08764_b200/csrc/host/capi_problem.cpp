@@ -64,7 +64,20 @@ pd_status pd_problem_create(const pd_problem_desc* desc, pd_problem** out) {
         pdb200::cpi::SchemeConfig cfg = pdb200::cpi::scheme_from_desc(r);
         if (r.dt_rule != PD_DT_GIVEN && !(cfg.tau > 0)) cfg.tau = 1.0; // placeholder until resolved
         if (r.dt_over_tau > 0 && !(cfg.T > 0)) cfg.T = 1.0;
-        P->tables = pdb200::build_tables(s, cfg, r.threads);
+        const bool devgen = r.coeff_gen == PD_COEFF_DEVICE;
+        P->tables = pdb200::build_tables(s, cfg, r.threads, !devgen);
+        if (devgen) { // no host tables; one reduction-only generator pass for the pins/guards
+            pd_engine_desc& ed = P->tables.desc;
+            ed.coeff_generator = &P->desc;
+            double st[5];
+            const pd_status gst = pd_coeffs_generate(&ed, nullptr, nullptr, st);
+            if (gst != PD_OK) throw pdb200::Error(gst, pd_last_error(nullptr));
+            P->tables.max_abs_ac = st[0];
+            P->tables.max_a_plus_c = st[1];
+            P->tables.max_abs_b = st[2];
+            if (st[2] > 0.0 && ed.bc_type == PD_BC_ROBIN)
+                throw pdb200::MixedTermUnsupported("mixed-derivative term with Robin patch conditions is not defined");
+        }
         // micro dt pins
         const double dmin = std::min(r.h_xi / r.nx, r.h_eta / r.ny);
         if (r.dt_rule == PD_DT_DIFFUSION) {

@@ -301,11 +301,11 @@ void EngineTables::relink() {
     desc.npatches = static_cast<int32_t>(patch_ij.size() / 2);
     desc.patch_ij = patch_ij.data();
     desc.coeff_set = coeff_set.empty() ? nullptr : coeff_set.data();
-    desc.coeffs = coeffs.data();
+    desc.coeffs = coeffs.empty() ? nullptr : coeffs.data();
     desc.source_spatial = source_spatial.empty() ? nullptr : source_spatial.data();
 }
 
-EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfig& cfg, int threads) {
+EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfig& cfg, int threads, bool sample) {
     if (!p.coeffs_time_independent)
         throw Unsupported("time-dependent coefficients are not on the device path");
     if (!p.source_zero && !p.source_separable)
@@ -371,6 +371,10 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
     d.ncoeff_sets = S;
     const int n1 = cfg.nx + 1, n2 = cfg.ny + 1;
     const size_t N = static_cast<size_t>(n1) * n2;
+    if (!sample) {
+        t.relink();
+        return t;
+    }
     t.coeffs.assign(static_cast<size_t>(S) * PD_NCOEF * N, 0.0);
     if (!p.source_zero) t.source_spatial.assign(static_cast<size_t>(S) * N, 0.0);
 

@@ -118,7 +118,10 @@ struct EngineTables {
 // Samples the solver-form coefficients for every patch (or every eta-row when
 // the reference would share integrators across the row).  Does not check the
 // explicit stability guard (that needs the final dt; see check_stability).
-EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfig& cfg, int threads);
+// sample = false: patch list and set map only (coefficients generated on the
+// device, pd_coeffgen.cu); the maxima then come from the generator.
+EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfig& cfg, int threads,
+                          bool sample = true);
 // PatchIntegrator's explicit guard  microsim.cpp:253-262
 void check_stability(const EngineTables& t, const cpi::SchemeConfig& cfg);
 

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "coeffgen.hpp"
 #include "kernels_adi.cuh"
 #include "kernels_exact.cuh"
 #include "kernels_fast.cuh"
@@ -79,6 +80,7 @@ struct pd_engine {
     DevBuf<int32_t> d_pij, d_nbr, d_cset, d_kinds, d_fail, d_cset_items;
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
     DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
+    double coeffgen_ms = 0.0;           // on-device table generation time at create (0: host tables)
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     bool subset = false;                // the patch list covers only part of the interior
     DevBuf<unsigned long long> d_slot;
@@ -178,13 +180,14 @@ void validate_desc(const pd_engine_desc* d) {
     if (!(d->h_xi > 0 && d->h_eta > 0 && d->tau > 0)) bad("micro grid needs positive h_xi, h_eta, tau");
     if (d->k < 0) bad("k must be non-negative");
     if (!(d->dt_macro > 0)) bad("macro step must be positive");
-    if (!d->coeffs) bad("coefficient table missing");
+    if (!d->coeffs && !d->coeff_generator) bad("coefficient table missing");
     if (d->ncoeff_sets < 1) bad("no coefficient sets");
     if (d->quadrature == PD_QUAD_SIMPSON && (d->nx % 2 || d->ny % 2))
         throw Status{PD_VALIDATION_ERROR, "Simpson restriction needs an even micro resolution"};
     if (d->bc_type == PD_BC_ROBIN && d->robin_w1 == 0.0 && d->robin_w2 == 0.0)
         bad("robin patch conditions need nonzero weights");
-    if (d->source_kind == PD_SOURCE_SEPARABLE && !d->source_spatial) bad("separable source needs a spatial table");
+    if (d->source_kind == PD_SOURCE_SEPARABLE && !d->source_spatial && !d->coeff_generator)
+        bad("separable source needs a spatial table");
     if (d->solver != PD_SOLVER_EXPLICIT && d->solver != PD_SOLVER_ADI) bad("unknown micro-solver");
     if (d->upwind_order < PD_UPWIND_TWO || d->upwind_order > PD_UPWIND_FOUR) bad("upwind order must be two, three or four");
     // the reference sizes its banded line matrix once per ADI step for the xi
@@ -280,6 +283,8 @@ pd_status guarded(pd_engine* e, F&& fn) {
         return PD_OK;
     } catch (const Status& s) {
         return fail_engine(e, s);
+    } catch (const pdb200::Error& x) { // host-side error types carry their status
+        return fail_engine(e, Status{static_cast<pd_status>(x.status), x.what()});
     } catch (const std::exception& x) {
         return fail_engine(e, Status{PD_VALIDATION_ERROR, x.what()});
     }
@@ -353,13 +358,32 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
         const size_t Ncoef = (size_t)d.ncoeff_sets * PD_NCOEF * p.N;
         double max_ac = 0.0;
         bool mixed = false;
-        for (int s = 0; s < d.ncoeff_sets; ++s) {
-            const double* c = d.coeffs + (size_t)s * PD_NCOEF * p.N;
-            for (int k = 0; k < p.N; ++k) {
-                max_ac = std::max({max_ac, std::fabs(c[PD_COEF_A * p.N + k]), std::fabs(c[PD_COEF_C * p.N + k])});
-                if (c[PD_COEF_B * p.N + k] != 0.0) mixed = true;
+        CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->own_stream = true;
+        CUDA_TRY(cudaEventCreate(&e->ev0));
+        CUDA_TRY(cudaEventCreate(&e->ev1));
+        const bool generate = !d.coeffs && d.coeff_generator;
+        if (generate) { // on-device mesh/metric generation (pd_coeffgen.cu)
+            const std::vector<int32_t> centres = pdb200::coeffgen_set_centres(d, e->pij.data(), P);
+            e->d_coeffs.alloc(Ncoef);
+            if (d.source_kind == PD_SOURCE_SEPARABLE) e->d_src.alloc((size_t)d.ncoeff_sets * p.N);
+            const pdb200::CoeffGenStats gs =
+                pdb200::coeffgen_run(*d.coeff_generator, d, centres.data(), e->d_coeffs.p, e->d_src.p, e->stream);
+            max_ac = gs.max_abs_ac;
+            mixed = gs.max_abs_b > 0.0;
+            e->coeffgen_ms = gs.device_ms;
+        } else {
+            for (int s = 0; s < d.ncoeff_sets; ++s) {
+                const double* c = d.coeffs + (size_t)s * PD_NCOEF * p.N;
+                for (int k = 0; k < p.N; ++k) {
+                    max_ac = std::max({max_ac, std::fabs(c[PD_COEF_A * p.N + k]), std::fabs(c[PD_COEF_C * p.N + k])});
+                    if (c[PD_COEF_B * p.N + k] != 0.0) mixed = true;
+                }
             }
         }
+        e->d.coeffs = nullptr; // host tables are not referenced after create
+        e->d.source_spatial = nullptr;
+        e->d.coeff_generator = nullptr;
         p.mixed = mixed ? 1 : 0;
         if (mixed && d.solver == PD_SOLVER_ADI)
             throw Status{PD_MIXED_TERM_UNSUPPORTED, "mixed-derivative term with the ADI micro-solver is not defined"};
@@ -376,10 +400,6 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
         e->subset = P < (d.Nxi - (d.periodic_xi ? 0 : 1)) * (d.Neta - 1);
         e->perim = pd_perimeter_len(d.Nxi, d.Neta);
         // device
-        CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-        e->own_stream = true;
-        CUDA_TRY(cudaEventCreate(&e->ev0));
-        CUDA_TRY(cudaEventCreate(&e->ev1));
         e->d_pij.alloc(e->pij.size());
         e->d_nbr.alloc(e->nbr.size());
         upload(e->d_pij.p, e->pij.data(), e->pij.size() * 4, e->stream);
@@ -388,11 +408,13 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             e->d_cset.alloc(e->cset.size());
             upload(e->d_cset.p, e->cset.data(), e->cset.size() * 4, e->stream);
         }
-        e->d_coeffs.alloc(Ncoef);
-        upload(e->d_coeffs.p, d.coeffs, Ncoef * 8, e->stream);
-        if (d.source_kind == PD_SOURCE_SEPARABLE) {
-            e->d_src.alloc((size_t)d.ncoeff_sets * p.N);
-            upload(e->d_src.p, d.source_spatial, (size_t)d.ncoeff_sets * p.N * 8, e->stream);
+        if (!generate) {
+            e->d_coeffs.alloc(Ncoef);
+            upload(e->d_coeffs.p, d.coeffs, Ncoef * 8, e->stream);
+            if (d.source_kind == PD_SOURCE_SEPARABLE) {
+                e->d_src.alloc((size_t)d.ncoeff_sets * p.N);
+                upload(e->d_src.p, d.source_spatial, (size_t)d.ncoeff_sets * p.N * 8, e->stream);
+            }
         }
         e->d_U.alloc(2 * e->NF);
         e->d_fail.alloc(4);

@@ -90,13 +90,14 @@ def lib() -> C.CDLL:
     L.pd_device_count.restype = C.c_int32
     L.pd_bench_step_kernel.argtypes = [vp, vp, vp, C.c_int32, _dp]
     L.pd_bench_fp64_peak.argtypes = [C.c_double, _dp, _dp]
+    L.pd_coeffs_generate.argtypes = [C.POINTER(EngineDesc), _dp, _dp, _dp]
     for name in ["pd_bench_step_kernel", "pd_bench_fp64_peak", "pd_engine_create", "pd_engine_tables", "pd_engine_set_stream", "pd_gaptooth_step",
                  "pd_projective_step", "pd_projective_step_device", "pd_run", "pd_run_device",
                  "pd_integrate_batch", "pd_lift_batch", "pd_restrict_batch", "pd_evolve_batch",
                  "pd_linear_weights", "pd_engine_set_linear", "pd_engine_set_step_kind", "pd_problem_create",
                  "pd_problem_resolved", "pd_problem_engine_desc", "pd_problem_initial_field",
                  "pd_problem_boundary", "pd_problem_boundary_table", "pd_problem_exact",
-                 "pd_problem_stability"]:
+                 "pd_problem_stability", "pd_coeffs_generate"]:
         getattr(L, name).restype = C.c_int32
     _lib = L
     return L
@@ -193,6 +194,20 @@ def fp64_peak(ms_target: float = 200.0):
     tf, ghz = C.c_double(), C.c_double()
     _check(lib().pd_bench_fp64_peak(ms_target, C.byref(tf), C.byref(ghz)))
     return tf.value, ghz.value
+
+
+def generate_coeffs(desc: EngineDesc, tables: bool = True):
+    """On-device mesh/metric generation (pd_coeffs_generate; desc.coeff_generator
+    set, e.g. the engine_desc of a Problem created with coeff_gen=PD_COEFF_DEVICE).
+    Returns (coeffs [sets][6][n1][n2] or None, source spatial [sets][n1][n2] or
+    None, stats dict)."""
+    n1, n2, S = desc.nx + 1, desc.ny + 1, desc.ncoeff_sets
+    co = np.empty((S, abi.PD_NCOEF, n1, n2)) if tables else None
+    sp = np.empty((S, n1, n2)) if tables and desc.source_kind == abi.PD_SOURCE_SEPARABLE else None
+    st = np.empty(5)
+    _check(lib().pd_coeffs_generate(C.byref(desc), _d(co), _d(sp), _d(st)))
+    return co, sp, {"max_abs_ac": st[0], "max_a_plus_c": st[1], "max_abs_b": st[2], "device_ms": st[3],
+                    "nodes": int(st[4])}
 
 
 def index_tables(desc: EngineDesc):

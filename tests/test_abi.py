@@ -192,3 +192,19 @@ def test_separable_source_time_factors():
     assert st.shape == (2, 1, 500)
     assert st[1, 0, 250] == pytest.approx(np.exp(dt + tau / 2), rel=1e-15)
     assert Problem(configs.load("c1_diffusion")[0]).source_time(0.0, 1) is None
+
+
+def test_device_coefficient_generation_fails_loudly_without_a_gpu():
+    """coeff_gen = PD_COEFF_DEVICE never falls back to host sampling: on a host
+    without a CUDA device the problem build reports a device error."""
+    from paper_2405_08764_b200.engine import device_count
+
+    if device_count() > 0:
+        pytest.skip("a CUDA device is visible (covered by tests/test_gpu.py)")
+    d = configs.copy_desc(configs.load("c1_diffusion")[0], coeff_gen=abi.PD_COEFF_DEVICE)
+    with pytest.raises(PatchdynError) as ei:
+        Problem(d)
+    assert ei.value.status == abi.PD_CUDA_ERROR
+    # the host path of the same problem is unaffected and still builds its tables
+    ed = Problem(configs.copy_desc(d, coeff_gen=abi.PD_COEFF_HOST)).engine_desc()
+    assert ed.coeffs and not ed.coeff_generator

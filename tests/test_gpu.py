@@ -695,3 +695,91 @@ def test_fast_padded_tiles_patch_conditions(bc, nx, ny, restated, gpu):
     assert E.mode == FAST
     Ug, _ = E.run(U0, 10, bnd=bt)
     assert rel(Ug, Uo) < TOL
+
+
+# ---------------------------------------------------------------------------
+# on-device mesh/metric generation (csrc/pd_coeffgen.cu)
+# ---------------------------------------------------------------------------
+def _ref_cdr(problem, lam):
+    d = configs.default_desc()
+    d.problem = problem
+    d.lambda_ = lam
+    d.N_xi = d.N_eta = 10
+    d.Nt, d.T, d.tau = 1001, 1.0, 1e-6
+    d.nx = d.ny = 10
+    d.nt = 2000  # explicit guard with the stretched metric and D = 1 + x
+    return d
+
+
+GEN_CASES = {
+    "c1_diffusion": lambda: configs.load("c1_diffusion")[0],
+    "c2_cdr_tanh": lambda: configs.load("c2_cdr_tanh")[0],
+    "c3_annulus": lambda: configs.load("c3_annulus")[0],
+    "c4_shear": lambda: configs.copy_desc(configs.load("c4_shear")[0], N_xi=65, N_eta=65),
+    "ref_annulus": lambda: configs.load("ref_annulus_16x10")[0],
+    "ref_cdr_stretched": lambda: _ref_cdr(abi.PD_PROBLEM_REF_CDR, 0.5),
+    "ref_cdr_var": lambda: _ref_cdr(abi.PD_PROBLEM_REF_CDR_VAR, 0.3),
+    "steady": lambda: configs.copy_desc(configs.default_desc(), problem=abi.PD_PROBLEM_STEADY, nt=500),
+}
+
+
+def _host_tables(P):
+    ed = P.engine_desc()
+    n1, n2, S = ed.nx + 1, ed.ny + 1, ed.ncoeff_sets
+    co = np.ctypeslib.as_array(ed.coeffs, shape=(S, abi.PD_NCOEF, n1, n2)).copy()
+    sp = (np.ctypeslib.as_array(ed.source_spatial, shape=(S, n1, n2)).copy()
+          if ed.source_kind == abi.PD_SOURCE_SEPARABLE else None)
+    return co, sp
+
+
+@pytest.mark.parametrize("name", list(GEN_CASES))
+def test_coeffgen_matches_host_tables(name, gpu):
+    """The device generator reproduces the host (reference-order) sampling to a
+    few ulp: same evaluation order, only the transcendental library differs."""
+    from paper_2405_08764_b200.engine import generate_coeffs
+
+    d = GEN_CASES[name]()
+    Ph = Problem(configs.copy_desc(d, coeff_gen=abi.PD_COEFF_HOST))
+    Pd = Problem(configs.copy_desc(d, coeff_gen=abi.PD_COEFF_DEVICE))
+    co_h, sp_h = _host_tables(Ph)
+    ed = Pd.engine_desc()
+    assert not ed.coeffs and ed.coeff_generator  # no host table was built
+    co_d, sp_d, st = generate_coeffs(ed)
+    assert co_d.shape == co_h.shape and st["nodes"] == co_h.shape[0] * co_h.shape[2] * co_h.shape[3]
+    for c in range(abi.PD_NCOEF):  # per coefficient, relative to its largest entry
+        scale = max(np.abs(co_h[:, c]).max(), 1e-300)
+        assert np.abs(co_d[:, c] - co_h[:, c]).max() <= 1e-13 * scale, c
+    assert (co_d[:, abi.PD_COEF_B] != 0).any() == (co_h[:, abi.PD_COEF_B] != 0).any()
+    if sp_h is not None:
+        assert np.abs(sp_d - sp_h).max() <= 1e-13 * np.abs(sp_h).max()
+    # the pins and guards see the same maxima: resolved tau / T agree to rounding
+    assert Pd.desc.tau == pytest.approx(Ph.desc.tau, rel=1e-14)
+    assert Pd.desc.T == pytest.approx(Ph.desc.T, rel=1e-14)
+    assert st["max_a_plus_c"] == pytest.approx(Ph.stability()[0], rel=1e-14)
+
+
+@pytest.mark.parametrize("name", ["c1_diffusion", "c3_annulus", "c4_shear", "ref_cdr_stretched"])
+@pytest.mark.parametrize("mode", [EXACT, FAST], ids=["exact", "fast"])
+def test_coeffgen_engine_run_matches_host_tables(name, mode, gpu):
+    d = GEN_CASES[name]()
+    Ph = Problem(configs.copy_desc(d, coeff_gen=abi.PD_COEFF_HOST))
+    Pd = Problem(configs.copy_desc(d, coeff_gen=abi.PD_COEFF_DEVICE))
+    n = 3
+    U0 = Ph.initial_field()
+    bt, stt = Ph.boundary_table(0.0, n), Ph.source_time(0.0, n)
+    Eh = Engine.from_problem(Ph, mode=mode)
+    Ed = Engine.from_problem(Pd, mode=mode)
+    assert Ed.mode == Eh.mode
+    Uh, _ = Eh.run(U0, n, bnd=bt, src_time=stt)
+    Ud, _ = Ed.run(U0, n, bnd=bt, src_time=stt)
+    # ulp-level table differences, amplified by the projective step's dt/tau (~1000 for ref-cdr)
+    assert rel(Ud, Uh) < max(1e-12, 1e-13 * (Ph.desc.T / Ph.desc.Nt) / Ph.desc.tau)
+
+
+def test_coeffgen_rejects_folded_maps_like_the_host(gpu):
+    # x = xi + A sin 2pi eta, y = eta + A sin 2pi xi has J = 1 - (2 pi A)^2 cos cos < 0 somewhere for A = 0.2
+    d = configs.copy_desc(GEN_CASES["c4_shear"](), amp=0.2)
+    for gen in (abi.PD_COEFF_HOST, abi.PD_COEFF_DEVICE):
+        with pytest.raises(PatchdynError) as ei:
+            Problem(configs.copy_desc(d, coeff_gen=gen))
+        assert ei.value.status == abi.PD_NON_POSITIVE_JACOBIAN
