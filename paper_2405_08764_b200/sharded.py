@@ -70,6 +70,8 @@ def slabs(Nxi: int, periodic: bool, world: int) -> list[Slab]:
 def subset_desc(ed: EngineDesc, slab: Slab) -> EngineDesc:
     """pd_engine_desc restricted to the slab's patches (reference order kept),
     with only the coefficient sets those patches use."""
+    if not ed.coeffs:
+        raise ValueError("subset_desc slices host coefficient tables (build the problem with coeff_gen=PD_COEFF_HOST)")
     P = ed.npatches
     pij = np.ctypeslib.as_array(ed.patch_ij, shape=(P, 2)).copy()
     sel = np.nonzero((pij[:, 0] >= slab.i0) & (pij[:, 0] < slab.i1))[0]
