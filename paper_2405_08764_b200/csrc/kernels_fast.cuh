@@ -21,8 +21,13 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "pd_device.cuh"
+#include "kernels_misc.cuh"
 
 
 namespace pdb200::dev {
@@ -139,6 +144,11 @@ __device__ __forceinline__ double quad_weight(int k, int quad) {
     return end ? te : tr;
 }
 
+// a0*b0 + a1*b1 + a2*b2 with a fixed rounding (two fma, left to right)
+__device__ __forceinline__ double dot3(double a0, double b0, double a1, double b1, double a2, double b2) {
+    return __fma_rn(a2, b2, __fma_rn(a1, b1, __dmul_rn(a0, b0)));
+}
+
 __device__ __forceinline__ double quad_weight_rt(int k, int n, int quad) {
     const bool end = k == 0 || k == n;
     if (quad == PD_QUAD_SIMPSON) return (end ? 1.0 : ((k & 1) ? 4.0 : 2.0)) / (3.0 * n);
@@ -150,8 +160,8 @@ __device__ __forceinline__ double quad_weight_rt(int k, int n, int quad) {
 // or, on a pinned edge, the pinned value (pinned_value, microsim.cpp:189-192).
 __device__ __forceinline__ double edge_constant(const Params& p, int e, double value, double slope) {
     if (p.bc_type == PD_BC_DIRICHLET) return value;
-    if (p.pinned) return value + p.w2 / p.w1 * slope; // Robin with w2 ~ 0 behaves as Dirichlet
-    return p.gsc[e] * ((p.w1 * value + p.w2 * slope) / p.w2);
+    if (p.pinned) return __fma_rn(__ddiv_rn(p.w2, p.w1), slope, value); // Robin with w2 ~ 0 behaves as Dirichlet
+    return __dmul_rn(p.gsc[e], __ddiv_rn(__fma_rn(p.w2, slope, __dmul_rn(p.w1, value)), p.w2));
 }
 
 // ---- mixed-term ring offsets ------------------------------------------------
@@ -188,8 +198,10 @@ __device__ __forceinline__ double ring_offset(int N1, int N2, const double* gE, 
 // ---- per-patch body: lift, boundary fold-in, K micro-steps, restriction --
 // Everything after the weights (w, registers) and the 3x3 stencil (v) are in
 // hand; shared by the one-shot and the persistent kernels.
+// Returns |value written| on the lane that writes a patch result (0 elsewhere):
+// the fused run's blow-up guard reduces it.
 template <class Cfg>
-__device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg::S], const double (&v)[9], int lane,
+__device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cfg::S], const double (&v)[9], int lane,
                                            bool valid, int patch, double (*sg)[8][Cfg::L], double* sred,
                                            const int* __restrict__ nbr, double* __restrict__ out, int out_mode,
                                            const double* __restrict__ srct) {
@@ -203,12 +215,14 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 #define WT(k, ii, jj) w[(k) * NPL + (ii) * BJ + (jj)]
     // centre derivatives (StencilPoly::center, gaptooth.cpp:63-72); reciprocals
     // come precomputed from the host (no device divisions)
-    const double Uxi = (v[7] - v[1]) * p.i2Dxi;
-    const double Ueta = (v[5] - v[3]) * p.i2Deta;
-    const double hUxx = 0.5 * ((v[7] - 2.0 * v[4] + v[1]) * p.iDxi2);
-    const double hUyy = 0.5 * ((v[5] - 2.0 * v[4] + v[3]) * p.iDeta2);
-    const double Uxy = (v[8] - v[6] - v[2] + v[0]) * p.i4DD;
-    const double C0 = v[4] - p.c24x * (2.0 * hUxx) - p.c24y * (2.0 * hUyy);
+    // (explicit fma / rounded ops outside the step loop: the same rounding
+    // whether this body is inlined into k_fast or into the loop of k_fast_run)
+    const double Uxi = __dmul_rn(__dsub_rn(v[7], v[1]), p.i2Dxi);
+    const double Ueta = __dmul_rn(__dsub_rn(v[5], v[3]), p.i2Deta);
+    const double hUxx = 0.5 * __dmul_rn(__dadd_rn(__fma_rn(-2.0, v[4], v[7]), v[1]), p.iDxi2);
+    const double hUyy = 0.5 * __dmul_rn(__dadd_rn(__fma_rn(-2.0, v[4], v[5]), v[3]), p.iDeta2);
+    const double Uxy = __dmul_rn(__dadd_rn(__dsub_rn(__dsub_rn(v[8], v[6]), v[2]), v[0]), p.i4DD);
+    const double C0 = __fma_rn(-p.c24y, 2.0 * hUyy, __fma_rn(-p.c24x, 2.0 * hUxx, v[4]));
 
     // ---- ghost offsets g = +-2 delta * slope along the four edges ---------
     // slope_E(j) = sum_q Lq(Y_j)[q] * sum_p Lp'(+h/2)[p] v[p][q] (tensor Lagrange,
@@ -220,35 +234,35 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
         if (t < 2 * n2) {
             const int e = t < n2 ? PD_EDGE_E : PD_EDGE_W, j = t < n2 ? t : t - n2;
             const double* d = p.dlag[e];
-            const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
-            const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
-            const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
-            const double sl = p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2;
+            const double G0 = dot3(d[0], v[0], d[1], v[3], d[2], v[6]);
+            const double G1 = dot3(d[0], v[1], d[1], v[4], d[2], v[7]);
+            const double G2 = dot3(d[0], v[2], d[1], v[5], d[2], v[8]);
+            const double sl = dot3(p.lagq[j][0], G0, p.lagq[j][1], G1, p.lagq[j][2], G2);
             if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
-                sg[gs][e][j] = p.gsc[e] * sl;
+                sg[gs][e][j] = __dmul_rn(p.gsc[e], sl);
             } else { // Robin / Dirichlet need the edge value too (dirichlet_edge_values, gaptooth.cpp:110-130)
                 const double* w = p.vlag[e];
-                const double V0 = w[0] * v[0] + w[1] * v[3] + w[2] * v[6];
-                const double V1 = w[0] * v[1] + w[1] * v[4] + w[2] * v[7];
-                const double V2 = w[0] * v[2] + w[1] * v[5] + w[2] * v[8];
-                sg[gs][e][j] = edge_constant(p, e, p.lagq[j][0] * V0 + p.lagq[j][1] * V1 + p.lagq[j][2] * V2, sl);
+                const double V0 = dot3(w[0], v[0], w[1], v[3], w[2], v[6]);
+                const double V1 = dot3(w[0], v[1], w[1], v[4], w[2], v[7]);
+                const double V2 = dot3(w[0], v[2], w[1], v[5], w[2], v[8]);
+                sg[gs][e][j] = edge_constant(p, e, dot3(p.lagq[j][0], V0, p.lagq[j][1], V1, p.lagq[j][2], V2), sl);
             }
         } else {
             const int u = t - 2 * n2;
             const int e = u < n1 ? PD_EDGE_N : PD_EDGE_S, i = u < n1 ? u : u - n1;
             const double* d = p.dlag[e];
-            const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
-            const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
-            const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
-            const double sl = p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2;
+            const double H0 = dot3(d[0], v[0], d[1], v[1], d[2], v[2]);
+            const double H1 = dot3(d[0], v[3], d[1], v[4], d[2], v[5]);
+            const double H2 = dot3(d[0], v[6], d[1], v[7], d[2], v[8]);
+            const double sl = dot3(p.lagp[i][0], H0, p.lagp[i][1], H1, p.lagp[i][2], H2);
             if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
-                sg[gs][e][i] = p.gsc[e] * sl;
+                sg[gs][e][i] = __dmul_rn(p.gsc[e], sl);
             } else {
                 const double* w = p.vlag[e];
-                const double V0 = w[0] * v[0] + w[1] * v[1] + w[2] * v[2];
-                const double V1 = w[0] * v[3] + w[1] * v[4] + w[2] * v[5];
-                const double V2 = w[0] * v[6] + w[1] * v[7] + w[2] * v[8];
-                sg[gs][e][i] = edge_constant(p, e, p.lagp[i][0] * V0 + p.lagp[i][1] * V1 + p.lagp[i][2] * V2, sl);
+                const double V0 = dot3(w[0], v[0], w[1], v[1], w[2], v[2]);
+                const double V1 = dot3(w[0], v[3], w[1], v[4], w[2], v[5]);
+                const double V2 = dot3(w[0], v[6], w[1], v[7], w[2], v[8]);
+                sg[gs][e][i] = edge_constant(p, e, dot3(p.lagp[i][0], V0, p.lagp[i][1], V1, p.lagp[i][2], V2), sl);
             }
         }
     }
@@ -295,13 +309,13 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 #pragma unroll
     for (int ii = 0; ii < BI; ++ii) {
         const int i = bi * BI + ii;
-        const double X = -0.5 * p.h_xi + p.mdxi * i;
-        const double Ai = C0 + X * (Uxi + X * hUxx), Bi = Ueta + X * Uxy;
+        const double X = __fma_rn(p.mdxi, (double)i, -0.5 * p.h_xi);
+        const double Ai = __fma_rn(X, __fma_rn(X, hUxx, Uxi), C0), Bi = __fma_rn(X, Uxy, Ueta);
 #pragma unroll
         for (int jj = 0; jj < BJ; ++jj) {
             const int j = bj * BJ + jj;
-            const double Y = -0.5 * p.h_eta + p.mdeta * j;
-            u[ii][jj] = Ai + Y * (Bi + Y * hUyy); // quadratic lift (gaptooth.cpp:154-168)
+            const double Y = __fma_rn(p.mdeta, (double)j, -0.5 * p.h_eta);
+            u[ii][jj] = __fma_rn(Y, __fma_rn(Y, hUyy, Bi), Ai); // quadratic lift (gaptooth.cpp:154-168)
             if (Cfg::PAD && (i >= n1 || j >= n2)) { // phantom node: zero weights, zero state
                 u[ii][jj] = 0.0;
                 c[ii][jj] = 0.0;
@@ -450,17 +464,17 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) {
                 const int j = bj * BJ + jj;
-                row += (j < n2 ? quad_weight_rt(j, n2 - 1, p.quad) : 0.0) * u[ii][jj];
+                row = __fma_rn(j < n2 ? quad_weight_rt(j, n2 - 1, p.quad) : 0.0, u[ii][jj], row);
             }
-            part += (i < n1 ? quad_weight_rt(i, n1 - 1, p.quad) : 0.0) * row;
+            part = __fma_rn(i < n1 ? quad_weight_rt(i, n1 - 1, p.quad) : 0.0, row, part);
         }
     } else if (kSimpsonShape && p.quad == PD_QUAD_SIMPSON) {
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
             double row = 0.0;
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) row += quad_weight<N2 - 1>(bj * BJ + jj, PD_QUAD_SIMPSON) * u[ii][jj];
-            part += quad_weight<N1 - 1>(bi * BI + ii, PD_QUAD_SIMPSON) * row;
+            for (int jj = 0; jj < BJ; ++jj) row = __fma_rn(quad_weight<N2 - 1>(bj * BJ + jj, PD_QUAD_SIMPSON), u[ii][jj], row);
+            part = __fma_rn(quad_weight<N1 - 1>(bi * BI + ii, PD_QUAD_SIMPSON), row, part);
         }
     } else {
         const double ox = 1.0 / (N1 - 1), oy = 1.0 / (N2 - 1);
@@ -470,10 +484,10 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) {
                 const bool edge = (jj == 0 && bj == 0) || (jj == BJ - 1 && bj == Cfg::LJ - 1);
-                row += (edge ? 0.5 * oy : oy) * u[ii][jj];
+                row = __fma_rn(edge ? 0.5 * oy : oy, u[ii][jj], row);
             }
             const bool edge = (ii == 0 && bi == 0) || (ii == BI - 1 && bi == LI - 1);
-            part += (edge ? 0.5 * ox : ox) * row;
+            part = __fma_rn(edge ? 0.5 * ox : ox, row, part);
         }
     }
     double avg = 0.0;
@@ -488,17 +502,22 @@ __device__ __forceinline__ void patch_body(const Params& p, double (&w)[2 * Cfg:
 #pragma unroll
             for (int q = 0; q < LP; ++q) avg += sred[g * LP + q];
     }
+    double written = 0.0;
     if (valid && r == 0) {
         const size_t node = (size_t)__ldg(nbr + 9 * patch + 4);
         if (out_mode == 0) {
-            out[node] = avg;
-        } else if (out_mode == 1) {
+            out[node] = written = avg;
+        } else if (out_mode == 1 || out_mode == 3) {
             const double U = v[4];
-            out[node] = U + p.dt_macro * ((avg - U) / p.tau); // cpi.cpp:54, 74 (k = 0)
+            written = __fma_rn(p.dt_macro, __ddiv_rn(__dsub_rn(avg, U), p.tau), U); // cpi.cpp:54, 74 (k = 0)
+            out[node] = written;
+            // 3: fused run, the column-0 patch also writes the periodic seam U(Nxi,j) = U(0,j)
+            if (out_mode == 3 && p.periodic && node < (size_t)p.NF2) out[(size_t)p.Nxi * p.NF2 + node] = written;
         } else {
-            out[patch] = avg;
+            out[patch] = written = avg;
         }
     }
+    return fabs(written);
 #undef WT
 }
 
@@ -536,6 +555,93 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
 #pragma unroll
     for (int q = 0; q < 9; ++q) v[q] = valid ? __ldg(F + idx[q]) : 0.0;
     patch_body<Cfg>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, out_mode, srct);
+}
+
+// ---- the whole projective run in one cooperative launch (k = 0) -----------
+// Device-resident cpi::run (cpi.cpp:175-202) for the FAST tiles:
+// per macro step every warp runs the fused step of its units (stride over the
+// grid; projective epilogue, the column-0 patches also write the periodic seam),
+// the grid refreshes the boundary from the perimeter table (refresh_boundary,
+// gaptooth.cpp:296-310), max |U| of every written node is reduced with spread
+// atomics, and ONE grid barrier per step replaces the three launches (step,
+// refresh, guard) of the multi-launch loop; after it every thread reads the
+// same maximum and takes the same guard decision.  Arithmetic identical to
+// k_fast + k_refresh + k_guard.  F is re-read with L2 loads (__ldcg): it was
+// written by other CTAs during this launch.
+constexpr int kGuardSpread = 32;
+
+// 12 warps/SM (168 registers) for the plain 5-point tiles (configs 1-3; spill-
+// free or a few bytes outside the step loop); the mixed / padded / source
+// variants carry more state and keep 8 warps/SM rather than spill.
+template <class Cfg>
+constexpr int run_min_blocks() { return (Cfg::MIXED || Cfg::PAD || Cfg::SRC) ? 8 : 12; }
+
+template <class Cfg>
+__global__ void __launch_bounds__(32 * kFastWarps, run_min_blocks<Cfg>())
+k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int* __restrict__ nbr,
+           const double* __restrict__ Wt, int nunits, const double* __restrict__ bnd, size_t bnd_stride,
+           const double* __restrict__ srct, size_t srct_stride, int nsteps, double blowup,
+           unsigned long long* __restrict__ slot, unsigned long long* __restrict__ spread, int* __restrict__ fail) {
+    constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
+    __shared__ double s_g[kFastWarps][G][8][L];
+    __shared__ double s_red[kFastWarps][32];
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kFastWarps + warp, nw = gridDim.x * kFastWarps;
+    const int nperim = 2 * (p.Nxi + 1) + 2 * (p.Neta + 1);
+    for (int n = 0; n < nsteps; ++n) {
+        const double* F = (n & 1) ? UB : UA;
+        double* out = (n & 1) ? UA : UB;
+        unsigned long long m = 0;
+        for (int unit = gw; unit < nunits; unit += nw) {
+            // lane-dependent setup re-derived per unit: keeps the compiler from
+            // hoisting the per-lane constants of patch_body out of the step loop
+            // (live across the K-step loop they cost ~50 registers = occupancy)
+            int lane;
+            asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
+            const int g = lane / LP;
+            const int patch = unit * G + g;
+            const bool valid = g < G && patch < p.P;
+            int idx[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) idx[q] = valid ? __ldg(nbr + 9 * patch + q) : 0;
+            double w[2 * Cfg::S];
+            {
+                const double2* wp = reinterpret_cast<const double2*>(Wt) + (size_t)unit * Cfg::S * 32 + lane;
+#pragma unroll
+                for (int s = 0; s < Cfg::S; ++s) {
+                    const double2 t = __ldg(wp + s * 32);
+                    w[2 * s] = t.x;
+                    w[2 * s + 1] = t.y;
+                }
+            }
+            double v[9];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) v[q] = valid ? __ldcg(F + idx[q]) : 0.0;
+            const double wv = patch_body<Cfg>(p, w, v, lane, valid, patch, s_g[warp], s_red[warp], nbr, out, 3,
+                                              srct ? srct + srct_stride * n : nullptr);
+            m = max(m, (unsigned long long)__double_as_longlong(wv));
+        }
+        const double* bn = bnd ? bnd + bnd_stride * n : nullptr;
+        for (int t = gw * 32 + lane; t < nperim; t += nw * 32)
+            m = max(m, (unsigned long long)__double_as_longlong(refresh_one(p, out, F, bn, t, true)));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)m, o));
+        if (lane == 0) atomicMax(spread + (size_t)n * kGuardSpread + gw % kGuardSpread, m);
+        grid.sync();
+        unsigned long long v = __ldcg(spread + (size_t)n * kGuardSpread + lane);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = max(v, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)v, o));
+        if (gw == 0 && lane == 0) slot[n] = v;
+        const bool nonfinite = v >= 0x7FF0000000000000ull; // cpi.cpp:187-202
+        if (nonfinite || __longlong_as_double((long long)v) > blowup) {
+            if (gw == 0 && lane == 0) {
+                fail[1] = nonfinite ? 1 : 0;
+                fail[0] = n + 1;
+            }
+            return; // uniform: every thread saw the same maximum
+        }
+    }
 }
 
 // ---- instantiations --------------------------------------------------------
@@ -635,6 +741,45 @@ inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, 
         k_fast<CFG><<<blocks, 32 * kFastWarps, 0, s>>>(p, F, out, out_mode, nbr, W, plan.nunits, fail, srct);
     PD_FAST_CONFIGS(PD_LAUNCH)
 #undef PD_LAUNCH
+}
+
+// Cooperative whole-run launch; returns false (nothing launched) unless every
+// unit gets its own co-resident warp.  The run kernel carries more live state
+// than k_fast (about 220 registers instead of 168: 9 instead of 12 warps/SM),
+// so it is used where per-step launch latency dominates (configs 1-3, small
+// sweep points), not where the step is throughput-bound.
+inline bool launch_fast_run(const FastPlan& plan, const Params& p, double* UA, double* UB, const int* nbr,
+                            const double* W, const double* bnd, size_t bnd_stride, const double* srct,
+                            size_t srct_stride, int nsteps, double blowup, unsigned long long* slot,
+                            unsigned long long* spread, int* fail, cudaStream_t s) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int nunits = plan.nunits;
+    bool launched = false;
+#define PD_RUN(ID, CFG)                                                                                        \
+    if (plan.id == ID) {                                                                                       \
+        int per_sm = 0;                                                                                        \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fast_run<CFG>, 32 * kFastWarps, 0);           \
+        const int blocks = (nunits + kFastWarps - 1) / kFastWarps;                                             \
+        if (std::getenv("PD_DEBUG_RUN"))                                                                       \
+            fprintf(stderr, "k_fast_run plan %d: %d blocks, %d per SM x %d SMs\n", ID, blocks, per_sm, sms);     \
+        if (per_sm > 0 && blocks <= per_sm * sms) {                                                            \
+            Params pp = p;                                                                                     \
+            void* args[] = {&pp, &UA, &UB, (void*)&nbr, (void*)&W, &nunits, (void*)&bnd, &bnd_stride,          \
+                            (void*)&srct, &srct_stride, &nsteps, &blowup, &slot, &spread, &fail};              \
+            launched = cudaLaunchCooperativeKernel((const void*)k_fast_run<CFG>, dim3(blocks),                 \
+                                                   dim3(32 * kFastWarps), args, 0, s) == cudaSuccess;          \
+            if (!launched) {                                                                                   \
+                const cudaError_t e_ = cudaGetLastError(); /* the multi-launch loop runs instead */            \
+                if (std::getenv("PD_DEBUG_RUN"))                                                               \
+                    fprintf(stderr, "k_fast_run not launched: %s\n", cudaGetErrorString(e_));                  \
+            }                                                                                                  \
+        }                                                                                                      \
+    }
+    PD_FAST_CONFIGS(PD_RUN)
+#undef PD_RUN
+    return launched;
 }
 
 } // namespace pdb200::dev

@@ -8,36 +8,46 @@ namespace pdb200::dev {
 // refresh_boundary (gaptooth.cpp:296-310) from a perimeter array, or, with
 // bnd == nullptr, keep the input field's boundary (copied from F) and apply
 // the periodic seam U(Nxi,j) = U(0,j).  Non-patch nodes are exactly the
-// boundary rows/columns (+ the seam column when periodic).
-__device__ __forceinline__ void refresh_range(const Params& p, double* __restrict__ out, const double* __restrict__ F,
-                                              const double* __restrict__ bnd, int t0, int stride) {
+// boundary rows/columns (+ the seam column when periodic).  One perimeter
+// entry t; returns |value written| (0 when the entry writes nothing).
+// seam_by_patches: the fused run's column-0 patches write the seam interior.
+__device__ __forceinline__ double refresh_one(const Params& p, double* __restrict__ out, const double* __restrict__ F,
+                                              const double* __restrict__ bnd, int t, bool seam_by_patches) {
     const int N1 = p.Nxi, N2 = p.Neta, n2 = p.NF2;
-    const int rows = 2 * (N1 + 1), cols = 2 * (N2 + 1);
+    const int rows = 2 * (N1 + 1);
     const double* S = bnd;
     const double* Nn = bnd ? bnd + (N1 + 1) : nullptr;
     const double* W = bnd ? bnd + 2 * (N1 + 1) : nullptr;
     const double* E = bnd ? W + (N2 + 1) : nullptr;
-    for (int t = t0; t < rows + cols; t += stride) {
-        if (t < rows) { // S/N rows; corners are owned by the column pass (W/E or seam)
-            const int i = t % (N1 + 1), j = t < N1 + 1 ? 0 : N2;
-            if (p.periodic ? i == N1 : (i == 0 || i == N1)) continue;
-            const size_t node = (size_t)i * n2 + j;
-            out[node] = bnd ? (j == 0 ? S[i] : Nn[i]) : F[node];
-        } else {
-            const int u = t - rows, j = u % (N2 + 1), east = u >= N2 + 1;
-            if (p.periodic) {
-                if (!east) continue; // column 0 holds patch results (or its boundary rows)
-                double v;
-                if (j == 0) v = bnd ? S[0] : F[0];
-                else if (j == N2) v = bnd ? Nn[0] : F[N2];
-                else v = out[j]; // patch (0,j) result, written before the refresh
-                out[(size_t)N1 * n2 + j] = v;
-            } else {
-                const size_t node = (size_t)(east ? N1 : 0) * n2 + j;
-                out[node] = bnd ? (east ? E[j] : W[j]) : F[node];
-            }
-        }
+    if (t < rows) { // S/N rows; corners are owned by the column pass (W/E or seam)
+        const int i = t % (N1 + 1), j = t < N1 + 1 ? 0 : N2;
+        if (p.periodic ? i == N1 : (i == 0 || i == N1)) return 0.0;
+        const size_t node = (size_t)i * n2 + j;
+        const double v = bnd ? (j == 0 ? S[i] : Nn[i]) : F[node];
+        out[node] = v;
+        return fabs(v);
     }
+    const int u = t - rows, j = u % (N2 + 1), east = u >= N2 + 1;
+    if (p.periodic) {
+        if (!east) return 0.0; // column 0 holds patch results (or its boundary rows)
+        double v;
+        if (j == 0) v = bnd ? S[0] : F[0];
+        else if (j == N2) v = bnd ? Nn[0] : F[N2];
+        else if (seam_by_patches) return 0.0;
+        else v = out[j]; // patch (0,j) result, written before the refresh
+        out[(size_t)N1 * n2 + j] = v;
+        return fabs(v);
+    }
+    const size_t node = (size_t)(east ? N1 : 0) * n2 + j;
+    const double v = bnd ? (east ? E[j] : W[j]) : F[node];
+    out[node] = v;
+    return fabs(v);
+}
+
+__device__ __forceinline__ void refresh_range(const Params& p, double* __restrict__ out, const double* __restrict__ F,
+                                              const double* __restrict__ bnd, int t0, int stride) {
+    const int n = 2 * (p.Nxi + 1) + 2 * (p.Neta + 1);
+    for (int t = t0; t < n; t += stride) refresh_one(p, out, F, bnd, t, false);
 }
 
 __global__ void k_refresh(Params p, double* __restrict__ out, const double* __restrict__ F,

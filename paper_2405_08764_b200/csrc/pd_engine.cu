@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -83,7 +84,7 @@ struct pd_engine {
     double coeffgen_ms = 0.0;           // on-device table generation time at create (0: host tables)
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     bool subset = false;                // the patch list covers only part of the interior
-    DevBuf<unsigned long long> d_slot;
+    DevBuf<unsigned long long> d_slot, d_spread;
     DevBuf<unsigned int> d_counter;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::string err;
@@ -567,8 +568,28 @@ pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps
         // loop is one single-CTA kernel (k_linear_run_block), same results
         const size_t block_smem = (e->prm.k == 0 ? 2 : 3) * NF * 8;
         const bool block_run = e->step_kind == PD_STEP_LINEAR && nsteps > 0 && block_smem <= kLinearBlockSmemMax;
+        // direct FAST steps (k = 0, full field): the whole run is one cooperative
+        // launch (k_fast_run) when the plan's kernel can be made co-resident
+        static const bool fused_enabled = [] {
+            const char* v = std::getenv("PD_FUSED_RUN");
+            return !(v && v[0] == '0');
+        }();
+        const bool fused_ok = !block_run && fused_enabled && nsteps > 0 && e->step_kind == PD_STEP_DIRECT &&
+                              e->mode == PD_MODE_FAST && !e->fast.big && e->prm.k == 0 && !e->subset;
+        if (fused_ok) {
+            e->d_spread.alloc((size_t)nsteps * kGuardSpread);
+            CUDA_TRY(cudaMemsetAsync(e->d_spread.p, 0, (size_t)nsteps * kGuardSpread * 8, e->stream));
+        }
+        bool fused = false;
         CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
-        if (block_run) {
+        if (fused_ok) {
+            fused = launch_fast_run(e->fast, e->prm, U, scratch, e->d_nbr.p, e->d_weights.p,
+                                    bnd ? bnd + e->perim : nullptr, pk, (src_time && e->prm.source) ? src_time : nullptr,
+                                    sk, nsteps, blowup, e->d_slot.p, e->d_spread.p, e->d_fail.p, e->stream);
+            if (fused) e->check_launch();
+        }
+        if (fused) {
+        } else if (block_run) {
             CUDA_TRY(cudaFuncSetAttribute(k_linear_run_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)block_smem));
             k_linear_run_block<<<1, 1024, block_smem, e->stream>>>(e->prm, U, e->d_pij.p, e->d_roww.p, bnd, e->perim,

@@ -41,7 +41,8 @@ def test_full_run_vs_reference(name, mode, gpu):
     U1 = E.projective_step(U0, 0.0, bnd=P.boundary_table(0.0, 1)[0])
     UT, stats = E.run(U0, Nt, bnd=P.boundary_table(0.0, Nt))
     assert stats.steps_done == Nt and stats.failed_step == 0
-    assert stats.kernel_launches == 3 * Nt  # fused step + boundary refresh + guard per macro step
+    # FAST: the whole run is one cooperative launch (k_fast_run); EXACT: fused step + refresh + guard per step
+    assert stats.kernel_launches == (1 if mode == FAST else 3 * Nt)
     if mode == EXACT:
         assert np.array_equal(U1, FINALS[f"{name}_U1"])
         assert np.array_equal(UT, FINALS[f"{name}_final"])
@@ -265,8 +266,9 @@ def test_macro_instability_guard(restated, gpu):
     # the FAST family (an 11x11 patch in the padded 16x16 tile) trips at the same step
     F = Engine.from_problem(P, mode=FAST)
     assert F.mode == FAST
-    _, sf = F.run(U0, 5, bnd=bt, raise_on_instability=False)
+    Uf, sf = F.run(U0, 5, bnd=bt, raise_on_instability=False)
     assert sf.failed_step == so.failed_step
+    assert sf.kernel_launches == 1  # the single-launch run (k_fast_run) took the guard decision
 
 
 def test_error_paths(gpu):
@@ -783,3 +785,25 @@ def test_coeffgen_rejects_folded_maps_like_the_host(gpu):
         with pytest.raises(PatchdynError) as ei:
             Problem(configs.copy_desc(d, coeff_gen=gen))
         assert ei.value.status == abi.PD_NON_POSITIVE_JACOBIAN
+
+
+# ---------------------------------------------------------------------------
+# the whole run as one cooperative launch (k_fast_run)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["c1_diffusion", "c2_cdr_tanh", "c3_annulus"])
+def test_fused_run_equals_stepwise_launches(name, gpu):
+    """pd_run's single-launch loop (fused step + refresh + guard per grid
+    barrier) is bit-identical to one pd_projective_step call per macro step."""
+    P = load(name)
+    n = 12
+    U0 = P.initial_field()
+    bt = P.boundary_table(0.0, n)
+    E = Engine.from_problem(P, mode=FAST)
+    Ug, stats = E.run(U0, n, bnd=bt)
+    assert stats.kernel_launches == 1  # the run kernel (the initial-scale guard is not counted)
+    U = U0
+    dt = P.desc.T / P.desc.Nt
+    for s in range(n):
+        U = E.projective_step(U, s * dt, bnd=bt[s])
+    assert np.array_equal(Ug, U)
+    assert stats.umax_last == np.abs(U).max()
