@@ -403,8 +403,10 @@ def main():
                        "stencil": "9-point (mixed term)" if mixed else "5-point",
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                        "kernel_family": "fast" if eng.mode == abi.PD_MODE_FAST else "exact",
-                       "l2": f"inputs larger than L2: {eng.device_bytes / 1e9:.2f} GB of device tables streamed "
-                             f"per macro step (> 126 MB L2)"},
+                       "l2": (f"inputs larger than L2: {eng.device_bytes / 1e9:.2f} GB of device tables streamed "
+                              f"per macro step (> 126 MB L2)") if eng.device_bytes > 126e6 else
+                             (f"L2-resident: {eng.device_bytes / 1e6:.1f} MB of device tables (< 126 MB L2), "
+                              f"no flush between steps (the reference re-reads the same tables every step)")},
             "roofline": roof, "e2e": e2e, "gpu_launches": int(stats.kernel_launches), "clocks": clk}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ed, U0, P, N, K)

@@ -569,6 +569,9 @@ k_fast(Params p, const double* __restrict__ F, double* __restrict__ out, int out
 // k_fast + k_refresh + k_guard.  F is re-read with L2 loads (__ldcg): it was
 // written by other CTAs during this launch.
 constexpr int kGuardSpread = 32;
+// Four warps per CTA: the grid barrier's arrival count is per CTA (one atomic
+// per CTA), so fewer, larger CTAs make it cheaper; 3 CTAs/SM = 12 warps.
+constexpr int kRunWarps = 4;
 
 // 12 warps/SM (168 registers) for the plain 5-point tiles (configs 1-3; spill-
 // free or a few bytes outside the step loop); the mixed / padded / source
@@ -577,17 +580,17 @@ template <class Cfg>
 constexpr int run_min_blocks() { return (Cfg::MIXED || Cfg::PAD || Cfg::SRC) ? 8 : 12; }
 
 template <class Cfg>
-__global__ void __launch_bounds__(32 * kFastWarps, run_min_blocks<Cfg>())
+__global__ void __launch_bounds__(32 * kRunWarps, run_min_blocks<Cfg>() / kRunWarps)
 k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int* __restrict__ nbr,
            const double* __restrict__ Wt, int nunits, const double* __restrict__ bnd, size_t bnd_stride,
            const double* __restrict__ srct, size_t srct_stride, int nsteps, double blowup,
            unsigned long long* __restrict__ slot, unsigned long long* __restrict__ spread, int* __restrict__ fail) {
     constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
-    __shared__ double s_g[kFastWarps][G][8][L];
-    __shared__ double s_red[kFastWarps][32];
+    __shared__ double s_g[kRunWarps][G][8][L];
+    __shared__ double s_red[kRunWarps][32];
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int gw = blockIdx.x * kFastWarps + warp, nw = gridDim.x * kFastWarps;
+    const int gw = blockIdx.x * kRunWarps + warp, nw = gridDim.x * kRunWarps;
     const int nperim = 2 * (p.Nxi + 1) + 2 * (p.Neta + 1);
     for (int n = 0; n < nsteps; ++n) {
         const double* F = (n & 1) ? UB : UA;
@@ -760,8 +763,8 @@ inline bool launch_fast_run(const FastPlan& plan, const Params& p, double* UA, d
 #define PD_RUN(ID, CFG)                                                                                        \
     if (plan.id == ID) {                                                                                       \
         int per_sm = 0;                                                                                        \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fast_run<CFG>, 32 * kFastWarps, 0);           \
-        const int blocks = (nunits + kFastWarps - 1) / kFastWarps;                                             \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fast_run<CFG>, 32 * kRunWarps, 0);            \
+        const int blocks = (nunits + kRunWarps - 1) / kRunWarps;                                               \
         if (std::getenv("PD_DEBUG_RUN"))                                                                       \
             fprintf(stderr, "k_fast_run plan %d: %d blocks, %d per SM x %d SMs\n", ID, blocks, per_sm, sms);     \
         if (per_sm > 0 && blocks <= per_sm * sms) {                                                            \
@@ -769,7 +772,7 @@ inline bool launch_fast_run(const FastPlan& plan, const Params& p, double* UA, d
             void* args[] = {&pp, &UA, &UB, (void*)&nbr, (void*)&W, &nunits, (void*)&bnd, &bnd_stride,          \
                             (void*)&srct, &srct_stride, &nsteps, &blowup, &slot, &spread, &fail};              \
             launched = cudaLaunchCooperativeKernel((const void*)k_fast_run<CFG>, dim3(blocks),                 \
-                                                   dim3(32 * kFastWarps), args, 0, s) == cudaSuccess;          \
+                                                   dim3(32 * kRunWarps), args, 0, s) == cudaSuccess;           \
             if (!launched) {                                                                                   \
                 const cudaError_t e_ = cudaGetLastError(); /* the multi-launch loop runs instead */            \
                 if (std::getenv("PD_DEBUG_RUN"))                                                               \
