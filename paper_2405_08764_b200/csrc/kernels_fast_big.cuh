@@ -316,19 +316,23 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     for (int step = 0; step < p.nt; ++step) {
         const int po = (step & 1) * LJ * ROW;
         double* mine = mine0 + po;
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii) mine[ii] = u[ii][0]; // local row jj = 0
+        static_assert(BI == 2, "the row hand-off moves one 16-byte pair per lane");
+        // local row jj = 0 as one 128-bit store / load per lane (bank-conflict free;
+        // two 64-bit accesses at a 16-byte lane stride conflicted 2-way)
+        *reinterpret_cast<double2*>(mine) = make_double2(u[0][0], u[1][0]);
         __syncthreads();
-        const double* rx = rx0 + po;
+        const double2 pr = *reinterpret_cast<const double2*>(rx0 + po);
         double hS[BI], hN[BI], eS[BI], eN[BI];
+        hS[0] = pr.x;
+        hS[1] = pr.y;
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii) {
-            hS[ii] = rx[ii];
-            hN[ii] = __shfl_xor_sync(0xffffffffu, u[ii][BJ - 1], 16); // partner half of this warp
-        }
+        for (int ii = 0; ii < BI; ++ii) hN[ii] = __shfl_xor_sync(0xffffffffu, u[ii][BJ - 1], 16); // partner half
         if constexpr (MIXED) {
-#pragma unroll
-            for (int ii = 0; ii < BI; ++ii) eS[ii] = rx[ii + 1] - rx[ii - 1];
+            // columns i0-1 and i0+2 of the partner row are the neighbouring lanes' pairs
+            // (at a half-warp end the value is finite and its weight zero: patch edge)
+            const double lft = __shfl_up_sync(0xffffffffu, pr.y, 1), rgt = __shfl_down_sync(0xffffffffu, pr.x, 1);
+            eS[0] = pr.y - lft;
+            eS[1] = rgt - pr.x;
         }
         double cE[BJ], cW[BJ];
 #pragma unroll
