@@ -263,12 +263,209 @@ __device__ inline void implicit_sweep_x(const Params& p, const double* rhsf, dou
     }
 }
 
+// ---- static line factors ----------------------------------------------------
+// Every value implicit_sweep computes for its line matrices depends only on the
+// coefficients, the patch conditions (cIn / cEdge / pinned, never the ghost
+// offsets b) and the upwind choice: the reference rebuilds and re-eliminates
+// them every micro step.  k_adi_factor replays that construction and the
+// matrix-only half of the elimination once per engine; the fused step then
+// replays only the right-hand-side arithmetic with the stored values - the same
+// IEEE operations on the same operands, so results stay bit-identical.
+// Table: [set][dir (0 = xi lines, 1 = eta lines)][line < L][k < L][kAdiFac].
+constexpr int kAdiFac = 8; // tri: lo, m, wk, adj | banded: f1, f2, B0, B1, B2, adj
+constexpr int kAdiAdj = 7; // slot of the ghost-offset coefficient (k = 0: sub, k = n-1: sup)
+
+__host__ __device__ inline size_t adi_factor_doubles(const Params& p) { return (size_t)2 * p.L * p.L * kAdiFac; }
+
+// row k of line `line` after the ghost fold-in (implicit_sweep, microsim.cpp:433-470)
+struct AdiRow {
+    double diag, sub, sup, lo2, hi2, adj;
+    int pinned;
+};
+__device__ inline AdiRow adi_row(const Params& p, const EdgeSh* E, const double* coef, bool xi_dir, int line,
+                                 int k) {
+    const int n2 = p.n2, N = p.N;
+    const double half = XMUL(0.5, p.mdt);
+    const int n = xi_dir ? p.nx + 1 : p.ny + 1;
+    const double dd = xi_dir ? p.mdxi : p.mdeta;
+    const int elo = xi_dir ? PD_EDGE_W : PD_EDGE_S, ehi = xi_dir ? PD_EDGE_E : PD_EDGE_N;
+    AdiRow r{};
+    if ((k == 0 && E[elo].pinned) || (k == n - 1 && E[ehi].pinned)) {
+        r.pinned = 1;
+        r.diag = 1.0; // di = 1, lo = up = 0 (the banded matrix: diagonal 1)
+        return r;
+    }
+    const int i = xi_dir ? k : line, j = xi_dir ? line : k, q = i * n2 + j;
+    const double A = xi_dir ? coef[PD_COEF_A * N + q] : coef[PD_COEF_C * N + q];
+    const double V = xi_dir ? coef[PD_COEF_VX * N + q] : coef[PD_COEF_VY * N + q];
+    const double sc = XDIV(XMUL(half, A), XMUL(dd, dd));
+    double diag = XADD(XADD(1.0, XMUL(2.0, sc)), XMUL(XMUL(half, 0.5), coef[PD_COEF_W * N + q]));
+    double sub = -sc, sup = -sc, lo2 = 0.0, hi2 = 0.0;
+    const UpwindW sw = upwind_fb_x(p.upwind_order, p.upwind_r, dd, V >= 0 ? 1 : -1, k, n - 1);
+    for (int m = 0; m < sw.n; ++m) {
+        const double wgt = XMUL(XMUL(half, V), sw.w[m]);
+        switch (sw.off[m]) {
+            case 0: diag = XADD(diag, wgt); break;
+            case -1: sub = XADD(sub, wgt); break;
+            case 1: sup = XADD(sup, wgt); break;
+            case -2: lo2 = XADD(lo2, wgt); break;
+            default: hi2 = XADD(hi2, wgt); break;
+        }
+    }
+    double adj = 0.0;
+    if (k == 0) {
+        adj = sub;
+        diag = XADD(diag, XMUL(sub, E[elo].cEdge));
+        sup = XADD(sup, XMUL(sub, E[elo].cIn));
+        sub = 0.0;
+    } else if (k == n - 1) {
+        adj = sup;
+        diag = XADD(diag, XMUL(sup, E[ehi].cEdge));
+        sub = XADD(sub, XMUL(sup, E[ehi].cIn));
+        sup = 0.0;
+    }
+    r.diag = diag;
+    r.sub = sub;
+    r.sup = sup;
+    r.lo2 = lo2;
+    r.hi2 = hi2;
+    r.adj = adj;
+    return r;
+}
+
+// One thread per (set, direction, line): rows, then the Thomas factors
+// (linalg.cpp:8-25: m_k, w_k) or the pivot-free band elimination (linalg.cpp:43-61).
+__global__ void k_adi_factor(Params p, const double* __restrict__ coeffs, int nsets, double* __restrict__ fac) {
+    const int kind = p.bc_type == PD_BC_DIRICHLET ? PD_EDGE_DIRICHLET
+                   : p.bc_type == PD_BC_ROBIN     ? PD_EDGE_ROBIN
+                                                  : PD_EDGE_NEUMANN;
+    EdgeSh E[4];
+    make_ghost_x(E[PD_EDGE_E], kind, p.w1, p.w2, p.mdxi, +1.0, 0, nullptr, nullptr, nullptr);
+    make_ghost_x(E[PD_EDGE_W], kind, p.w1, p.w2, p.mdxi, -1.0, 0, nullptr, nullptr, nullptr);
+    make_ghost_x(E[PD_EDGE_N], kind, p.w1, p.w2, p.mdeta, +1.0, 0, nullptr, nullptr, nullptr);
+    make_ghost_x(E[PD_EDGE_S], kind, p.w1, p.w2, p.mdeta, -1.0, 0, nullptr, nullptr, nullptr);
+    const int L = p.L;
+    const int total = nsets * 2 * L;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int set = t / (2 * L), dir = (t / L) % 2, line = t % L;
+        const bool xi_dir = dir == 0;
+        const int nline = xi_dir ? p.ny : p.nx, n = xi_dir ? p.nx + 1 : p.ny + 1;
+        if (line > nline) continue;
+        const double* coef = coeffs + (size_t)set * PD_NCOEF * p.N;
+        double* F = fac + (((size_t)set * 2 + dir) * L + line) * L * kAdiFac;
+        if (p.upwind_order == PD_UPWIND_TWO) {
+            double wprev = 0.0;
+            for (int k = 0; k < n; ++k) {
+                const AdiRow r = adi_row(p, E, coef, xi_dir, line, k);
+                const double lo = r.pinned ? 0.0 : r.sub, up = r.pinned ? 0.0 : r.sup;
+                const double m = k == 0 ? r.diag : XSUB(r.diag, XMUL(lo, wprev));
+                wprev = XDIV(up, m);
+                F[k * kAdiFac + 0] = lo;
+                F[k * kAdiFac + 1] = m;
+                F[k * kAdiFac + 2] = wprev;
+                F[k * kAdiFac + kAdiAdj] = r.adj;
+            }
+        } else {
+            // band rows B(r, -2..2) held in the table's slots 2..6 during the elimination
+            for (int k = 0; k < n; ++k) {
+                const AdiRow r = adi_row(p, E, coef, xi_dir, line, k);
+                double* b = F + k * kAdiFac;
+                b[0] = b[1] = 0.0;
+                b[2] = r.pinned ? 0.0 : (r.lo2 != 0.0 ? r.lo2 : 0.0);
+                b[3] = (r.pinned || k == 0) ? 0.0 : r.sub;
+                b[4] = r.diag;
+                b[5] = (r.pinned || k == n - 1) ? 0.0 : r.sup;
+                b[6] = r.pinned ? 0.0 : (r.hi2 != 0.0 ? r.hi2 : 0.0);
+                b[kAdiAdj] = r.adj;
+            }
+            auto B = [&](int row, int off) -> double& { return F[row * kAdiFac + 4 + off]; };
+            for (int k = 0; k < n - 1; ++k) {
+                const double piv = B(k, 0);
+                const int last = min(k + 2, n - 1);
+                for (int r = k + 1; r <= last; ++r) {
+                    const double f = XDIV(B(r, k - r), piv);
+                    F[k * kAdiFac + (r == k + 1 ? 0 : 1)] = f; // multiplier slots f1, f2
+                    if (f == 0.0) continue;
+                    for (int c = k + 1; c <= min(k + 2, n - 1); ++c) B(r, c - r) = XSUB(B(r, c - r), XMUL(f, B(k, c - k)));
+                }
+            }
+        }
+    }
+}
+
+// implicit_sweep with the stored line factors (one thread per line): the
+// right-hand side as the reference builds it, then the Thomas / band
+// substitutions with the stored multipliers, pivots and upper band.
+__device__ inline void implicit_sweep_cached(const Params& p, const double* rhsf, double* out, const EdgeSh* E,
+                                             const double* gb, const double* val, const double* slope,
+                                             const double* fac, double* lsc, bool xi_dir) {
+    const int nx = p.nx, ny = p.ny, n2 = p.n2, L = p.L;
+    const int nline = xi_dir ? ny : nx;
+    const int n = xi_dir ? nx + 1 : ny + 1;
+    const int elo = xi_dir ? PD_EDGE_W : PD_EDGE_S, ehi = xi_dir ? PD_EDGE_E : PD_EDGE_N;
+    const int slo = xi_dir ? PD_EDGE_S : PD_EDGE_W, shi = xi_dir ? PD_EDGE_N : PD_EDGE_E;
+    const bool banded = p.upwind_order != PD_UPWIND_TWO;
+    for (int line = threadIdx.x; line <= nline; line += blockDim.x) {
+        auto put = [&](int k, double v) {
+            if (xi_dir) out[k * n2 + line] = v;
+            else out[line * n2 + k] = v;
+        };
+        if ((line == 0 && E[slo].pinned) || (line == nline && E[shi].pinned)) {
+            const int e = line == 0 ? slo : shi;
+            for (int k = 0; k < n; ++k) put(k, pinned_value_x(E[e], val + e * L, slope + e * L, k));
+            continue;
+        }
+        const double* F = fac + ((size_t)(xi_dir ? 0 : 1) * L + line) * L * kAdiFac;
+        double* rhs = lsc + (size_t)line * 6 * L;
+        for (int k = 0; k < n; ++k) {
+            const bool pin_lo = k == 0 && E[elo].pinned, pin_hi = k == n - 1 && E[ehi].pinned;
+            if (pin_lo || pin_hi) {
+                const int e = pin_lo ? elo : ehi;
+                rhs[k] = pinned_value_x(E[e], val + e * L, slope + e * L, line);
+                continue;
+            }
+            const int q = xi_dir ? k * n2 + line : line * n2 + k;
+            double rr = rhsf[q];
+            if (k == 0) rr = XSUB(rr, XMUL(F[kAdiAdj], gb[elo * L + line]));
+            else if (k == n - 1) rr = XSUB(rr, XMUL(F[k * kAdiFac + kAdiAdj], gb[ehi * L + line]));
+            rhs[k] = rr;
+        }
+        if (banded) {
+            for (int k = 0; k < n - 1; ++k) {
+                const int last = min(k + 2, n - 1);
+                for (int r = k + 1; r <= last; ++r) {
+                    const double f = F[k * kAdiFac + (r == k + 1 ? 0 : 1)];
+                    if (f == 0.0) continue;
+                    rhs[r] = XSUB(rhs[r], XMUL(f, rhs[k]));
+                }
+            }
+            for (int r = n - 1; r >= 0; --r) {
+                double sacc = rhs[r];
+                for (int c = r + 1; c <= min(r + 2, n - 1); ++c) sacc = XSUB(sacc, XMUL(F[r * kAdiFac + 4 + (c - r)], rhs[c]));
+                rhs[r] = XDIV(sacc, F[r * kAdiFac + 4]);
+            }
+        } else {
+            double prev = XDIV(rhs[0], F[1]);
+            rhs[0] = prev;
+            for (int k = 1; k < n; ++k) {
+                prev = XDIV(XSUB(rhs[k], XMUL(F[k * kAdiFac + 0], prev)), F[k * kAdiFac + 1]);
+                rhs[k] = prev;
+            }
+            for (int k = n - 1; k-- > 0;) {
+                prev = XSUB(rhs[k], XMUL(F[k * kAdiFac + 2], prev));
+                rhs[k] = prev;
+            }
+        }
+        for (int k = 0; k < n; ++k) put(k, rhs[k]);
+    }
+}
+
 // K Peaceman-Rachford steps on the shared tile (integrate with Scheme::ADI,
 // microsim.cpp:535-548): source at t0 + (step + 1/2) dt, supplied by the host
 // as src_time[step] = time(t_mid)/l.  Returns the buffer holding the result.
 __device__ inline double* micro_loop_adi(const Params& p, PatchSh& s, const EdgeSh* eg, const double* coef,
                                          const double* src_sp, const double* src_time, double* rhsf,
-                                         double* lsc) {
+                                         double* lsc, const double* fac = nullptr) {
     const double half = XMUL(0.5, p.mdt);
     double* u = s.u0;
     double* work = s.u1;
@@ -285,7 +482,8 @@ __device__ inline double* micro_loop_adi(const Params& p, PatchSh& s, const Edge
                               : XADD(f[t], XMUL(half, XADD(cross_term_x(p, f, eg, s.gb, coef, i, j, xi_dir), G)));
             }
             __syncthreads();
-            implicit_sweep_x(p, rhsf, xi_dir ? work : u, eg, s.gb, s.val, s.slope, coef, lsc, xi_dir);
+            if (fac) implicit_sweep_cached(p, rhsf, xi_dir ? work : u, eg, s.gb, s.val, s.slope, fac, lsc, xi_dir);
+            else implicit_sweep_x(p, rhsf, xi_dir ? work : u, eg, s.gb, s.val, s.slope, coef, lsc, xi_dir);
             __syncthreads();
         }
     }

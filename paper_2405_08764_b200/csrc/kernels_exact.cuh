@@ -95,7 +95,7 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
                  const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
                  const double* __restrict__ src_sp, const double* __restrict__ src_time,
                  const int* __restrict__ fail_flag, const double* __restrict__ stencil_in = nullptr,
-                 const int* __restrict__ item_patch = nullptr) {
+                 const int* __restrict__ item_patch = nullptr, const double* __restrict__ adi_fac = nullptr) {
     extern __shared__ double sm[];
     if (fail_flag && *fail_flag) return;
     // item_patch != NULL: evolve_patch of given 3x3 values (stencil_in [items][9])
@@ -135,7 +135,8 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
     double* res;
     if (p.solver == PD_SOLVER_ADI) {
         double* xs = adi_scratch(sm, p);
-        res = micro_loop_adi(p, s, eg, coef, sp, src_time, xs, xs + p.N);
+        res = micro_loop_adi(p, s, eg, coef, sp, src_time, xs, xs + p.N,
+                             adi_fac ? adi_fac + (size_t)set * adi_factor_doubles(p) : nullptr);
     } else {
         res = micro_loop_x(p, s, eg, coef, sp, src_time, p.mixed != 0);
     }

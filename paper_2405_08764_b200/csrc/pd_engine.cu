@@ -81,6 +81,7 @@ struct pd_engine {
     DevBuf<int32_t> d_pij, d_nbr, d_cset, d_kinds, d_fail, d_cset_items;
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
     DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
+    DevBuf<double> d_adi_fac;           // ADI static line factors [sets][2][L][L][kAdiFac] (k_adi_factor)
     double coeffgen_ms = 0.0;           // on-device table generation time at create (0: host tables)
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     bool subset = false;                // the patch list covers only part of the interior
@@ -113,7 +114,8 @@ struct pd_engine {
             launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream, srct);
         } else {
             k_gaptooth_exact<<<prm.P, exact_threads(prm), exact_smem_bytes(prm), stream>>>(
-                prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail);
+                prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail, nullptr, nullptr,
+                d_adi_fac.p);
         }
         check_launch();
     }
@@ -420,6 +422,21 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
         e->d_U.alloc(2 * e->NF);
         e->d_fail.alloc(4);
         e->device_bytes = Ncoef * 8 + e->pij.size() * 4 + e->nbr.size() * 4 + 2 * e->NF * 8;
+        // ADI: the line matrices are static; factor them once (bit-identical replay)
+        static const bool adi_cache = [] {
+            const char* v = std::getenv("PD_ADI_FACTOR_CACHE");
+            return !(v && v[0] == '0');
+        }();
+        if (d.solver == PD_SOLVER_ADI && adi_cache) {
+            const size_t nf = (size_t)d.ncoeff_sets * adi_factor_doubles(p);
+            e->d_adi_fac.alloc(nf);
+            CUDA_TRY(cudaMemsetAsync(e->d_adi_fac.p, 0, nf * 8, e->stream));
+            const int threads = 128, total = d.ncoeff_sets * 2 * p.L;
+            k_adi_factor<<<(total + threads - 1) / threads, threads, 0, e->stream>>>(p, e->d_coeffs.p, d.ncoeff_sets,
+                                                                                       e->d_adi_fac.p);
+            e->check_launch();
+            e->device_bytes += nf * 8;
+        }
         // kernel family
         e->mode = PD_MODE_EXACT;
         if (exact_smem_bytes(p) > 48 * 1024) {
@@ -779,7 +796,7 @@ pd_status pd_evolve_batch(pd_engine* e, int32_t n, const int32_t* patch_index, c
         double* res = e->d_tmp2.p + (size_t)9 * n;
         k_gaptooth_exact<<<n, kExactThreads, exact_smem_bytes(p), e->stream>>>(
             p, nullptr, res, OUT_PATCH, e->d_pij.p, e->d_cset.p, e->d_coeffs.p, nullptr, nullptr, nullptr,
-            e->d_tmp2.p, e->d_cset_items.p);
+            e->d_tmp2.p, e->d_cset_items.p, e->d_adi_fac.p);
         e->check_launch();
         download(out, res, (size_t)n * 8, e->stream);
         CUDA_TRY(cudaStreamSynchronize(e->stream));
