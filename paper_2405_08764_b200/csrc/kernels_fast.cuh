@@ -576,6 +576,24 @@ constexpr int kRunWarps = 4;
 // 12 warps/SM (168 registers) for the plain 5-point tiles (configs 1-3; spill-
 // free or a few bytes outside the step loop); the mixed / padded / source
 // variants carry more state and keep 8 warps/SM rather than spill.
+// blow-up guard (cpi.cpp:187-202) on the spread maxima of one step: max over
+// the warp's 32 slots, recorded in slot[step]; true when the run stops.
+__device__ __forceinline__ bool guard_trips(unsigned long long v, int step, int gw, int lane, double blowup,
+                                            unsigned long long* slot, int* fail) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)v, o));
+    if (gw == 0 && lane == 0) slot[step] = v;
+    const bool nonfinite = v >= 0x7FF0000000000000ull;
+    if (nonfinite || __longlong_as_double((long long)v) > blowup) {
+        if (gw == 0 && lane == 0) {
+            fail[1] = nonfinite ? 1 : 0;
+            fail[0] = step + 1;
+        }
+        return true;
+    }
+    return false;
+}
+
 template <class Cfg>
 constexpr int run_min_blocks() { return (Cfg::MIXED || Cfg::PAD || Cfg::SRC) ? 8 : 12; }
 
@@ -592,6 +610,7 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.x * kRunWarps + warp, nw = gridDim.x * kRunWarps;
     const int nperim = 2 * (p.Nxi + 1) + 2 * (p.Neta + 1);
+    unsigned long long pend = 0; // this lane's spread slot of the previous step
     for (int n = 0; n < nsteps; ++n) {
         const double* F = (n & 1) ? UB : UA;
         double* out = (n & 1) ? UA : UB;
@@ -631,20 +650,16 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
 #pragma unroll
         for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)m, o));
         if (lane == 0) atomicMax(spread + (size_t)n * kGuardSpread + gw % kGuardSpread, m);
+        // the guard decision of step n-1 is taken here, one step late: its maximum
+        // was loaded right after the previous barrier, so the L2 round trip hid
+        // behind this step's body.  Step n wrote the other buffer, so a trip still
+        // leaves the field after step n-1 (and its statistics) exactly as cpi::run
+        // reports them; every thread decides alike (same maximum).
+        if (n > 0 && guard_trips(pend, n - 1, gw, lane, blowup, slot, fail)) return;
         grid.sync();
-        unsigned long long v = __ldcg(spread + (size_t)n * kGuardSpread + lane);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) v = max(v, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)v, o));
-        if (gw == 0 && lane == 0) slot[n] = v;
-        const bool nonfinite = v >= 0x7FF0000000000000ull; // cpi.cpp:187-202
-        if (nonfinite || __longlong_as_double((long long)v) > blowup) {
-            if (gw == 0 && lane == 0) {
-                fail[1] = nonfinite ? 1 : 0;
-                fail[0] = n + 1;
-            }
-            return; // uniform: every thread saw the same maximum
-        }
+        pend = __ldcg(spread + (size_t)n * kGuardSpread + lane);
     }
+    if (nsteps > 0) guard_trips(pend, nsteps - 1, gw, lane, blowup, slot, fail);
 }
 
 // ---- instantiations --------------------------------------------------------
