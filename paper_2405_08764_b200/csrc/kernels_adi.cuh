@@ -80,45 +80,53 @@ __device__ inline UpwindW upwind_fb_x(int order, double r, double delta, int vel
 }
 
 // explicit operator of the direction not being swept, reaction carried half
-// (cross_term, microsim.cpp:357-395).  f: [n1][n2] tile; coef [6][N].
-__device__ inline double cross_term_x(const Params& p, const double* f, const EdgeSh* E, const double* gb,
-                                      const double* coef, int i, int j, bool eta_dir) {
+// (cross_term, microsim.cpp:357-395).  f(k): tile value at flat node k;
+// gb(k): ghost offset b at [edge * L + position]; coef [6][N].  Templated on
+// the accessors so the FAST fold can probe it with unit vectors.
+template <class FA, class GA>
+__device__ inline double cross_term_t(const Params& p, FA f, const EdgeSh* E, GA gb, const double* coef, int i, int j,
+                                      bool eta_dir) {
     const int nx = p.nx, ny = p.ny, n2 = p.n2, L = p.L, N = p.N, k = i * n2 + j;
     if (eta_dir) {
         const EdgeSh &gS = E[PD_EDGE_S], &gN = E[PD_EDGE_N];
-        const double glo = ghost_x(gS, f[i * n2 + 1], f[i * n2], gb[PD_EDGE_S * L + i]);
-        const double ghi = ghost_x(gN, f[i * n2 + ny - 1], f[i * n2 + ny], gb[PD_EDGE_N * L + i]);
-        const double um = j > 0 ? f[k - 1] : glo;
-        const double up = j < ny ? f[k + 1] : ghi;
-        const double uc = f[k];
+        const double glo = ghost_x(gS, f(i * n2 + 1), f(i * n2), gb(PD_EDGE_S * L + i));
+        const double ghi = ghost_x(gN, f(i * n2 + ny - 1), f(i * n2 + ny), gb(PD_EDGE_N * L + i));
+        const double um = j > 0 ? f(k - 1) : glo;
+        const double up = j < ny ? f(k + 1) : ghi;
+        const double uc = f(k);
         const double uyy = XDIV(XADD(XSUB(um, XMUL(2.0, uc)), up), XMUL(p.mdeta, p.mdeta));
         const double v = coef[PD_COEF_VY * N + k];
         const UpwindW sw = upwind_fb_x(p.upwind_order, p.upwind_r, p.mdeta, v >= 0 ? 1 : -1, j, ny);
         double du = 0.0;
         for (int m = 0; m < sw.n; ++m) {
             const int jj = j + sw.off[m];
-            const double val = jj < 0 ? glo : (jj > ny ? ghi : f[i * n2 + jj]);
+            const double val = jj < 0 ? glo : (jj > ny ? ghi : f(i * n2 + jj));
             du = XADD(du, XMUL(sw.w[m], val));
         }
         return XSUB(XSUB(XMUL(coef[PD_COEF_C * N + k], uyy), XMUL(v, du)),
                     XMUL(XMUL(0.5, coef[PD_COEF_W * N + k]), uc));
     }
     const EdgeSh &gW = E[PD_EDGE_W], &gE = E[PD_EDGE_E];
-    const double glo = ghost_x(gW, f[n2 + j], f[j], gb[PD_EDGE_W * L + j]);
-    const double ghi = ghost_x(gE, f[(nx - 1) * n2 + j], f[nx * n2 + j], gb[PD_EDGE_E * L + j]);
-    const double um = i > 0 ? f[k - n2] : glo;
-    const double up = i < nx ? f[k + n2] : ghi;
-    const double uc = f[k];
+    const double glo = ghost_x(gW, f(n2 + j), f(j), gb(PD_EDGE_W * L + j));
+    const double ghi = ghost_x(gE, f((nx - 1) * n2 + j), f(nx * n2 + j), gb(PD_EDGE_E * L + j));
+    const double um = i > 0 ? f(k - n2) : glo;
+    const double up = i < nx ? f(k + n2) : ghi;
+    const double uc = f(k);
     const double uxx = XDIV(XADD(XSUB(um, XMUL(2.0, uc)), up), XMUL(p.mdxi, p.mdxi));
     const double v = coef[PD_COEF_VX * N + k];
     const UpwindW sw = upwind_fb_x(p.upwind_order, p.upwind_r, p.mdxi, v >= 0 ? 1 : -1, i, nx);
     double du = 0.0;
     for (int m = 0; m < sw.n; ++m) {
         const int ii = i + sw.off[m];
-        const double val = ii < 0 ? glo : (ii > nx ? ghi : f[ii * n2 + j]);
+        const double val = ii < 0 ? glo : (ii > nx ? ghi : f(ii * n2 + j));
         du = XADD(du, XMUL(sw.w[m], val));
     }
     return XSUB(XSUB(XMUL(coef[PD_COEF_A * N + k], uxx), XMUL(v, du)), XMUL(XMUL(0.5, coef[PD_COEF_W * N + k]), uc));
+}
+
+__device__ inline double cross_term_x(const Params& p, const double* f, const EdgeSh* E, const double* gb,
+                                      const double* coef, int i, int j, bool eta_dir) {
+    return cross_term_t(p, [f](int k) { return f[k]; }, E, [gb](int k) { return gb[k]; }, coef, i, j, eta_dir);
 }
 
 // node_pinned  microsim.cpp:285-288

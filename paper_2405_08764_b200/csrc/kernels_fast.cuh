@@ -37,6 +37,7 @@ struct FastPlan {
     int LP = 0, G = 0, S = 0, nunits = 0;
     int mixed = 0;
     int big = 0; // 32x32 patches: kernels_fast_big.cuh (one CTA of 4 warps per patch)
+    int adi = 0; // ADI micro-solver: kernels_adi_fast.cuh (one warp per patch)
 };
 
 template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_, bool PAD_ = false, bool GEN_ = false, bool SRC_ = false>

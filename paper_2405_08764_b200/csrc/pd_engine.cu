@@ -18,6 +18,7 @@
 
 #include "coeffgen.hpp"
 #include "kernels_adi.cuh"
+#include "kernels_adi_fast.cuh"
 #include "kernels_exact.cuh"
 #include "kernels_fast.cuh"
 #include "kernels_fast_big.cuh"
@@ -82,6 +83,7 @@ struct pd_engine {
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
     DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
     DevBuf<double> d_adi_fac;           // ADI static line factors [sets][2][L][L][kAdiFac] (k_adi_factor)
+    DevBuf<double> d_adi_fast;          // FAST ADI folded tables [sets][2][N][kFA] (k_adi_fast_fold)
     double coeffgen_ms = 0.0;           // on-device table generation time at create (0: host tables)
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     bool subset = false;                // the patch list covers only part of the interior
@@ -108,6 +110,9 @@ struct pd_engine {
     void launch_step(const double* F, double* out, int out_mode, const double* srct, const int* fail) {
         if (step_kind == PD_STEP_LINEAR) {
             k_linear_step<<<(prm.P + 127) / 128, 128, 0, stream>>>(prm, F, out, out_mode, d_pij.p, d_roww.p, fail);
+        } else if (mode == PD_MODE_FAST && fast.adi) {
+            k_fast_adi<<<(prm.P + kFastAdiWarps - 1) / kFastAdiWarps, 32 * kFastAdiWarps, fast_adi_smem_bytes(prm),
+                         stream>>>(prm, F, out, out_mode, d_nbr.p, d_cset.p, d_adi_fast.p, srct, fail);
         } else if (mode == PD_MODE_FAST && fast.big) {
             launch_big(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
         } else if (mode == PD_MODE_FAST) {
@@ -445,6 +450,23 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             CUDA_TRY(cudaFuncSetAttribute(k_integrate_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)exact_smem_bytes(p)));
         }
+        // FAST ADI (kernels_adi_fast.cuh) up to 16 nodes per side: measured faster than the
+        // EXACT ADI kernel there (11^2: 1.3-1.4x) and slower beyond (21^2: its per-node
+        // tables outgrow the caches), where EXACT (bit-identical) stays the family
+        if (d.mode == PD_MODE_FAST && d.solver == PD_SOLVER_ADI && p.L <= 16) {
+            const size_t nf = (size_t)d.ncoeff_sets * adi_fast_doubles(p);
+            e->d_adi_fast.alloc(nf);
+            const int threads = 64, total = d.ncoeff_sets * 2 * p.L;
+            k_adi_fast_fold<<<(total + threads - 1) / threads, threads, 0, e->stream>>>(p, e->d_coeffs.p, e->d_src.p,
+                                                                                         d.ncoeff_sets, e->d_adi_fast.p);
+            e->check_launch();
+            if (fast_adi_smem_bytes(p) > 48 * 1024)
+                CUDA_TRY(cudaFuncSetAttribute(k_fast_adi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)fast_adi_smem_bytes(p)));
+            e->device_bytes += nf * 8;
+            e->fast.adi = 1;
+            e->mode = PD_MODE_FAST;
+        }
         if (d.mode == PD_MODE_FAST && d.solver == PD_SOLVER_EXPLICIT) { // the plans decide on sources
             if (plan_big(p, e->fast)) {
                 const size_t wcount = fast_weights_count(e->fast, p);
@@ -592,7 +614,7 @@ pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps
             return !(v && v[0] == '0');
         }();
         const bool fused_ok = !block_run && fused_enabled && nsteps > 0 && e->step_kind == PD_STEP_DIRECT &&
-                              e->mode == PD_MODE_FAST && !e->fast.big && e->prm.k == 0 && !e->subset;
+                              e->mode == PD_MODE_FAST && !e->fast.big && !e->fast.adi && e->prm.k == 0 && !e->subset;
         if (fused_ok) {
             e->d_spread.alloc((size_t)nsteps * kGuardSpread);
             CUDA_TRY(cudaMemsetAsync(e->d_spread.p, 0, (size_t)nsteps * kGuardSpread * 8, e->stream));

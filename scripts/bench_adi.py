@@ -1,5 +1,5 @@
-"""ADI micro-solver on the B200 (EXACT family) vs the unmodified reference on one host core.
-Writes profiles/r01_adi.jsonl.   python scripts/bench_adi.py"""
+"""ADI micro-solver on the B200 (EXACT and FAST families) vs the unmodified reference on one host core.
+Writes profiles/r01_adi.jsonl (or the path given).   python scripts/bench_adi.py [out.jsonl]"""
 import json, sys, time
 from pathlib import Path
 
@@ -23,17 +23,20 @@ cases = [
 out = []
 for label, over, steps in cases:
     P = Problem(configs.copy_desc(base, **over))
-    E = Engine.from_problem(P)
     U0 = P.initial_field()
     bnd, src = P.boundary_table(0.0, steps), P.source_time(0.0, steps)
-    E.run(U0, 3, bnd=bnd[:3], src_time=src[:3])
-    U, st = E.run(U0, steps, bnd=bnd, src_time=src, raise_on_instability=False)
-    assert st.steps_done == steps, f"{label}: macro guard tripped at step {st.failed_step}" 
     n1, n2, nt = P.desc.nx + 1, P.desc.ny + 1, P.desc.nt
-    upd = E.P * n1 * n2 * nt
-    rec = {"workload": label, "patches": E.P, "micro_nodes": n1 * n2, "nt": nt, "macro_steps": steps,
-           "gpu_ms_per_macro_step": st.device_ms / steps, "gpu_node_updates_per_s": upd * steps / (st.device_ms * 1e-3),
-           "kernel_family": "exact (ADI)"}
+    rec = {"workload": label, "micro_nodes": n1 * n2, "nt": nt, "macro_steps": steps}
+    for fam, mode in (("exact", abi.PD_MODE_EXACT), ("fast", abi.PD_MODE_FAST)):
+        E = Engine.from_problem(P, mode=mode)
+        E.run(U0, 3, bnd=bnd[:3], src_time=src[:3])
+        U, st = E.run(U0, steps, bnd=bnd, src_time=src, raise_on_instability=False)
+        assert st.steps_done == steps, f"{label} {fam}: macro guard tripped at step {st.failed_step}"
+        upd = E.P * n1 * n2 * nt
+        rec["patches"] = E.P
+        rec[f"gpu_{fam}_ms_per_macro_step"] = st.device_ms / steps
+        rec[f"gpu_{fam}_node_updates_per_s"] = upd * steps / (st.device_ms * 1e-3)
+        rec[f"gpu_{fam}_kernel_family"] = "exact" if E.mode == abi.PD_MODE_EXACT else "fast"
     if reference_available():
         R = Reference().engine(P.desc)
         Ur = R.initial_field()
@@ -43,4 +46,4 @@ for label, over, steps in cases:
                     "ref_cores": 1, "ref_sample_steps": n})
     out.append(rec)
     print(json.dumps(rec), flush=True)
-(ROOT / "profiles" / "r01_adi.jsonl").write_text("".join(json.dumps(r) + "\n" for r in out))
+(Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "profiles" / "r01_adi.jsonl").write_text("".join(json.dumps(r) + "\n" for r in out))
