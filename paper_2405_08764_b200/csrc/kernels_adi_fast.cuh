@@ -13,12 +13,12 @@
 // with reciprocal pivots: Thomas (l, 1/m, w) for two-point upwinding, the
 // pivot-free kl = ku = 2 band elimination (multipliers, 1/B0, upper band)
 // otherwise (linalg.cpp:8-61).  The fused step then does, per micro step and
-// pass, one 5-term dot product and one substitution per node.
+// pass, one 3- (5-)term dot product and one substitution per node.
 //
-// One warp per patch (patches up to 32x32): lane l owns line l of the current
-// pass; the tile lives in shared memory (two padded copies, ping-pong), so the
-// explicit direction's neighbours are plain shared loads and the line solve
-// runs down the lane's own column/row.  Within 1e-11 of the reference like the
+// One warp per patch (patches up to 32x32): the tile lives in shared memory
+// (two padded copies, ping-pong); the right-hand side runs with the lanes
+// across nodes, then lane l solves line l of the current pass down its own
+// column/row.  Within 1e-11 of the reference like the
 // explicit FAST kernels (reciprocal pivots and fma instead of IEEE divisions
 // in the reference's order); EXACT stays the bit-identical path.
 #pragma once
@@ -28,14 +28,35 @@
 
 namespace pdb200::dev {
 
-constexpr int kFA = 16; // doubles per (set, direction, node)
-enum { FA_W = 0, FA_BLO = 5, FA_BHI = 6, FA_SRC = 7, FA_F0 = 8, FA_F1 = 9, FA_F2 = 10, FA_F3 = 11, FA_F4 = 12,
-       FA_ADJ = 13 };
 constexpr int kFastAdiWarps = 4;
 
-__host__ __device__ inline size_t adi_fast_doubles(const Params& p) { return (size_t)2 * p.N * kFA; }
+// Per-set table, [dir] = 0 (implicit xi: lines j, k = i) / 1 (implicit eta: lines i, k = j), nodes in
+// line order (t = line * n + k):
+//   core [2][N][KC]: the explicit half's along-direction weights and the line factors
+//        two-point upwinding  KC = 6:  W(-1) W(0) W(+1) | l  1/m  w        (Thomas)
+//        three/four-point     KC = 10: W(-2..+2)        | f1 f2 1/B0 B1 B2 (band LU)
+//   blo/bhi [2][L]: ghost-offset weights, nonzero only on the first / last line
+//   adjlo/adjhi [2][L]: the implicit rows' ghost-offset coefficient at k = 0 / n-1
+//   src [2][N]: half * spatial source (separable sources only)
+// Only what a node uses is stored: 48 bytes per node and pass for two-point upwinding.
+struct AdiFastLayout {
+    int KC;
+    size_t blo, bhi, adjlo, adjhi, src, total;
+};
+__host__ __device__ inline AdiFastLayout adi_fast_layout(const Params& p) {
+    AdiFastLayout l;
+    l.KC = p.upwind_order == PD_UPWIND_TWO ? 6 : 10;
+    l.blo = (size_t)2 * p.N * l.KC;
+    l.bhi = l.blo + 2 * (size_t)p.L;
+    l.adjlo = l.bhi + 2 * (size_t)p.L;
+    l.adjhi = l.adjlo + 2 * (size_t)p.L;
+    l.src = l.adjhi + 2 * (size_t)p.L;
+    l.total = l.src + (p.source == PD_SOURCE_SEPARABLE ? 2 * (size_t)p.N : 0);
+    return l;
+}
+__host__ __device__ inline size_t adi_fast_doubles(const Params& p) { return adi_fast_layout(p).total; }
 
-// Table: [set][dir][line][k][kFA]; dir 0 = implicit xi (lines j, k = i), dir 1 = implicit eta (lines i, k = j)
+// One thread per (set, direction, line); the table must be zeroed (unused weights stay 0).
 __global__ void k_adi_fast_fold(Params p, const double* __restrict__ coeffs, const double* __restrict__ src_sp,
                                 int nsets, double* __restrict__ tab) {
     const int kind = p.bc_type == PD_BC_DIRICHLET ? PD_EDGE_DIRICHLET
@@ -56,36 +77,42 @@ __global__ void k_adi_fast_fold(Params p, const double* __restrict__ coeffs, con
         if (line > nline) continue;
         const double* coef = coeffs + (size_t)set * PD_NCOEF * p.N;
         const double* sp = src_sp ? src_sp + (size_t)set * p.N : nullptr;
-        double* T = tab + (size_t)set * adi_fast_doubles(p) + ((size_t)dir * p.N + (size_t)line * n) * kFA;
+        const AdiFastLayout lay = adi_fast_layout(p);
+        double* S0 = tab + (size_t)set * lay.total;                       // this set's table (zeroed)
+        double* C = S0 + ((size_t)dir * p.N + (size_t)line * n) * lay.KC; // this line's core rows
         const int elo_x = xi_dir ? PD_EDGE_S : PD_EDGE_W, ehi_x = xi_dir ? PD_EDGE_N : PD_EDGE_E; // explicit dir
+        const int wide = lay.KC == 10 ? 2 : 1;                            // weight offsets stored: -wide..wide
         for (int k = 0; k < n; ++k) {
             const int i = xi_dir ? k : line, j = xi_dir ? line : k, q = i * n2 + j;
-            double* o = T + (size_t)k * kFA;
-            for (int f = 0; f < kFA; ++f) o[f] = 0.0;
+            double* o = C + (size_t)k * lay.KC;
             if (!node_pinned_x(E, i, j, p.nx, p.ny)) {
                 // explicit half (rhs = f + half (cross_term + G)), probed with unit vectors
-                for (int off = -2; off <= 2; ++off) {
+                for (int off = -wide; off <= wide; ++off) {
                     const int ii = xi_dir ? i : i + off, jj = xi_dir ? j + off : j;
                     if (ii < 0 || ii > p.nx || jj < 0 || jj > p.ny) continue;
                     const int tgt = ii * n2 + jj;
                     auto fu = [tgt](int kk) { return kk == tgt ? 1.0 : 0.0; };
                     auto g0 = [](int) { return 0.0; };
                     const double ct = cross_term_t(p, fu, E, g0, coef, i, j, xi_dir);
-                    o[FA_W + off + 2] = XADD(off == 0 ? 1.0 : 0.0, XMUL(half, ct));
+                    o[off + wide] = XADD(off == 0 ? 1.0 : 0.0, XMUL(half, ct));
                 }
                 const int pos = xi_dir ? i : j;
                 auto f0 = [](int) { return 0.0; };
                 const int glo = elo_x * L + pos, ghi = ehi_x * L + pos;
-                o[FA_BLO] = XMUL(half, cross_term_t(p, f0, E, [glo](int kk) { return kk == glo ? 1.0 : 0.0; }, coef,
-                                                    i, j, xi_dir));
-                o[FA_BHI] = XMUL(half, cross_term_t(p, f0, E, [ghi](int kk) { return kk == ghi ? 1.0 : 0.0; }, coef,
-                                                    i, j, xi_dir));
-                if (sp) o[FA_SRC] = XMUL(half, sp[q]);
+                // a ghost is read only by the first / last line's nodes (cross_term: j == 0 / ny)
+                if (line == 0)
+                    S0[lay.blo + dir * L + k] = XMUL(
+                        half, cross_term_t(p, f0, E, [glo](int kk) { return kk == glo ? 1.0 : 0.0; }, coef, i, j, xi_dir));
+                if (line == nline)
+                    S0[lay.bhi + dir * L + k] = XMUL(
+                        half, cross_term_t(p, f0, E, [ghi](int kk) { return kk == ghi ? 1.0 : 0.0; }, coef, i, j, xi_dir));
+                if (sp) S0[lay.src + (size_t)dir * p.N + (size_t)line * n + k] = XMUL(half, sp[q]);
             }
-            o[FA_ADJ] = adi_row(p, E, coef, xi_dir, line, k).adj;
+            if (k == 0) S0[lay.adjlo + dir * L + line] = adi_row(p, E, coef, xi_dir, line, k).adj;
+            if (k == n - 1) S0[lay.adjhi + dir * L + line] = adi_row(p, E, coef, xi_dir, line, k).adj;
         }
         // implicit half: factor the line matrix with reciprocal pivots
-        if (p.upwind_order == PD_UPWIND_TWO) {
+        if (lay.KC == 6) {
             double wprev = 0.0;
             for (int k = 0; k < n; ++k) {
                 const AdiRow r = adi_row(p, E, coef, xi_dir, line, k);
@@ -93,41 +120,36 @@ __global__ void k_adi_fast_fold(Params p, const double* __restrict__ coeffs, con
                 const double m = k == 0 ? r.diag : r.diag - lo * wprev;
                 const double im = 1.0 / m;
                 wprev = up * im;
-                T[(size_t)k * kFA + FA_F0] = lo;
-                T[(size_t)k * kFA + FA_F1] = im;
-                T[(size_t)k * kFA + FA_F2] = wprev;
+                C[(size_t)k * 6 + 3] = lo;
+                C[(size_t)k * 6 + 4] = im;
+                C[(size_t)k * 6 + 5] = wprev;
             }
         } else {
-            // band B(r, -2..2) in F0..F4 during the elimination, then multipliers in F0/F1,
-            // 1/B0 in F2, B1/B2 in F3/F4
+            double band[33][5], mult[33][2];
             for (int k = 0; k < n; ++k) {
                 const AdiRow r = adi_row(p, E, coef, xi_dir, line, k);
-                double* b = T + (size_t)k * kFA + FA_F0;
-                b[0] = r.pinned ? 0.0 : r.lo2;
-                b[1] = (r.pinned || k == 0) ? 0.0 : r.sub;
-                b[2] = r.diag;
-                b[3] = (r.pinned || k == n - 1) ? 0.0 : r.sup;
-                b[4] = r.pinned ? 0.0 : r.hi2;
+                band[k][0] = r.pinned ? 0.0 : r.lo2;
+                band[k][1] = (r.pinned || k == 0) ? 0.0 : r.sub;
+                band[k][2] = r.diag;
+                band[k][3] = (r.pinned || k == n - 1) ? 0.0 : r.sup;
+                band[k][4] = r.pinned ? 0.0 : r.hi2;
+                mult[k][0] = mult[k][1] = 0.0;
             }
-            auto B = [&](int row, int off) -> double& { return T[(size_t)row * kFA + FA_F0 + 2 + off]; };
-            double mult[2 * 33];
-            for (int k = 0; k < n - 1; ++k) {
-                const double piv = B(k, 0);
+            for (int k = 0; k < n - 1; ++k) { // pivot-free elimination (linalg.cpp:43-61)
+                const double piv = band[k][2];
                 for (int r = k + 1; r <= min(k + 2, n - 1); ++r) {
-                    const double f = B(r, k - r) / piv;
-                    mult[2 * k + (r - k - 1)] = f;
-                    for (int c = k + 1; c <= min(k + 2, n - 1); ++c) B(r, c - r) -= f * B(k, c - k);
+                    const double f = band[r][2 + k - r] / piv;
+                    mult[k][r - k - 1] = f;
+                    for (int c = k + 1; c <= min(k + 2, n - 1); ++c) band[r][2 + c - r] -= f * band[k][2 + c - k];
                 }
-                if (k + 2 > n - 1) mult[2 * k + 1] = 0.0;
             }
             for (int k = 0; k < n; ++k) {
-                double* b = T + (size_t)k * kFA;
-                const double b0 = b[FA_F0 + 2], b1 = b[FA_F0 + 3], b2 = b[FA_F0 + 4];
-                b[FA_F0] = k < n - 1 ? mult[2 * k] : 0.0;
-                b[FA_F1] = k < n - 1 ? mult[2 * k + 1] : 0.0;
-                b[FA_F2] = 1.0 / b0;
-                b[FA_F3] = k + 1 < n ? b1 : 0.0;
-                b[FA_F4] = k + 2 < n ? b2 : 0.0;
+                double* c = C + (size_t)k * 10;
+                c[5] = mult[k][0];
+                c[6] = mult[k][1];
+                c[7] = 1.0 / band[k][2];
+                c[8] = k + 1 < n ? band[k][3] : 0.0;
+                c[9] = k + 2 < n ? band[k][4] : 0.0;
             }
         }
     }
@@ -213,9 +235,11 @@ k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int
     __syncwarp();
 
     const int set = cset ? cset[patch] : patch;
-    const double* T0 = tab + (size_t)set * adi_fast_doubles(p);
-    const bool banded = p.upwind_order != PD_UPWIND_TWO;
+    const AdiFastLayout lay = adi_fast_layout(p);
+    const double* S0 = tab + (size_t)set * lay.total;
+    const bool banded = lay.KC == 10;
     const bool pin = p.pinned != 0;
+    const double* srcw = p.source == PD_SOURCE_SEPARABLE ? S0 + lay.src : nullptr;
     for (int step = 0; step < p.nt; ++step) {
         const double ft = srct ? __ldg(srct + step) : 0.0;
 #pragma unroll 1
@@ -228,6 +252,7 @@ k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const int is = xi_dir ? TS : 1;  // implicit-direction stride
             const int elo = xi_dir ? PD_EDGE_W : PD_EDGE_S, ehi = xi_dir ? PD_EDGE_E : PD_EDGE_N;
             const int xlo = xi_dir ? PD_EDGE_S : PD_EDGE_W, xhi = xi_dir ? PD_EDGE_N : PD_EDGE_E;
+            const double* Cd = S0 + (size_t)dir * p.N * lay.KC;
             // right-hand side (explicit half) on every node, lanes across nodes
             for (int t = lane; t < (nline + 1) * n; t += 32) {
                 const int line = t / n, k = t - line * n;
@@ -238,17 +263,23 @@ k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int
                 } else if (pin && (k == 0 || k == n - 1)) {
                     r = gb[(k == 0 ? elo : ehi) * L + line];
                 } else {
-                    const double* w = T0 + ((size_t)dir * p.N + (size_t)t) * kFA;
-                    r = w[FA_W + 2] * src[c];
-                    r = __fma_rn(w[FA_W + 1], src[c - es], r);
-                    r = __fma_rn(w[FA_W + 3], src[c + es], r);
-                    r = __fma_rn(w[FA_W + 0], src[c - 2 * es], r);
-                    r = __fma_rn(w[FA_W + 4], src[c + 2 * es], r);
-                    r = __fma_rn(w[FA_BLO], gb[xlo * L + k], r);
-                    r = __fma_rn(w[FA_BHI], gb[xhi * L + k], r);
-                    r = __fma_rn(w[FA_SRC], ft, r);
-                    if (k == 0) r = __fma_rn(-w[FA_ADJ], gb[elo * L + line], r);
-                    else if (k == n - 1) r = __fma_rn(-w[FA_ADJ], gb[ehi * L + line], r);
+                    const double* w = Cd + (size_t)t * lay.KC;
+                    if (!banded) {
+                        r = w[1] * src[c];
+                        r = __fma_rn(w[0], src[c - es], r);
+                        r = __fma_rn(w[2], src[c + es], r);
+                    } else {
+                        r = w[2] * src[c];
+                        r = __fma_rn(w[1], src[c - es], r);
+                        r = __fma_rn(w[3], src[c + es], r);
+                        r = __fma_rn(w[0], src[c - 2 * es], r);
+                        r = __fma_rn(w[4], src[c + 2 * es], r);
+                    }
+                    if (line == 0) r = __fma_rn(S0[lay.blo + dir * L + k], gb[xlo * L + k], r);
+                    if (line == nline) r = __fma_rn(S0[lay.bhi + dir * L + k], gb[xhi * L + k], r);
+                    if (srcw) r = __fma_rn(srcw[(size_t)dir * p.N + t], ft, r);
+                    if (k == 0) r = __fma_rn(-S0[lay.adjlo + dir * L + line], gb[elo * L + line], r);
+                    else if (k == n - 1) r = __fma_rn(-S0[lay.adjhi + dir * L + line], gb[ehi * L + line], r);
                 }
                 dst[c] = r;
             }
@@ -257,37 +288,37 @@ k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int
             for (int line = lane; line <= nline; line += 32) {
                 if (pin && (line == 0 || line == nline)) continue;
                 const int base = xi_dir ? at(0, line) : at(line, 0);
-                const double* T = T0 + ((size_t)dir * p.N + (size_t)line * n) * kFA;
+                const double* T = Cd + (size_t)line * n * lay.KC;
                 if (!banded) { // Thomas with reciprocal pivots
                     double y = 0.0;
 #pragma unroll 4
                     for (int k = 0; k < n; ++k) {
-                        const double* w = T + (size_t)k * kFA;
+                        const double* w = T + (size_t)k * 6;
                         const int c = base + k * is;
-                        y = (k == 0 ? dst[c] : __fma_rn(-w[FA_F0], y, dst[c])) * w[FA_F1];
+                        y = (k == 0 ? dst[c] : __fma_rn(-w[3], y, dst[c])) * w[4];
                         dst[c] = y;
                     }
 #pragma unroll 4
                     for (int k = n - 2; k >= 0; --k) {
                         const int c = base + k * is;
-                        y = __fma_rn(-T[(size_t)k * kFA + FA_F2], y, dst[c]);
+                        y = __fma_rn(-T[(size_t)k * 6 + 5], y, dst[c]);
                         dst[c] = y;
                     }
                 } else { // pivot-free band LU (kl = ku = 2)
 #pragma unroll 4
                     for (int k = 0; k < n - 1; ++k) {
-                        const double* w = T + (size_t)k * kFA;
+                        const double* w = T + (size_t)k * 10;
                         const int c = base + k * is;
                         const double rk = dst[c];
-                        dst[c + is] = __fma_rn(-w[FA_F0], rk, dst[c + is]);
-                        if (k + 2 < n) dst[c + 2 * is] = __fma_rn(-w[FA_F1], rk, dst[c + 2 * is]);
+                        dst[c + is] = __fma_rn(-w[5], rk, dst[c + is]);
+                        if (k + 2 < n) dst[c + 2 * is] = __fma_rn(-w[6], rk, dst[c + 2 * is]);
                     }
                     double x1 = 0.0, x2 = 0.0;
 #pragma unroll 4
                     for (int k = n - 1; k >= 0; --k) {
-                        const double* w = T + (size_t)k * kFA;
+                        const double* w = T + (size_t)k * 10;
                         const int c = base + k * is;
-                        const double x = __fma_rn(-w[FA_F4], x2, __fma_rn(-w[FA_F3], x1, dst[c])) * w[FA_F2];
+                        const double x = __fma_rn(-w[9], x2, __fma_rn(-w[8], x1, dst[c])) * w[7];
                         dst[c] = x;
                         x2 = x1;
                         x1 = x;

@@ -83,7 +83,7 @@ struct pd_engine {
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
     DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
     DevBuf<double> d_adi_fac;           // ADI static line factors [sets][2][L][L][kAdiFac] (k_adi_factor)
-    DevBuf<double> d_adi_fast;          // FAST ADI folded tables [sets][2][N][kFA] (k_adi_fast_fold)
+    DevBuf<double> d_adi_fast;          // FAST ADI folded tables (adi_fast_layout, k_adi_fast_fold)
     double coeffgen_ms = 0.0;           // on-device table generation time at create (0: host tables)
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     bool subset = false;                // the patch list covers only part of the interior
@@ -453,9 +453,10 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
         // FAST ADI (kernels_adi_fast.cuh) up to 16 nodes per side: measured faster than the
         // EXACT ADI kernel there (11^2: 1.3-1.4x) and slower beyond (21^2: its per-node
         // tables outgrow the caches), where EXACT (bit-identical) stays the family
-        if (d.mode == PD_MODE_FAST && d.solver == PD_SOLVER_ADI && p.L <= 16) {
+        if (d.mode == PD_MODE_FAST && d.solver == PD_SOLVER_ADI && p.L <= 32) {
             const size_t nf = (size_t)d.ncoeff_sets * adi_fast_doubles(p);
             e->d_adi_fast.alloc(nf);
+            CUDA_TRY(cudaMemsetAsync(e->d_adi_fast.p, 0, nf * 8, e->stream));
             const int threads = 64, total = d.ncoeff_sets * 2 * p.L;
             k_adi_fast_fold<<<(total + threads - 1) / threads, threads, 0, e->stream>>>(p, e->d_coeffs.p, e->d_src.p,
                                                                                          d.ncoeff_sets, e->d_adi_fast.p);

@@ -580,6 +580,25 @@ def test_fast_adi_vs_reference(name, gpu):
     assert rel(Uf, Ue) < 1e-13 * (P.desc.T / P.desc.Nt) / P.desc.tau
 
 
+@pytest.mark.parametrize("over", [dict(nx=20, ny=20), dict(nx=20, ny=20, upwind_order=abi.PD_UPWIND_FOUR),
+                                  dict(nx=31, ny=31, bc_type=abi.PD_BC_DIRICHLET), dict(nx=14, ny=24)],
+                         ids=["21x21", "21x21-four", "32x32-dirichlet", "15x25"])
+def test_fast_adi_larger_patches_vs_exact(over, gpu):
+    P = load("ref_table1_cdr_const", N_xi=6, N_eta=6, nt=4, **over)
+    Ef = Engine.from_problem(P, mode=FAST)
+    Ee = Engine.from_problem(P, mode=EXACT)
+    assert Ef.mode == FAST and Ee.mode == EXACT
+    U0 = P.initial_field()
+    n = 5
+    bt, stt = P.boundary_table(0.0, n), P.source_time(0.0, n)
+    g1f = Ef.step_direct(U0, 0.0, bnd=bt[0][0], src_time=stt[0][0])
+    g1e = Ee.step_direct(U0, 0.0, bnd=bt[0][0], src_time=stt[0][0])
+    assert rel(g1f, g1e) < 1e-13
+    Uf, _ = Ef.run(U0, n, bnd=bt, src_time=stt)
+    Ue, _ = Ee.run(U0, n, bnd=bt, src_time=stt)
+    assert rel(Uf, Ue) < 1e-13 * (P.desc.T / P.desc.Nt) / P.desc.tau
+
+
 def test_adi_reproduces_shipped_table1_output(gpu):
     """proj/out/table1: problem1_constant(0), ADI, nt = 2, 1001 macro steps —
     every shipped snapshot reproduced bit for bit."""
