@@ -161,7 +161,7 @@ inline size_t fast_adi_smem_bytes(const Params& p) {
 }
 
 // The fused step with the FAST ADI micro-solver, one warp per patch.
-__global__ void __launch_bounds__(32 * kFastAdiWarps)
+__global__ void __launch_bounds__(32 * kFastAdiWarps, 4)
 k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
            const int* __restrict__ cset, const double* __restrict__ tab, const double* __restrict__ srct,
            const int* __restrict__ fail_flag) {
