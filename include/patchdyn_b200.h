@@ -126,7 +126,7 @@ typedef struct pd_engine_desc {
     double l;
     int32_t mode;
     /* micro-solver: PD_SOLVER_EXPLICIT (microsim.cpp:292-332) or PD_SOLVER_ADI
-     * (Peaceman-Rachford, microsim.cpp:334-507; EXACT family, or FAST for patches up to 16x16), with the
+     * (Peaceman-Rachford, microsim.cpp:334-507; EXACT family, or FAST for patches up to 32x32), with the
      * ADI upwind order/parameter (UpwindSpec, microsim.hpp) */
     int32_t solver;
     int32_t upwind_order;

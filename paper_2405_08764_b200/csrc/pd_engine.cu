@@ -450,9 +450,9 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             CUDA_TRY(cudaFuncSetAttribute(k_integrate_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)exact_smem_bytes(p)));
         }
-        // FAST ADI (kernels_adi_fast.cuh) up to 16 nodes per side: measured faster than the
-        // EXACT ADI kernel there (11^2: 1.3-1.4x) and slower beyond (21^2: its per-node
-        // tables outgrow the caches), where EXACT (bit-identical) stays the family
+        // FAST ADI (kernels_adi_fast.cuh) up to 32 nodes per side: with the compact per-node
+        // tables it measured 1.5-2.3x faster than the EXACT ADI kernel at 11^2 and 3.0x at 21^2
+        // (profiles/r01_adi.jsonl); larger patches stay on EXACT (bit-identical)
         if (d.mode == PD_MODE_FAST && d.solver == PD_SOLVER_ADI && p.L <= 32) {
             const size_t nf = (size_t)d.ncoeff_sets * adi_fast_doubles(p);
             e->d_adi_fast.alloc(nf);
