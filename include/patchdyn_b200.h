@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define PD_ABI_VERSION 3
+#define PD_ABI_VERSION 4
 
 /* Status codes map 1:1 onto the reference exception types
  * (proj/include/patchdyn/errors.hpp:9-61). */
@@ -206,6 +206,20 @@ pd_status pd_run(pd_engine* e, double* U_host, int32_t nsteps, double t0, const 
 pd_status pd_run_device(pd_engine* e, double* U_dev, double* U_scratch_dev, int32_t nsteps,
                         double t0, const double* bnd_dev, const double* src_time_dev,
                         pd_run_stats* stats);
+/* pd_run / pd_run_device plus cpi::run's per-step exact-error metric on the
+ * device (max_percent_error, cpi.cpp:79-94 called at cpi.cpp:204-209; replaces
+ * the host loop a RunResult's step_max_pct_err needs): exact: [nsteps][NF] =
+ * the exact solution sampled on every macro node at t0 + (n+1) dt_macro
+ * (ProblemSpec::exact(xi(i), eta(j), t), i-major like Field2D; only the patch
+ * nodes are read); err_out: [nsteps] = max over the patch nodes with
+ * |exact| >= 1e-12 of |U - exact| / |exact| * 100, 0 when none — bit-identical
+ * to the reference's loop.  Steps after a tripped guard are left at 0. */
+pd_status pd_run_exact(pd_engine* e, double* U_host, int32_t nsteps, double t0, const double* bnd_host,
+                       const double* src_time_host, const double* exact_host, double* err_out_host,
+                       pd_run_stats* stats);
+pd_status pd_run_device_exact(pd_engine* e, double* U_dev, double* U_scratch_dev, int32_t nsteps,
+                              double t0, const double* bnd_dev, const double* src_time_dev,
+                              const double* exact_dev, double* err_out_dev, pd_run_stats* stats);
 
 /* Measurement hooks (no reference analogue; used by bench.py).
  * pd_device_count: CUDA devices visible (0 on a CPU-only host).

@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-PD_ABI_VERSION = 3
+PD_ABI_VERSION = 4
 
 # pd_status  (errors.hpp:9-61 mapping)
 PD_OK = 0

@@ -295,8 +295,13 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
     };
     for (auto [pi, pj] : opts.probe_nodes) res.probes.push_back(ProbeSeries{pi, pj, {}});
     maybe_snapshot(0, 0.0);
-    const bool per_step = !opts.probe_nodes.empty() || engine.problem().has_exact() || !snap.empty() ||
-                          opts.progress_every > 0;
+    // the exact-error metric runs on the device (pd_run_exact); probes, snapshots
+    // and progress callbacks need the field on the host after every step
+    const bool per_step = !opts.probe_nodes.empty() || !snap.empty() || opts.progress_every > 0;
+    const bool has_exact = engine.problem().has_exact();
+    const auto& g = engine.grid();
+    const size_t NF = static_cast<size_t>(g.Nxi + 1) * (g.Neta + 1);
+    const int i_lo = U.periodic_xi() ? 0 : 1;
     const int chunk = per_step ? 1 : cfg.Nt;
     const int k = cfg.k;
     const size_t L = pd_perimeter_len(cfg.N_xi, cfg.N_eta);
@@ -315,10 +320,25 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
             src.insert(src.end(), f.begin(), f.end());
         }
         (void)L;
+        // exact solution on the patch nodes at the end of every step of the chunk,
+        // sampled as max_percent_error does (cpi.cpp:79-94)
+        std::vector<double> exact, err;
+        if (has_exact) {
+            exact.assign(NF * static_cast<size_t>(m), 0.0);
+            err.assign(static_cast<size_t>(m), 0.0);
+            for (int q = 0; q < m; ++q) {
+                const double t1 = (n + q + 1) * dt;
+                double* ex = exact.data() + NF * static_cast<size_t>(q);
+                for (int i = i_lo; i <= g.Nxi - 1; ++i)
+                    for (int j = 1; j <= g.Neta - 1; ++j)
+                        ex[static_cast<size_t>(i) * (g.Neta + 1) + j] = engine.problem().exact(g.xi(i), g.eta(j), t1);
+            }
+        }
         pd_run_stats st{};
         engine.select_default_step(); // projective_step -> engine.step  cpi.cpp:65
-        const int rc = pd_run(engine.device(), U.U.data(), m, n * dt, bnd.data(), src.empty() ? nullptr : src.data(),
-                              &st);
+        const int rc = pd_run_exact(engine.device(), U.U.data(), m, n * dt, bnd.data(),
+                                    src.empty() ? nullptr : src.data(), has_exact ? exact.data() : nullptr,
+                                    has_exact ? err.data() : nullptr, &st);
         if (rc == PD_MACRO_INSTABILITY) {
             std::ostringstream os;
             os << pd_last_error(engine.device());
@@ -328,8 +348,7 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
         for (int q = 0; q < m; ++q) res.times.push_back((n + q + 1) * dt);
         const double t1 = (n + m) * dt;
         for (auto& ps : res.probes) ps.values.push_back(U.at(ps.i, ps.j));
-        if (engine.problem().has_exact()) {
-            const double e = max_percent_error(engine, U, t1);
+        for (double e : err) { // device max_percent_error of every step of the chunk
             res.step_max_pct_err.push_back(e);
             res.max_pct_err = std::max(res.max_pct_err, e);
         }

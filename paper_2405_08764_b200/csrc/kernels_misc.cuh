@@ -98,6 +98,37 @@ __global__ void k_guard(const double* __restrict__ U, size_t n, unsigned long lo
     }
 }
 
+// ---- cpi::run's per-step exact-error metric (max_percent_error, cpi.cpp:79-94) ----
+// max over the patch nodes i in [i_lo, Nxi-1], j in [1, Neta-1] (i_lo = 0 when
+// periodic) with |exact| >= 1e-12 of |U - exact| / |exact| * 100, in the
+// reference's operation order (no contraction: subtract, abs, divide, scale),
+// reduced as the bit pattern of a non-negative double into err[step] (zeroed
+// by the caller; 0 when no node qualifies, like the reference's `worst`).
+// A tripped guard (fail_flag) makes it a no-op: cpi::run throws before it.
+__global__ void k_exact_err(Params p, const double* __restrict__ U, const double* __restrict__ ex,
+                            unsigned long long* err, const int* __restrict__ fail_flag, int step) {
+    if (*fail_flag) return;
+    const int i_lo = p.periodic ? 0 : 1;
+    const int ni = p.Nxi - i_lo, nj = p.Neta - 1;
+    const size_t n = (size_t)ni * nj;
+    unsigned long long m = 0;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+        const size_t node = (size_t)(i_lo + (int)(t / nj)) * p.NF2 + 1 + (int)(t % nj);
+        const double e = ex[node];
+        if (fabs(e) < 1e-12) continue;
+        const double pct = __dmul_rn(__ddiv_rn(fabs(__dsub_rn(U[node], e)), fabs(e)), 100.0);
+        m = max(m, (unsigned long long)__double_as_longlong(pct));
+    }
+    for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)m, o));
+    __shared__ unsigned long long wm[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, wm[w]);
+        if (m) atomicMax(err + step, m);
+    }
+}
+
 // ---- whole linear-response run in one CTA (fields resident in shared memory) ----
 // pd_run_device with PD_STEP_LINEAR when the macro field fits in shared memory:
 // every macro step (k+1 linear substeps, the projective extrapolation, the

@@ -84,6 +84,7 @@ struct pd_engine {
     DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
     DevBuf<double> d_adi_fac;           // ADI static line factors [sets][2][L][L][kAdiFac] (k_adi_factor)
     DevBuf<double> d_adi_fast;          // FAST ADI folded tables (adi_fast_layout, k_adi_fast_fold)
+    DevBuf<double> d_exact;             // pd_run_exact: exact-solution table [nsteps][NF] + errors [nsteps]
     double coeffgen_ms = 0.0;           // on-device table generation time at create (0: host tables)
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     bool subset = false;                // the patch list covers only part of the interior
@@ -577,9 +578,13 @@ pd_status pd_projective_step(pd_engine* e, const double* U_in, double* U_out, do
     });
 }
 
-pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps, double t0, const double* bnd,
-                        const double* src_time, pd_run_stats* stats) {
-    if (!e || !U || !scratch || nsteps < 0) return PD_VALIDATION_ERROR;
+namespace {
+// exact/err (device, optional): the per-step exact-error metric (k_exact_err)
+// after every step's guard; it needs the field of every step, so it takes the
+// multi-launch loop (still no host round trip inside the run)
+pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nsteps, double t0, const double* bnd,
+                          const double* src_time, const double* exact, double* err, pd_run_stats* stats) {
+    if (!e || !U || !scratch || nsteps < 0 || (exact != nullptr) != (err != nullptr)) return PD_VALIDATION_ERROR;
     (void)t0;
     pd_status result = PD_OK;
     const pd_status st = guarded(e, [&] {
@@ -607,19 +612,21 @@ pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps
         // linear-response steps on a field that fits in shared memory: the whole
         // loop is one single-CTA kernel (k_linear_run_block), same results
         const size_t block_smem = (e->prm.k == 0 ? 2 : 3) * NF * 8;
-        const bool block_run = e->step_kind == PD_STEP_LINEAR && nsteps > 0 && block_smem <= kLinearBlockSmemMax;
+        const bool block_run =
+            !exact && e->step_kind == PD_STEP_LINEAR && nsteps > 0 && block_smem <= kLinearBlockSmemMax;
         // direct FAST steps (k = 0, full field): the whole run is one cooperative
         // launch (k_fast_run) when the plan's kernel can be made co-resident
         static const bool fused_enabled = [] {
             const char* v = std::getenv("PD_FUSED_RUN");
             return !(v && v[0] == '0');
         }();
-        const bool fused_ok = !block_run && fused_enabled && nsteps > 0 && e->step_kind == PD_STEP_DIRECT &&
+        const bool fused_ok = !block_run && !exact && fused_enabled && nsteps > 0 && e->step_kind == PD_STEP_DIRECT &&
                               e->mode == PD_MODE_FAST && !e->fast.big && !e->fast.adi && e->prm.k == 0 && !e->subset;
         if (fused_ok) {
             e->d_spread.alloc((size_t)nsteps * kGuardSpread);
             CUDA_TRY(cudaMemsetAsync(e->d_spread.p, 0, (size_t)nsteps * kGuardSpread * 8, e->stream));
         }
+        if (exact && nsteps > 0) CUDA_TRY(cudaMemsetAsync(err, 0, (size_t)nsteps * 8, e->stream));
         bool fused = false;
         CUDA_TRY(cudaEventRecord(e->ev0, e->stream));
         if (fused_ok) {
@@ -644,6 +651,12 @@ pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps
                 k_guard<<<gblocks, 256, 0, e->stream>>>(nxt, NF, e->d_slot.p, e->d_counter.p, e->d_fail.p,
                                                         e->d_fail.p + 1, n, blowup);
                 e->check_launch();
+                if (exact) {
+                    k_exact_err<<<gblocks, 256, 0, e->stream>>>(e->prm, nxt, exact + NF * n,
+                                                                reinterpret_cast<unsigned long long*>(err),
+                                                                e->d_fail.p, n);
+                    e->check_launch();
+                }
                 std::swap(cur, nxt);
             }
         }
@@ -684,10 +697,28 @@ pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps
     });
     return st != PD_OK ? st : result;
 }
+} // namespace
+
+pd_status pd_run_device(pd_engine* e, double* U, double* scratch, int32_t nsteps, double t0, const double* bnd,
+                        const double* src_time, pd_run_stats* stats) {
+    return run_device_impl(e, U, scratch, nsteps, t0, bnd, src_time, nullptr, nullptr, stats);
+}
+
+pd_status pd_run_device_exact(pd_engine* e, double* U, double* scratch, int32_t nsteps, double t0,
+                              const double* bnd, const double* src_time, const double* exact, double* err,
+                              pd_run_stats* stats) {
+    if (!exact || !err) return PD_VALIDATION_ERROR;
+    return run_device_impl(e, U, scratch, nsteps, t0, bnd, src_time, exact, err, stats);
+}
 
 pd_status pd_run(pd_engine* e, double* U_host, int32_t nsteps, double t0, const double* bnd, const double* src_time,
                  pd_run_stats* stats) {
-    if (!e || !U_host) return PD_VALIDATION_ERROR;
+    return pd_run_exact(e, U_host, nsteps, t0, bnd, src_time, nullptr, nullptr, stats);
+}
+
+pd_status pd_run_exact(pd_engine* e, double* U_host, int32_t nsteps, double t0, const double* bnd,
+                       const double* src_time, const double* exact, double* err_out, pd_run_stats* stats) {
+    if (!e || !U_host || nsteps < 0 || (exact != nullptr) != (err_out != nullptr)) return PD_VALIDATION_ERROR;
     pd_status result = PD_OK;
     const pd_status st = guarded(e, [&] {
         const size_t NF = e->NF;
@@ -706,9 +737,18 @@ pd_status pd_run(pd_engine* e, double* U_host, int32_t nsteps, double t0, const 
             upload(e->d_srct.p, src_time, n * 8, e->stream);
             dsrc = e->d_srct.p;
         }
-        result = pd_run_device(e, e->d_U.p, e->d_U.p + NF, nsteps, t0, dbnd, dsrc, stats);
+        double* dex = nullptr;
+        double* derr = nullptr;
+        if (exact && nsteps > 0) {
+            e->d_exact.alloc(NF * (size_t)nsteps + (size_t)nsteps);
+            dex = e->d_exact.p;
+            derr = dex + NF * (size_t)nsteps;
+            upload(dex, exact, NF * (size_t)nsteps * 8, e->stream);
+        }
+        result = run_device_impl(e, e->d_U.p, e->d_U.p + NF, nsteps, t0, dbnd, dsrc, dex, derr, stats);
         if (result != PD_OK && result != PD_MACRO_INSTABILITY) throw Status{result, e->err};
         download(U_host, e->d_U.p, NF * 8, e->stream);
+        if (derr) download(err_out, derr, (size_t)nsteps * 8, e->stream);
         CUDA_TRY(cudaStreamSynchronize(e->stream));
     });
     return st != PD_OK ? st : result;

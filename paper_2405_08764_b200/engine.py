@@ -67,6 +67,8 @@ def lib() -> C.CDLL:
     L.pd_projective_step_device.argtypes = [vp, vp, vp, C.c_double, vp, vp]
     L.pd_run.argtypes = [vp, _dp, C.c_int32, C.c_double, _dp, _dp, C.POINTER(RunStats)]
     L.pd_run_device.argtypes = [vp, vp, vp, C.c_int32, C.c_double, vp, vp, C.POINTER(RunStats)]
+    L.pd_run_exact.argtypes = [vp, _dp, C.c_int32, C.c_double, _dp, _dp, _dp, _dp, C.POINTER(RunStats)]
+    L.pd_run_device_exact.argtypes = [vp, vp, vp, C.c_int32, C.c_double, vp, vp, vp, vp, C.POINTER(RunStats)]
     L.pd_integrate_batch.argtypes = [vp, _dp, _ip, _dp, _dp, _dp, C.c_double, _dp, _dp]
     L.pd_lift_batch.argtypes = [vp, C.c_int32, _dp, _dp, _dp, _dp, _dp]
     L.pd_restrict_batch.argtypes = [vp, C.c_int32, _dp, _dp]
@@ -302,6 +304,23 @@ class Engine:
         if st != abi.PD_MACRO_INSTABILITY or raise_on_instability:
             _check(st, self.h)
         return U, stats
+
+    def run_exact(self, U0, nsteps, exact, t0=0.0, bnd=None, src_time=None, raise_on_instability=True):
+        """run() plus cpi::run's per-step exact-error metric on the device
+        (max_percent_error, cpi.cpp:79-94): exact [nsteps][Nxi+1][Neta+1] at the
+        end of every step; returns (U, stats, err[nsteps])."""
+        U = np.array(U0, dtype=np.float64, copy=True, order="C")
+        b = None if bnd is None else np.ascontiguousarray(bnd, dtype=np.float64)
+        s = None if src_time is None else np.ascontiguousarray(src_time, dtype=np.float64)
+        ex = np.ascontiguousarray(exact, dtype=np.float64)
+        if ex.shape != (nsteps,) + U.shape:
+            raise ValueError(f"exact table shape {ex.shape} != {(nsteps,) + U.shape}")
+        err = np.zeros(nsteps)
+        stats = RunStats()
+        st = lib().pd_run_exact(self.h, _d(U), nsteps, t0, _d(b), _d(s), _d(ex), _d(err), C.byref(stats))
+        if st != abi.PD_MACRO_INSTABILITY or raise_on_instability:
+            _check(st, self.h)
+        return U, stats, err
 
     # ---- device-resident entries (pointers are raw device addresses) ----
     def projective_step_device(self, in_ptr: int, out_ptr: int, t: float = 0.0):

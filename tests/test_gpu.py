@@ -51,6 +51,59 @@ def test_full_run_vs_reference(name, mode, gpu):
         assert rel(UT, FINALS[f"{name}_final"]) < TOL
 
 
+@pytest.mark.parametrize("name", ["c1_diffusion", "c2_cdr_tanh"])
+@pytest.mark.parametrize("mode", [EXACT, FAST], ids=["exact", "fast"])
+def test_run_exact_error_metric_vs_reference(name, mode, gpu):
+    """cpi::run's per-step max_percent_error (cpi.cpp:79-94, 204-209) computed on
+    the device inside the run (pd_run_exact): EXACT reproduces the reference's
+    RunResult::max_pct_err bit for bit, and every step's value equals the host
+    formula on that step's field."""
+    P = load(name)
+    E = Engine.from_problem(P, mode=mode)
+    U0, Nt = P.initial_field(), P.desc.Nt
+    dt = P.desc.T / Nt
+    ex = np.stack([P.exact((n + 1) * dt) for n in range(Nt)])
+    bt = P.boundary_table(0.0, Nt)
+    UT, stats, err = E.run_exact(U0, Nt, ex, bnd=bt)
+    assert stats.steps_done == Nt and err.shape == (Nt,)
+    assert stats.kernel_launches == 4 * Nt  # step, refresh, guard, error: no host round trip
+    if mode == EXACT:
+        assert np.array_equal(UT, FINALS[f"{name}_final"])
+        assert err.max() == float(FINALS[f"{name}_maxpct"])
+    else:
+        assert rel(UT, FINALS[f"{name}_final"]) < TOL
+        assert err.max() == pytest.approx(float(FINALS[f"{name}_maxpct"]), rel=1e-6)
+    # per step: the reference's loop on the field after that step
+    d = P.engine_desc()
+    i_lo = 0 if d.periodic_xi else 1
+    U = U0
+    for n in range(4):
+        U, _ = E.run(U, 1, t0=n * dt, bnd=bt[n:n + 1])
+        e = ex[n][i_lo:-1, 1:-1]
+        Ui = U[i_lo:-1, 1:-1]
+        m = np.abs(e) >= 1e-12
+        host = (np.abs(Ui - e)[m] / np.abs(e)[m] * 100.0).max() if m.any() else 0.0
+        assert err[n] == host, n
+
+
+def test_run_exact_error_metric_stops_at_guard(gpu):
+    """the unstable setup of test_macro_instability_guard: no error is recorded
+    for the failing step or after it (cpi::run throws before measuring)"""
+    d = configs.default_desc()
+    d.problem = abi.PD_PROBLEM_REF_ANNULUS
+    d.N_xi, d.N_eta, d.Nt, d.T, d.tau = 16, 10, 5, 1.0, 1e-6
+    d.h_xi = d.h_eta = 1e-3
+    d.nx = d.ny = 10
+    d.nt = 400
+    P = Problem(d)
+    E = Engine.from_problem(P, mode=EXACT)
+    U0 = P.initial_field()
+    ex = np.ones((5,) + U0.shape)
+    _, stats, err = E.run_exact(U0, 5, ex, bnd=P.boundary_table(0.0, 5), raise_on_instability=False)
+    assert stats.failed_step >= 1
+    assert np.all(err[:stats.failed_step - 1] > 0.0) and np.all(err[stats.failed_step - 1:] == 0.0)
+
+
 def test_engine_index_tables_are_the_host_tables(gpu):
     for name in ["c1_diffusion", "c3_annulus"]:
         P = load(name)
