@@ -603,7 +603,8 @@ __global__ void __launch_bounds__(32 * kRunWarps, run_min_blocks<Cfg>() / kRunWa
 k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int* __restrict__ nbr,
            const double* __restrict__ Wt, int nunits, const double* __restrict__ bnd, size_t bnd_stride,
            const double* __restrict__ srct, size_t srct_stride, int nsteps, double blowup,
-           unsigned long long* __restrict__ slot, unsigned long long* __restrict__ spread, int* __restrict__ fail) {
+           unsigned long long* __restrict__ slot, unsigned long long* __restrict__ spread, int* __restrict__ fail,
+           const double* __restrict__ exact, unsigned long long* __restrict__ err) {
     constexpr int G = Cfg::G, LP = Cfg::LP, L = Cfg::L;
     __shared__ double s_g[kRunWarps][G][8][L];
     __shared__ double s_red[kRunWarps][32];
@@ -659,6 +660,20 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
         if (n > 0 && guard_trips(pend, n - 1, gw, lane, blowup, slot, fail)) return;
         grid.sync();
         pend = __ldcg(spread + (size_t)n * kGuardSpread + lane);
+        if (exact) { // cpi::run's max_percent_error of step n (k_exact_err's arithmetic) over the patch nodes
+            const double* ex = exact + (size_t)n * (p.Nxi + 1) * p.NF2;
+            unsigned long long em = 0;
+            for (int q = gw * 32 + lane; q < p.P; q += nw * 32) {
+                const int node = __ldg(nbr + 9 * q + 4);
+                const double e = ex[node];
+                if (fabs(e) < 1e-12) continue;
+                const double pct = __dmul_rn(__ddiv_rn(fabs(__dsub_rn(__ldcg(out + node), e)), fabs(e)), 100.0);
+                em = max(em, (unsigned long long)__double_as_longlong(pct));
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) em = max(em, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)em, o));
+            if (lane == 0 && em) atomicMax(err + n, em);
+        }
     }
     if (nsteps > 0) guard_trips(pend, nsteps - 1, gw, lane, blowup, slot, fail);
 }
@@ -770,7 +785,8 @@ inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, 
 inline bool launch_fast_run(const FastPlan& plan, const Params& p, double* UA, double* UB, const int* nbr,
                             const double* W, const double* bnd, size_t bnd_stride, const double* srct,
                             size_t srct_stride, int nsteps, double blowup, unsigned long long* slot,
-                            unsigned long long* spread, int* fail, cudaStream_t s) {
+                            unsigned long long* spread, int* fail, cudaStream_t s, const double* exact = nullptr,
+                            double* err = nullptr) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -786,7 +802,8 @@ inline bool launch_fast_run(const FastPlan& plan, const Params& p, double* UA, d
         if (per_sm > 0 && blocks <= per_sm * sms) {                                                            \
             Params pp = p;                                                                                     \
             void* args[] = {&pp, &UA, &UB, (void*)&nbr, (void*)&W, &nunits, (void*)&bnd, &bnd_stride,          \
-                            (void*)&srct, &srct_stride, &nsteps, &blowup, &slot, &spread, &fail};              \
+                            (void*)&srct, &srct_stride, &nsteps, &blowup, &slot, &spread, &fail,               \
+                            (void*)&exact, (void*)&err};                                                       \
             launched = cudaLaunchCooperativeKernel((const void*)k_fast_run<CFG>, dim3(blocks),                 \
                                                    dim3(32 * kRunWarps), args, 0, s) == cudaSuccess;           \
             if (!launched) {                                                                                   \

@@ -579,9 +579,9 @@ pd_status pd_projective_step(pd_engine* e, const double* U_in, double* U_out, do
 }
 
 namespace {
-// exact/err (device, optional): the per-step exact-error metric (k_exact_err)
-// after every step's guard; it needs the field of every step, so it takes the
-// multi-launch loop (still no host round trip inside the run)
+// exact/err (device, optional): the per-step exact-error metric after every
+// step — inside the single-launch run (k_fast_run) when that runs, else one
+// k_exact_err launch per step; no host round trip either way
 pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nsteps, double t0, const double* bnd,
                           const double* src_time, const double* exact, double* err, pd_run_stats* stats) {
     if (!e || !U || !scratch || nsteps < 0 || (exact != nullptr) != (err != nullptr)) return PD_VALIDATION_ERROR;
@@ -620,7 +620,7 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
             const char* v = std::getenv("PD_FUSED_RUN");
             return !(v && v[0] == '0');
         }();
-        const bool fused_ok = !block_run && !exact && fused_enabled && nsteps > 0 && e->step_kind == PD_STEP_DIRECT &&
+        const bool fused_ok = !block_run && fused_enabled && nsteps > 0 && e->step_kind == PD_STEP_DIRECT &&
                               e->mode == PD_MODE_FAST && !e->fast.big && !e->fast.adi && e->prm.k == 0 && !e->subset;
         if (fused_ok) {
             e->d_spread.alloc((size_t)nsteps * kGuardSpread);
@@ -632,7 +632,7 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         if (fused_ok) {
             fused = launch_fast_run(e->fast, e->prm, U, scratch, e->d_nbr.p, e->d_weights.p,
                                     bnd ? bnd + e->perim : nullptr, pk, (src_time && e->prm.source) ? src_time : nullptr,
-                                    sk, nsteps, blowup, e->d_slot.p, e->d_spread.p, e->d_fail.p, e->stream);
+                                    sk, nsteps, blowup, e->d_slot.p, e->d_spread.p, e->d_fail.p, e->stream, exact, err);
             if (fused) e->check_launch();
         }
         if (fused) {
@@ -670,6 +670,10 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         CUDA_TRY(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
         // the field after the last executed step lives in buffer (done % 2 == 1 ? scratch : U)
         const int done = fail[0] ? fail[0] : nsteps;
+        // the single-launch run measures a step before its (one step late) guard
+        // decision: no error for the failing step or after it, as cpi::run
+        if (exact && fail[0] && fail[0] <= nsteps)
+            CUDA_TRY(cudaMemsetAsync(err + (fail[0] - 1), 0, (size_t)(nsteps - fail[0] + 1) * 8, e->stream));
         if (!block_run && done % 2 == 1)
             CUDA_TRY(cudaMemcpyAsync(U, scratch, NF * 8, cudaMemcpyDeviceToDevice, e->stream));
         CUDA_TRY(cudaStreamSynchronize(e->stream));

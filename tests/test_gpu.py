@@ -66,7 +66,9 @@ def test_run_exact_error_metric_vs_reference(name, mode, gpu):
     bt = P.boundary_table(0.0, Nt)
     UT, stats, err = E.run_exact(U0, Nt, ex, bnd=bt)
     assert stats.steps_done == Nt and err.shape == (Nt,)
-    assert stats.kernel_launches == 4 * Nt  # step, refresh, guard, error: no host round trip
+    # FAST: still the single-launch run (k_fast_run measures after each grid barrier);
+    # EXACT: step, refresh, guard, error per step — no host round trip either way
+    assert stats.kernel_launches == (1 if mode == FAST else 4 * Nt)
     if mode == EXACT:
         assert np.array_equal(UT, FINALS[f"{name}_final"])
         assert err.max() == float(FINALS[f"{name}_maxpct"])
@@ -102,6 +104,10 @@ def test_run_exact_error_metric_stops_at_guard(gpu):
     _, stats, err = E.run_exact(U0, 5, ex, bnd=P.boundary_table(0.0, 5), raise_on_instability=False)
     assert stats.failed_step >= 1
     assert np.all(err[:stats.failed_step - 1] > 0.0) and np.all(err[stats.failed_step - 1:] == 0.0)
+    F = Engine.from_problem(P, mode=FAST)  # the single-launch run measures before its late guard decision
+    _, sf, ef = F.run_exact(U0, 5, ex, bnd=P.boundary_table(0.0, 5), raise_on_instability=False)
+    assert sf.kernel_launches == 1 and sf.failed_step == stats.failed_step
+    assert np.all(ef[:sf.failed_step - 1] > 0.0) and np.all(ef[sf.failed_step - 1:] == 0.0)
 
 
 def test_engine_index_tables_are_the_host_tables(gpu):
