@@ -155,28 +155,52 @@ __global__ void k_adi_fast_fold(Params p, const double* __restrict__ coeffs, con
     }
 }
 
-inline size_t fast_adi_smem_bytes(const Params& p) {
-    const size_t tile = (size_t)(p.n1 + 4) * (p.n2 + 4);
-    return sizeof(double) * kFastAdiWarps * (2 * tile + 4 * (size_t)p.L + 32);
+// A set's table is staged in shared memory by one bulk copy per patch (the
+// serial line substitutions then read it at shared-memory latency) when it is
+// at most this large and its size keeps 16-byte alignment; else read from global.
+constexpr size_t kAdiStageMax = 24 * 1024;
+__host__ __device__ inline bool adi_fast_staged(const Params& p) {
+    const size_t t = adi_fast_doubles(p);
+    return t % 2 == 0 && t * sizeof(double) <= kAdiStageMax;
 }
+// per-warp shared region in doubles: tiles A, Bt | gb [4][L] | red [32] | mbarrier (2) | staged table
+__host__ __device__ inline size_t fast_adi_warp_doubles(const Params& p) {
+    const size_t tile = (size_t)(p.n1 + 4) * (p.n2 + 4);
+    const size_t base = 2 * tile + 4 * (size_t)p.L + 32 + 2;
+    return base + (adi_fast_staged(p) ? adi_fast_doubles(p) : 0);
+}
+inline size_t fast_adi_smem_bytes(const Params& p) { return sizeof(double) * kFastAdiWarps * fast_adi_warp_doubles(p); }
 
 // The fused step with the FAST ADI micro-solver, one warp per patch.
+// STAGED (adi_fast_staged): the set's table is read from shared memory; else
+// through the read-only global path (a template so neither variant reads
+// through a generic pointer)
+template <bool STAGED>
 __global__ void __launch_bounds__(32 * kFastAdiWarps, 4)
 k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode, const int* __restrict__ nbr,
            const int* __restrict__ cset, const double* __restrict__ tab, const double* __restrict__ srct,
            const int* __restrict__ fail_flag) {
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
     if (fail_flag && *fail_flag) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int patch = blockIdx.x * kFastAdiWarps + warp;
     if (patch >= p.P) return; // warp-uniform
     const int n1 = p.n1, n2 = p.n2, nx = p.nx, ny = p.ny, L = p.L, TS = n2 + 4;
     const size_t tile = (size_t)(n1 + 4) * TS;
-    double* A = sm + (size_t)warp * (2 * tile + 4 * L + 32);
+    double* A = sm + (size_t)warp * fast_adi_warp_doubles(p);
     double* Bt = A + tile;
     double* gb = Bt + tile;     // [4][L] ghost offsets b, or pinned values on pinned edges
     double* red = gb + 4 * L;   // [32]
     auto at = [TS](int i, int j) { return (i + 2) * TS + (j + 2); };
+    // the set's static table streams into shared memory behind the gather, slopes and lift
+    const int set = cset ? cset[patch] : patch;
+    const AdiFastLayout lay = adi_fast_layout(p);
+    double* stage = red + 32 + 2;
+    const unsigned bar = smem_u32(red + 32);
+    if (STAGED && lane == 0) {
+        mbar_init(bar, 1);
+        bulk_load(smem_u32(stage), tab + (size_t)set * lay.total, (unsigned)(lay.total * sizeof(double)), bar);
+    }
 
     double v[9];
 #pragma unroll
@@ -234,9 +258,16 @@ k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int
     }
     __syncwarp();
 
-    const int set = cset ? cset[patch] : patch;
-    const AdiFastLayout lay = adi_fast_layout(p);
-    const double* S0 = tab + (size_t)set * lay.total;
+    const double* S0;
+    if constexpr (STAGED) {
+        __syncwarp();
+        mbar_wait(bar, 0);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+        S0 = stage;
+    } else {
+        S0 = tab + (size_t)set * lay.total;
+    }
     const bool banded = lay.KC == 10;
     const bool pin = p.pinned != 0;
     const double* srcw = p.source == PD_SOURCE_SEPARABLE ? S0 + lay.src : nullptr;
