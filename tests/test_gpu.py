@@ -6,6 +6,8 @@ be within the north_star tolerance: 1e-11 relative max-norm after the full run.
 The checkers are the committed reference fixtures (tests/golden) and the CPU
 oracle; nothing here reads /root/reference.
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -915,3 +917,46 @@ def test_fused_run_equals_stepwise_launches(name, gpu):
         U = E.projective_step(U, s * dt, bnd=bt[s])
     assert np.array_equal(Ug, U)
     assert stats.umax_last == np.abs(U).max()
+
+
+# ---------------------------------------------------------------------------
+# edge cases: the smallest grid, ragged warp units, empty runs
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,N", [("c1_diffusion", 2), ("c1_diffusion", 4), ("c2_cdr_tanh", 3),
+                                    ("c4_shear", 2), ("c4_shear", 4)],
+                         ids=["c1-1patch", "c1-9patches", "c2-4patches", "c4-1patch", "c4-9patches"])
+def test_smallest_and_ragged_grids_vs_oracle(name, N, restated, gpu):
+    """One patch, and patch counts that leave the last warp unit ragged (7x7
+    tiles hold four patches per warp, 9x9 three, 16x16 one): EXACT bit-exact,
+    FAST within 1e-11 of the restated reference after a short run."""
+    P = load(name, N_xi=N, N_eta=N)
+    n = 5
+    U0 = P.initial_field()
+    bt = P.boundary_table(0.0, n)
+    st, Uo, so = restated.run(P.engine_desc(), U0, n, bnd=bt)
+    assert st == abi.PD_OK
+    Ue, se = Engine.from_problem(P, mode=EXACT).run(U0, n, bnd=bt)
+    assert np.array_equal(Ue, Uo)
+    F = Engine.from_problem(P, mode=FAST)
+    assert F.mode == FAST
+    Uf, sf = F.run(U0, n, bnd=bt)
+    assert rel(Uf, Uo) < TOL and sf.steps_done == n
+
+
+def test_empty_run_and_argument_checks(gpu):
+    P = load("c1_diffusion")
+    E = Engine.from_problem(P, mode=FAST)
+    U0 = P.initial_field()
+    U, st = E.run(U0, 0)
+    assert np.array_equal(U, U0) and st.steps_done == 0 and st.failed_step == 0
+    U, st, err = E.run_exact(U0, 0, np.zeros((0,) + U0.shape))
+    assert np.array_equal(U, U0) and err.shape == (0,)
+    with pytest.raises(ValueError):
+        E.run_exact(U0, 3, np.zeros((2,) + U0.shape))  # one exact field per step
+    # the C-ABI validates its pointers: exact without err (or the reverse) is rejected
+    from paper_2405_08764_b200.engine import lib
+    Uc = np.array(U0)
+    ex = np.zeros((1,) + U0.shape)
+    st = lib().pd_run_exact(E.h, Uc.ctypes.data_as(C.POINTER(C.c_double)), 1, 0.0, None, None,
+                            ex.ctypes.data_as(C.POINTER(C.c_double)), None, None)
+    assert st == abi.PD_VALIDATION_ERROR
