@@ -777,11 +777,28 @@ inline void launch_fast(const FastPlan& plan, const Params& p, const double* F, 
 #undef PD_LAUNCH
 }
 
-// Cooperative whole-run launch; returns false (nothing launched) unless every
-// unit gets its own co-resident warp.  The run kernel carries more live state
-// than k_fast (about 220 registers instead of 168: 9 instead of 12 warps/SM),
-// so it is used where per-step launch latency dominates (configs 1-3, small
-// sweep points), not where the step is throughput-bound.
+// Cooperative whole-run launch (at most one block per co-resident slot);
+// returns false (nothing launched) when the units exceed run_waves() per
+// co-resident warp.  The run kernel carries more live state than k_fast (about
+// 220 registers instead of 168: 8-9 instead of 12 warps/SM), so it is used
+// where per-step launch latency dominates (configs 1-3, small sweep points),
+// not where the step is throughput-bound.
+// The run kernel's warps stride over the units.  Measured (config-5 shapes,
+// 20-step runs): with at most two units per co-resident warp the single launch
+// wins at every K (8x8, 2^13 patches: 22.7 -> 14.1 us per step at K = 10,
+// 102.3 -> 99.7 at K = 200); with more it wins only while a step is short
+// (<= 2.5e7 node updates: 16x16 2^12 at K = 10 26.7 -> 20.8 us, 8x8 2^15
+// 46.8 -> 42.4) and loses beyond (the run kernel's lower occupancy: 16x16 2^12
+// at K = 200 165 -> 196 us).  PD_RUN_WAVES overrides for A/B runs.
+inline int run_waves(const Params& p) {
+    static const int forced = [] {
+        const char* e = std::getenv("PD_RUN_WAVES");
+        return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    if (forced) return forced;
+    const double updates = (double)p.P * p.n1 * p.n2 * p.nt;
+    return updates <= 2.5e7 ? 8 : 2;
+}
 inline bool launch_fast_run(const FastPlan& plan, const Params& p, double* UA, double* UB, const int* nbr,
                             const double* W, const double* bnd, size_t bnd_stride, const double* srct,
                             size_t srct_stride, int nsteps, double blowup, unsigned long long* slot,
@@ -799,12 +816,13 @@ inline bool launch_fast_run(const FastPlan& plan, const Params& p, double* UA, d
         const int blocks = (nunits + kRunWarps - 1) / kRunWarps;                                               \
         if (std::getenv("PD_DEBUG_RUN"))                                                                       \
             fprintf(stderr, "k_fast_run plan %d: %d blocks, %d per SM x %d SMs\n", ID, blocks, per_sm, sms);     \
-        if (per_sm > 0 && blocks <= per_sm * sms) {                                                            \
+        if (per_sm > 0 && blocks <= run_waves(p) * per_sm * sms) {                                              \
             Params pp = p;                                                                                     \
             void* args[] = {&pp, &UA, &UB, (void*)&nbr, (void*)&W, &nunits, (void*)&bnd, &bnd_stride,          \
                             (void*)&srct, &srct_stride, &nsteps, &blowup, &slot, &spread, &fail,               \
                             (void*)&exact, (void*)&err};                                                       \
-            launched = cudaLaunchCooperativeKernel((const void*)k_fast_run<CFG>, dim3(blocks),                 \
+            const int grid = std::min(blocks, per_sm * sms); /* warps stride over the units */                 \
+            launched = cudaLaunchCooperativeKernel((const void*)k_fast_run<CFG>, dim3(grid),                   \
                                                    dim3(32 * kRunWarps), args, 0, s) == cudaSuccess;           \
             if (!launched) {                                                                                   \
                 const cudaError_t e_ = cudaGetLastError(); /* the multi-launch loop runs instead */            \
