@@ -237,7 +237,9 @@ def run_sweep(args):
                 steps = max(3, min(20, int(2e11 // (P * N * K)) or 3))
                 torch.cuda.synchronize()
                 st = eng.run_device(dU.data_ptr(), dS.data_ptr(), steps)
-                kms = eng.bench_step_kernel(dU.data_ptr(), dS.data_ptr(), reps=3)
+                # kernel-only time: best of three 3-launch averages (one noisy sample
+                # otherwise moves a point's fraction by 0.1)
+                kms = min(eng.bench_step_kernel(dU.data_ptr(), dS.data_ptr(), reps=3) for _ in range(3))
                 upd = P * N * K
                 flops, byts = upd * 14, P * (N * 48 + 16)
                 t_fp, t_bw = flops / (p64 * 1e12), byts / (bw * 1e9)
