@@ -172,6 +172,12 @@ void pd_engine_destroy(pd_engine* engine);
 /* Kernel family actually used by the engine (FAST may fall back to EXACT for
  * shapes or features the fast kernel does not cover; never to a CPU path). */
 int32_t pd_engine_mode(const pd_engine* engine);
+/* 1 when the engine's coefficient table carries the mixed term (some |b| > 1e-12,
+ * the 9-point operator; microsim.cpp:239), 0 for the 5-point operator, -1 for NULL. */
+int32_t pd_engine_mixed(const pd_engine* engine);
+/* Kernels the engine has launched since it was created (every entry point
+ * counts its own launches; pd_run_stats.kernel_launches is the per-call share). */
+int64_t pd_engine_launch_count(const pd_engine* engine);
 /* Bit-exact index tables built by the engine: patch_ij [P][2] and the 3x3
  * neighbour table [P][9] of flat macro indices i*(Neta+1)+j, stencil order
  * vals[p+1][q+1] with p along xi (gaptooth.cpp:74-104).  Either may be NULL. */
@@ -276,6 +282,16 @@ pd_status pd_linear_weights(pd_engine* e, double* row_w_host);
 pd_status pd_engine_set_linear(pd_engine* e, const double* row_w_host);
 pd_status pd_engine_set_step_kind(pd_engine* e, int32_t kind);
 int32_t pd_engine_step_kind(const pd_engine* e);
+
+/* Segmented cpi::run (cpi.cpp:134-216 split around probes / snapshots /
+ * progress callbacks): the blow-up threshold is 10 x max(scale0, 1e-12) with
+ * scale0 = max|U| of the RUN's initial field after refresh_boundary
+ * (cpi.cpp:142-144), not of each segment's input.  With scale0 > 0 every later
+ * pd_run* call uses it (scale0 <= 0: measure the call's own input, the
+ * default); step_offset = macro steps already done, so the instability message
+ * names the run's step and time ("macro step n (t=...)", cpi.cpp:196-200).
+ * pd_run_stats.failed_step stays relative to the call. */
+pd_status pd_engine_set_run_guard(pd_engine* e, double scale0, int32_t step_offset);
 
 /* ---------------------------------------------------------------------------
  * Host problem builder: the B200 framework's own mesh/metric setup for the

@@ -65,6 +65,13 @@ int pdo_run(const pd_engine_desc* d, double* U, int nsteps, double t0, const dou
 double pdo_patch_subset(const pd_engine_desc* d, const double* U_in, double t, int nsub,
                         const int* patch_index, double* avg_out);
 
+/* Input builder for the shear-cdr family (configs 4/5) without the product
+ * library (pd_oracle_problem.c): resolves d's pins in place and fills the
+ * seeded initial field U0 [(N_xi+1)(N_eta+1)], the patch list [P][2] and the
+ * solver-form coefficient table [P][6][nx+1][ny+1].  Returns a pd_status. */
+int pdo_shear_problem(pd_problem_desc* d, double* U0, int32_t* patch_ij, double* coeffs);
+void pdo_seeded_field(int Nxi, int Neta, uint64_t seed, int sweeps, double* U);
+
 /* Linear-response path (GapToothEngine::step with linear_cache, gaptooth.cpp:377-418).
  * evolve_batch: evolve_patch for n given stencils [n][3][3] (vals[p+1][q+1]) with patch
  * patch_index[m]'s integrator and centre.  linear_weights: build_row_weights,

@@ -68,6 +68,8 @@ class Restated:
         L.pdo_linear_step.argtypes = [desc_p, _dp, _dp, _dp, _dp]
         L.pdo_linear_projective_step.argtypes = [desc_p, _dp, _dp, _dp, C.c_double, _dp]
         L.pdo_linear_run.argtypes = [desc_p, _dp, _dp, C.c_int, C.c_double, _dp, C.POINTER(RunStats)]
+        L.pdo_shear_problem.argtypes = [C.POINTER(ProblemDesc), _dp, _ip, _dp]
+        L.pdo_seeded_field.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, _dp]
         if threads is not None:
             L.pdo_set_threads(int(threads))
 
@@ -157,6 +159,22 @@ class Restated:
         r = self.lib.pdo_linear_run(C.byref(desc), _d(w), _d(U), nsteps, t0, _d(bnd), C.byref(stats))
         return r, U, stats
 
+    def shear_problem(self, pdesc: ProblemDesc, mode: int = 1):
+        """Configs 4/5 built by the oracle alone (pd_oracle_problem.c): the
+        resolved problem description, an engine descriptor over oracle-owned
+        tables and the seeded initial field — no product library involved."""
+        r = ProblemDesc.from_buffer_copy(pdesc)
+        n1, n2 = r.nx + 1, r.ny + 1
+        P = (r.N_xi - 1) * (r.N_eta - 1)
+        U0 = np.empty((r.N_xi + 1, r.N_eta + 1))
+        pij = np.empty((P, 2), dtype=np.int32)
+        coeffs = np.empty((P, 6, n1, n2))
+        st = self.lib.pdo_shear_problem(C.byref(r), _d(U0), _i(pij), _d(coeffs))
+        if st:
+            raise RuntimeError(f"oracle shear problem: status {st}")
+        ed = engine_desc_from_tables(r, False, (0.0, 1.0, 0.0, 1.0), pij, coeffs, mode=mode)
+        return r, ed, U0
+
     def patch_subset(self, desc: EngineDesc, U, t, patch_index):
         U = np.ascontiguousarray(U, dtype=np.float64)
         idx = np.ascontiguousarray(patch_index, dtype=np.int32)
@@ -202,6 +220,7 @@ class Reference:
                                C.c_double, C.c_int, C.c_int, _dp, _dp, _dp]
         L.ref_restrict.argtypes = [_dp, C.c_int, C.c_int, C.c_int]
         L.ref_restrict.restype = C.c_double
+        L.ref_problem_domain.argtypes = [pd, _dp, _ip]
 
     def error(self) -> str:
         return self.lib.ref_last_error().decode()
@@ -334,6 +353,48 @@ class RefEngine:
         return out
 
 
+def ref_problem_desc(desc: ProblemDesc) -> ProblemDesc:
+    """Resolve a config's pins without the product library,
+    as pd_problem_create does: h = h_frac * Delta over the reference's own
+    domain, dt = 0.2 min(delta)^2 / eps (diffusion rule) or / max(|A| + |C|)
+    over the reference's own coefficient sampling (metric rule), tau = nt dt,
+    T = Nt (Dt/tau) tau.  tests/test_oracle.py pins it against the product."""
+    ref = Reference()
+    L = ref.lib
+    r = ProblemDesc.from_buffer_copy(desc)
+    dom = np.zeros(4)
+    flags = np.zeros(2, dtype=np.int32)
+    st = L.ref_problem_domain(C.byref(r), _d(dom), _i(flags))
+    if st:
+        raise RuntimeError(f"reference problem: {st}: {ref.error()}")
+    a, b, c, d = (float(x) for x in dom)
+    if r.h_frac > 0.0:
+        r.h_xi = r.h_frac * ((b - a) / r.N_xi)
+        r.h_eta = r.h_frac * ((d - c) / r.N_eta)
+    if r.dt_rule != 0 and not r.tau > 0:
+        r.tau = 1.0  # placeholder: node coordinates do not depend on it
+    if r.dt_over_tau > 0 and not r.T > 0:
+        r.T = 1.0
+    dmin = min(r.h_xi / r.nx, r.h_eta / r.ny)
+    if r.dt_rule == 1:  # PD_DT_DIFFUSION
+        r.tau = r.nt * (0.2 * dmin * dmin / r.eps)
+    elif r.dt_rule == 2:  # PD_DT_METRIC
+        pij = reference_patch_order(r.N_xi, r.N_eta, bool(flags[0]))
+        if flags[1]:  # one integrator per eta-row (gaptooth.cpp:254-266): its first patch
+            pij = pij[pij[:, 0] == pij[0, 0]]
+        m = 0.0
+        for q in range(0, len(pij), 4096):
+            co = ref.sample_coeffs(r, pij[q:q + 4096])
+            m = max(m, float((np.abs(co[:, 0]) + np.abs(co[:, 2])).max()))
+        r.tau = r.nt * (0.2 * dmin * dmin / m)
+    if r.dt_over_tau > 0:
+        r.T = r.Nt * (r.dt_over_tau * r.tau)
+    r.dt_rule = 0
+    r.h_frac = 0.0
+    r.dt_over_tau = 0.0
+    return r
+
+
 def reference_patch_order(Nxi, Neta, periodic):
     """Patch order of the GapToothEngine ctor (gaptooth.cpp:251-280)."""
     i_lo = 0 if periodic else 1
@@ -367,5 +428,5 @@ def engine_desc_from_tables(pdesc: ProblemDesc, periodic: bool, dom, patch_ij, c
     return d
 
 
-__all__ = ["Restated", "Reference", "reference_available", "reference_patch_order",
+__all__ = ["Restated", "Reference", "reference_available", "reference_patch_order", "ref_problem_desc",
            "engine_desc_from_tables", "perimeter_len", "build_restated"]

@@ -261,6 +261,26 @@ int ref_sample_coeffs_desc(const pd_problem_desc* d, int npatch, const int* patc
     }
 }
 
+// The problem's computational domain, xi-periodicity and row sharing (ProblemSpec
+// a, b, c, d, periodic_xi, structure hints; problems.hpp:17-41): what the pin
+// resolution (h = h_frac * Delta, the metric dt rule) needs.  flags[2].
+int ref_problem_domain(const pd_problem_desc* d, double* abcd, int* periodic) {
+    try {
+        const refshim::Built b = refshim::build(*d);
+        abcd[0] = b.spec.a;
+        abcd[1] = b.spec.b;
+        abcd[2] = b.spec.c;
+        abcd[3] = b.spec.d;
+        // periodic_xi, and whether the engine shares one integrator per eta-row
+        // (gaptooth.cpp:254-266: time- and xi-independent coefficients, no source)
+        periodic[0] = b.spec.periodic_xi ? 1 : 0;
+        periodic[1] = b.spec.coeffs_time_independent && b.spec.coeffs_xi_independent && b.spec.source_zero;
+        return 0;
+    } catch (const std::exception& e) {
+        return map_exception(e);
+    }
+}
+
 // Neighbour indices through the reference's build_stencil (gaptooth.cpp:74-104):
 // the field holds each node's flat index, so the gathered values ARE the indices.
 int ref_neighbours(void* h, int npatch, const int* patch_ij, int* out) {

@@ -303,6 +303,9 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
     const size_t NF = static_cast<size_t>(g.Nxi + 1) * (g.Neta + 1);
     const int i_lo = U.periodic_xi() ? 0 : 1;
     const int chunk = per_step ? 1 : cfg.Nt;
+    // one blow-up scale for the whole run (cpi.cpp:142-144), whatever the segmentation
+    double scale0 = 0.0;
+    for (double v : U.U.raw()) scale0 = std::max(scale0, std::abs(v));
     const int k = cfg.k;
     const size_t L = pd_perimeter_len(cfg.N_xi, cfg.N_eta);
     for (int n = 0; n < cfg.Nt; n += chunk) {
@@ -336,6 +339,7 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
         }
         pd_run_stats st{};
         engine.select_default_step(); // projective_step -> engine.step  cpi.cpp:65
+        throw_status(pd_engine_set_run_guard(engine.device(), std::max(scale0, 1e-12), n), engine.device());
         const int rc = pd_run_exact(engine.device(), U.U.data(), m, n * dt, bnd.data(),
                                     src.empty() ? nullptr : src.data(), has_exact ? exact.data() : nullptr,
                                     has_exact ? err.data() : nullptr, &st);
@@ -356,6 +360,7 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
         if (opts.progress_every > 0 && opts.progress && (n + m) % opts.progress_every == 0)
             opts.progress(n + m, t1, res.max_pct_err);
     }
+    throw_status(pd_engine_set_run_guard(engine.device(), 0.0, 0), engine.device());
     res.final_field = std::move(U);
     return res;
 }

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -67,6 +68,19 @@ struct DevBuf {
     ~DevBuf() { free(); }
 };
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function and process-wide:
+// engines of different sizes share it, so it only ever grows (an engine created
+// later with a smaller need must not lower it under a live larger one).
+std::mutex g_attr_mutex;
+void raise_dyn_smem(const void* func, size_t bytes) {
+    if (bytes <= 48 * 1024) return;
+    std::lock_guard<std::mutex> lock(g_attr_mutex);
+    cudaFuncAttributes a{};
+    CUDA_TRY(cudaFuncGetAttributes(&a, func));
+    if ((size_t)a.maxDynamicSharedSizeBytes >= bytes) return;
+    CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
 } // namespace
 
 constexpr size_t kLinearBlockSmemMax = 220 * 1024; // dynamic shared memory of k_linear_run_block
@@ -88,6 +102,9 @@ struct pd_engine {
     double coeffgen_ms = 0.0;           // on-device table generation time at create (0: host tables)
     int step_kind = PD_STEP_DIRECT;     // what one gap-tooth step means (micro-solve or linear response)
     bool subset = false;                // the patch list covers only part of the interior
+    int adi_carveout = -1;              // k_fast_adi<false> shared-memory carve-out (percent), -1: default
+    double guard_scale = 0.0;           // > 0: blow-up scale of a segmented run (pd_engine_set_run_guard)
+    int32_t step_offset = 0;            // macro steps before this segment, for the instability message
     DevBuf<unsigned long long> d_slot, d_spread;
     DevBuf<unsigned int> d_counter;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -113,6 +130,11 @@ struct pd_engine {
             k_linear_step<<<(prm.P + 127) / 128, 128, 0, stream>>>(prm, F, out, out_mode, d_pij.p, d_roww.p, fail);
         } else if (mode == PD_MODE_FAST && fast.adi) {
             auto* kern = adi_fast_staged(prm) ? k_fast_adi<true> : k_fast_adi<false>;
+            if (adi_carveout >= 0) {
+                std::lock_guard<std::mutex> lock(g_attr_mutex);
+                CUDA_TRY(cudaFuncSetAttribute(k_fast_adi<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              adi_carveout));
+            }
             kern<<<(prm.P + kFastAdiWarps - 1) / kFastAdiWarps, 32 * kFastAdiWarps, fast_adi_smem_bytes(prm), stream>>>(
                 prm, F, out, out_mode, d_nbr.p, d_cset.p, d_adi_fast.p, srct, fail);
         } else if (mode == PD_MODE_FAST && fast.big) {
@@ -446,12 +468,8 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
         }
         // kernel family
         e->mode = PD_MODE_EXACT;
-        if (exact_smem_bytes(p) > 48 * 1024) {
-            CUDA_TRY(cudaFuncSetAttribute(k_gaptooth_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)exact_smem_bytes(p)));
-            CUDA_TRY(cudaFuncSetAttribute(k_integrate_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)exact_smem_bytes(p)));
-        }
+        raise_dyn_smem((const void*)k_gaptooth_exact, exact_smem_bytes(p));
+        raise_dyn_smem((const void*)k_integrate_exact, exact_smem_bytes(p));
         // FAST ADI (kernels_adi_fast.cuh) up to 32 nodes per side: with the compact per-node
         // tables it measured 1.5-2.3x faster than the EXACT ADI kernel at 11^2 and 3.0x at 21^2
         // (profiles/r01_adi.jsonl); larger patches stay on EXACT (bit-identical)
@@ -463,18 +481,17 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
             k_adi_fast_fold<<<(total + threads - 1) / threads, threads, 0, e->stream>>>(p, e->d_coeffs.p, e->d_src.p,
                                                                                          d.ncoeff_sets, e->d_adi_fast.p);
             e->check_launch();
-            if (fast_adi_smem_bytes(p) > 48 * 1024)
-                CUDA_TRY(cudaFuncSetAttribute(adi_fast_staged(p) ? k_fast_adi<true> : k_fast_adi<false>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)fast_adi_smem_bytes(p)));
+            raise_dyn_smem(adi_fast_staged(p) ? (const void*)k_fast_adi<true> : (const void*)k_fast_adi<false>,
+                           fast_adi_smem_bytes(p));
             if (!adi_fast_staged(p)) {
                 // the unstaged kernel reads its tables through L1: carve out only the shared
                 // memory of the blocks that can be resident (at most four: its register
                 // limit) and leave the rest to L1 (21^2: 1.53 -> 1.27 ms per macro step)
                 const size_t per_block = fast_adi_smem_bytes(p) + 1024, smem_max = 233472;
                 const size_t blocks = std::max<size_t>(1, std::min<size_t>(4, smem_max / per_block));
-                const int pct = (int)std::min<size_t>(100, (blocks * per_block * 100 + smem_max - 1) / smem_max);
-                CUDA_TRY(cudaFuncSetAttribute(k_fast_adi<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+                // (the carve-out is a process-wide function attribute too: each engine
+                // applies its own value right before its launches, launch_step)
+                e->adi_carveout = (int)std::min<size_t>(100, (blocks * per_block * 100 + smem_max - 1) / smem_max);
             }
             e->device_bytes += nf * 8;
             e->fast.adi = 1;
@@ -507,6 +524,8 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
 void pd_engine_destroy(pd_engine* e) { delete e; }
 
 int32_t pd_engine_mode(const pd_engine* e) { return e ? e->mode : -1; }
+int32_t pd_engine_mixed(const pd_engine* e) { return e ? e->prm.mixed : -1; }
+int64_t pd_engine_launch_count(const pd_engine* e) { return e ? e->launches : -1; }
 
 pd_status pd_engine_tables(const pd_engine* e, int32_t* patch_ij, int32_t* neighbours) {
     if (!e) return PD_VALIDATION_ERROR;
@@ -607,15 +626,17 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         CUDA_TRY(cudaMemsetAsync(e->d_counter.p, 0, ((size_t)nsteps + 1) * 4, e->stream));
         CUDA_TRY(cudaMemsetAsync(e->d_fail.p, 0, 16, e->stream));
         const int gblocks = (int)std::min<size_t>(1184, (NF + 255) / 256);
-        // initial scale: flags go to the scratch pair d_fail[2..3], never to the run's flag
-        k_guard<<<gblocks, 256, 0, e->stream>>>(U, NF, e->d_slot.p + nsteps, e->d_counter.p + nsteps,
-                                                e->d_fail.p + 2, e->d_fail.p + 3, 0, INFINITY);
-        e->check_launch();
-        unsigned long long s0 = 0;
-        download(&s0, e->d_slot.p + nsteps, 8, e->stream);
-        CUDA_TRY(cudaStreamSynchronize(e->stream));
-        double scale0;
-        std::memcpy(&scale0, &s0, 8);
+        double scale0 = e->guard_scale;
+        if (!(scale0 > 0.0)) {
+            // initial scale: flags go to the scratch pair d_fail[2..3], never to the run's flag
+            k_guard<<<gblocks, 256, 0, e->stream>>>(U, NF, e->d_slot.p + nsteps, e->d_counter.p + nsteps,
+                                                    e->d_fail.p + 2, e->d_fail.p + 3, 0, INFINITY);
+            e->check_launch();
+            unsigned long long s0 = 0;
+            download(&s0, e->d_slot.p + nsteps, 8, e->stream);
+            CUDA_TRY(cudaStreamSynchronize(e->stream));
+            std::memcpy(&scale0, &s0, 8);
+        }
         const double blowup = 10.0 * std::max(scale0, 1e-12);
         const size_t pk = e->perim * (e->prm.k + 2);
         const size_t sk = (size_t)e->prm.nt * (e->prm.k + 1);
@@ -648,8 +669,7 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         }
         if (fused) {
         } else if (block_run) {
-            CUDA_TRY(cudaFuncSetAttribute(k_linear_run_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)block_smem));
+            raise_dyn_smem((const void*)k_linear_run_block, block_smem);
             k_linear_run_block<<<1, 1024, block_smem, e->stream>>>(e->prm, U, e->d_pij.p, e->d_roww.p, bnd, e->perim,
                                                                     nsteps, blowup, e->d_slot.p, e->d_fail.p);
             e->check_launch();
@@ -704,7 +724,7 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         if (fail[0]) {
             std::ostringstream m;
             m << "coarse field " << (fail[1] ? "became non-finite" : "exceeded 10x the initial magnitude")
-              << " at macro step " << fail[0] << " (t=" << fail[0] * e->prm.dt_macro
+              << " at macro step " << fail[0] + e->step_offset << " (t=" << (fail[0] + e->step_offset) * e->prm.dt_macro
               << "); the projective step size is likely beyond the stable range";
             e->err = m.str();
             result = PD_MACRO_INSTABILITY;
@@ -948,6 +968,13 @@ pd_status pd_engine_set_step_kind(pd_engine* e, int32_t kind) {
 }
 
 int32_t pd_engine_step_kind(const pd_engine* e) { return e ? e->step_kind : -1; }
+
+pd_status pd_engine_set_run_guard(pd_engine* e, double scale0, int32_t step_offset) {
+    if (!e || step_offset < 0 || std::isnan(scale0)) return PD_VALIDATION_ERROR;
+    e->guard_scale = scale0 > 0.0 ? scale0 : 0.0;
+    e->step_offset = step_offset;
+    return PD_OK;
+}
 
 } // extern "C"
 

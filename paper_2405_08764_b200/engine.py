@@ -78,6 +78,11 @@ def lib() -> C.CDLL:
     L.pd_engine_set_step_kind.argtypes = [vp, C.c_int32]
     L.pd_engine_step_kind.argtypes = [vp]
     L.pd_engine_step_kind.restype = C.c_int32
+    L.pd_engine_set_run_guard.argtypes = [vp, C.c_double, C.c_int32]
+    L.pd_engine_mixed.argtypes = [vp]
+    L.pd_engine_mixed.restype = C.c_int32
+    L.pd_engine_launch_count.argtypes = [vp]
+    L.pd_engine_launch_count.restype = C.c_int64
     L.pd_problem_create.argtypes = [C.POINTER(ProblemDesc), C.POINTER(vp)]
     L.pd_problem_destroy.argtypes = [vp]
     L.pd_problem_resolved.argtypes = [vp, C.POINTER(ProblemDesc)]
@@ -96,7 +101,8 @@ def lib() -> C.CDLL:
     for name in ["pd_bench_step_kernel", "pd_bench_fp64_peak", "pd_engine_create", "pd_engine_tables", "pd_engine_set_stream", "pd_gaptooth_step",
                  "pd_projective_step", "pd_projective_step_device", "pd_run", "pd_run_device",
                  "pd_integrate_batch", "pd_lift_batch", "pd_restrict_batch", "pd_evolve_batch",
-                 "pd_linear_weights", "pd_engine_set_linear", "pd_engine_set_step_kind", "pd_problem_create",
+                 "pd_linear_weights", "pd_engine_set_linear", "pd_engine_set_step_kind", "pd_engine_set_run_guard",
+                 "pd_problem_create",
                  "pd_problem_resolved", "pd_problem_engine_desc", "pd_problem_initial_field",
                  "pd_problem_boundary", "pd_problem_boundary_table", "pd_problem_exact",
                  "pd_problem_stability", "pd_coeffs_generate"]:
@@ -304,6 +310,21 @@ class Engine:
         if st != abi.PD_MACRO_INSTABILITY or raise_on_instability:
             _check(st, self.h)
         return U, stats
+
+    @property
+    def mixed(self) -> bool:
+        """True when the table carries the mixed term (9-point operator)."""
+        return lib().pd_engine_mixed(self.h) == 1
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().pd_engine_launch_count(self.h))
+
+    def set_run_guard(self, scale0: float = 0.0, step_offset: int = 0):
+        """Segmented cpi::run: later runs use 10 x max(scale0, 1e-12) as the
+        blow-up threshold and number steps from step_offset (scale0 <= 0:
+        measure each call's input, the default)."""
+        _check(lib().pd_engine_set_run_guard(self.h, float(scale0), int(step_offset)), self.h)
 
     def run_exact(self, U0, nsteps, exact, t0=0.0, bnd=None, src_time=None, raise_on_instability=True):
         """run() plus cpi::run's per-step exact-error metric on the device

@@ -100,6 +100,14 @@ def subset_desc(ed: EngineDesc, slab: Slab) -> EngineDesc:
     return d
 
 
+@dataclass
+class RunResult:
+    U: object            # this rank's full-size field after the last completed step
+    steps_done: int
+    failed_step: int     # 0, or the macro step whose guard tripped (cpi.cpp:187-202)
+    device_ms: float     # CUDA-event time of the loop (0 on CPU)
+
+
 class ShardedRun:
     """The cpi::run macro loop (cpi.cpp:175-202) over xi-slabs.
 
@@ -190,6 +198,69 @@ class ShardedRun:
                 return U, n, n + 1
         return U, nsteps, 0
 
+    def owned_mask(self, device=None):
+        """The nodes this rank's guard covers (owned_max's scope), as a mask."""
+        import torch
+
+        s = self.s
+        m = torch.zeros(s.Nxi + 1, self.n2, dtype=torch.bool, device=device)
+        m[s.i0:s.i1] = True
+        m[:, 0] = m[:, -1] = True
+        if not s.periodic:
+            m[0] = m[-1] = True
+        return m.reshape(-1)
+
+    def run_deferred(self, U, nsteps: int, dt: float, t0: float = 0.0, bnd_table=None) -> "RunResult":
+        """The macro loop without any host round trip or collective per step:
+        each step's owned max |U| (non-finite -> +inf) goes to a device array,
+        and ONE all-reduce(max) of that array after the loop takes cpi::run's
+        guard decision (cpi.cpp:187-202) for every step at once.  On a trip at
+        step n the loop is replayed with the per-step guard (run()), so the
+        result is run()'s: the same failing step and field.  Device time
+        (CUDA events on the current stream) covers the loop and the reduction."""
+        import torch
+
+        d = self.dist
+        dev = U.device
+        cuda = dev.type == "cuda"
+        red = (lambda x: x.cpu()) if self.stage_cpu else (lambda x: x)
+        back = (lambda x: x.to(dev)) if self.stage_cpu else (lambda x: x)
+        mask = self.owned_mask(dev)
+        zero = torch.zeros((), dtype=U.dtype, device=dev)
+        inf = torch.full((), float("inf"), dtype=U.dtype, device=dev)
+        U0 = U.clone()
+        if cuda:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+        m0 = red(torch.where(mask, U.abs(), zero).amax().reshape(1))
+        d.all_reduce(m0, op=d.ReduceOp.MAX, group=self.group)
+        blowup = 10.0 * torch.clamp(back(m0), min=1e-12)
+        maxes = torch.zeros(max(nsteps, 1), dtype=U.dtype, device=dev)
+        nxt = U.clone()  # columns a rank never computes stay finite
+        for n in range(nsteps):
+            self.step_fn(U, nxt, t0 + n * dt, None if bnd_table is None else bnd_table[n])
+            self.exchange(nxt)
+            m = torch.where(mask, nxt.abs(), zero).amax()
+            maxes[n] = torch.where(torch.isfinite(m), m, inf)
+            U, nxt = nxt, U
+        allm = red(maxes)
+        d.all_reduce(allm, op=d.ReduceOp.MAX, group=self.group)
+        trips = back(allm)[:nsteps] > blowup
+        if cuda:
+            ev1.record()
+        trips = trips.cpu().numpy()
+        ms = 0.0
+        if cuda:
+            ev1.synchronize()
+            ms = ev0.elapsed_time(ev1)
+        if not trips.any():
+            return RunResult(U, nsteps, 0, ms)
+        # replay with the per-step guard: stops at the same step with the same
+        # field as run() (the state right after the failing step)
+        U, done, fail = self.run(U0, nsteps, dt, t0, bnd_table)
+        assert fail == int(np.argmax(trips)) + 1, (fail, trips)
+        return RunResult(U, done, fail, ms)
+
     def gather(self, U):
         """Assemble the full field on every rank from each rank's own columns."""
         import torch
@@ -227,3 +298,18 @@ def device_step_fn(engine, k: int, perim: int, device):
                                                None if b is None else b.data_ptr(), None), engine.h)
 
     return step
+
+
+def device_runner(engine, slab: Slab, ed: EngineDesc, dist, device, group=None) -> ShardedRun:
+    """The product wiring for one rank: the slab's subset engine on the current
+    torch stream (so its kernels, NCCL's halo exchange and the guard reductions
+    are ordered on one stream with no host synchronisation), the fused
+    projective step per macro step (pd_projective_step_device)."""
+    import torch
+
+    from .engine import _check, lib
+
+    stream = torch.cuda.current_stream(device)
+    _check(lib().pd_engine_set_stream(engine.h, stream.cuda_stream), engine.h)
+    step = device_step_fn(engine, ed.k, engine.perim, device)
+    return ShardedRun(slab, ed.Neta, step, dist, group=group, k=ed.k)

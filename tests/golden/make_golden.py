@@ -16,6 +16,10 @@ c4_small.npz        config-4 equation on 32x32 patches, 100 macro steps, by the
                     itself rejects b != 0 — parity unpinned by the reference).
 c4_sample.npz       full-size config 4: one gap-tooth substep on 1024 sampled
                     patches by the restated oracle.
+c4_full.npz         full-size config 4 (512x512 patches of 16x16, K = 50): the
+                    field after the first projective step and after the full
+                    100-step run, by the restated oracle (OpenMP over patches,
+                    bit-identical to one thread: patches are independent).
 table1_cdr.npz      the reference's shipped Table-1 output (proj/out/table1/snapshots,
                     problem1_constant(0) with the ADI micro-solver) as arrays.
 ref_adi.npz         ADI micro-solver variants (upwind two/three/four, Neumann/
@@ -157,6 +161,23 @@ def c4(O):
     print(f"c4 sample: {sec:.2f} s")
 
 
+def c4_full(O):
+    """BASELINE config 4 at its stated size, the whole cpi::run (cpi.cpp:134-216)."""
+    import time
+    d, _ = configs.load("c4_shear")
+    prob = Problem(d)
+    ed = prob.engine_desc()
+    U0 = prob.initial_field()
+    t0 = time.perf_counter()
+    st, U1 = O.projective_step(ed, U0, 0.0)
+    assert st == 0
+    st, UT, stats = O.run(ed, U0, prob.desc.Nt)
+    assert st == 0 and stats.steps_done == prob.desc.Nt, (st, stats.steps_done)
+    np.savez_compressed(OUT / "c4_full.npz", U1=U1, final=UT, nsteps=prob.desc.Nt, tau=prob.desc.tau,
+                        T=prob.desc.T, U0_sum=U0.sum(), umax_last=np.array(stats.umax_last))
+    print(f"c4 full oracle run: {prob.desc.Nt} steps, {time.perf_counter() - t0:.1f} s, {O.threads} threads")
+
+
 def unit_cases(ref):
     """Integrate / lift / restrict through the reference (fixtures for the GPU box)."""
     rng = np.random.default_rng(99)
@@ -198,6 +219,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["linear"]:
         ref_linear(ref)
         sys.exit(0)
+    if sys.argv[1:] == ["c4full"]:
+        c4_full(O)
+        sys.exit(0)
     if sys.argv[1:] == ["adi"]:
         table1()
         ref_adi(ref)
@@ -208,4 +232,5 @@ if __name__ == "__main__":
     ref_adi(ref)
     annulus()
     c4(O)
+    c4_full(O)
     unit_cases(ref)

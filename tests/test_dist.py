@@ -48,7 +48,7 @@ def test_replica_value_uses_max_over_ranks():
 # the sharded run equals the single-engine run bit for bit (restated oracle as
 # the per-rank compute, gloo point-to-point for the halo columns).
 # ---------------------------------------------------------------------------
-def _shard_worker(rank, world, port, name, over, nsteps, out):
+def _shard_worker(rank, world, port, name, over, nsteps, out, deferred=False):
     import numpy as np
     import torch
 
@@ -72,16 +72,22 @@ def _shard_worker(rank, world, port, name, over, nsteps, out):
     runner = sharded.ShardedRun(sl, ed.Neta, step, dist, k=P.desc.k)
     U0 = torch.from_numpy(P.initial_field().reshape(-1).copy())
     dt = P.desc.T / P.desc.Nt
-    U, done, failed = runner.run(U0, nsteps, dt, 0.0, P.boundary_table(0.0, nsteps))
+    if deferred:  # bench.py's loop: no per-step host round trip, one guard reduction at the end
+        res = runner.run_deferred(U0, nsteps, dt, 0.0, P.boundary_table(0.0, nsteps))
+        U, done, failed = res.U, res.steps_done, res.failed_step
+    else:
+        U, done, failed = runner.run(U0, nsteps, dt, 0.0, P.boundary_table(0.0, nsteps))
     full = runner.gather(U)
     out[rank] = (full.numpy().copy(), done, failed)
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("deferred", [False, True], ids=["per-step-guard", "deferred-guard"])
 @pytest.mark.parametrize("name,over,world", [("c1_diffusion", {}, 2), ("c1_diffusion", {}, 3),
                                              ("c3_annulus", {}, 2), ("c3_annulus", {}, 3),
-                                             ("c1_diffusion", {"dt_over_tau": 1000, "Nt": 50}, 2)])
-def test_sharded_run_equals_single_engine(name, over, world):
+                                             ("c1_diffusion", {"dt_over_tau": 1000, "Nt": 50}, 2),
+                                             ("c1_diffusion", {"dt_over_tau": 150, "Nt": 50}, 3)])
+def test_sharded_run_equals_single_engine(name, over, world, deferred):
     import numpy as np
 
     from oracle.pyoracle import Restated
@@ -92,7 +98,7 @@ def test_sharded_run_equals_single_engine(name, over, world):
     port = _free_port()
     with mp.Manager() as m:
         out = m.dict()
-        mp.spawn(_shard_worker, args=(world, port, name, over, nsteps, out), nprocs=world, join=True)
+        mp.spawn(_shard_worker, args=(world, port, name, over, nsteps, out, deferred), nprocs=world, join=True)
         res = dict(out)
     P = Problem(configs.copy_desc(configs.load(name)[0], **over))
     ed = P.engine_desc()
@@ -102,5 +108,7 @@ def test_sharded_run_equals_single_engine(name, over, world):
         if st == 0:
             assert failed == 0 and done == nsteps
             assert np.array_equal(U.reshape(P.shape), Uref)
-        else:  # the guard trips at the same macro step on every rank
+        else:  # the guard trips at the same macro step on every rank, with the same field
             assert failed == stats.failed_step and done == stats.steps_done
+            if deferred:
+                assert np.array_equal(U.reshape(P.shape), Uref)
