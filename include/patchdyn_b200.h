@@ -66,7 +66,7 @@ typedef enum pd_status {
     PD_MACRO_PATCH_ERROR = 13,     /* MacroPatchError      errors.hpp:50 */
     PD_VALIDATION_ERROR = 15,      /* ValidationError      errors.hpp:56 */
     PD_CUDA_ERROR = 100,           /* device failure (no reference analogue) */
-    PD_UNSUPPORTED = 101           /* feature outside the device path (ADI, general source) */
+    PD_UNSUPPORTED = 101           /* feature outside the device path (general sources, time-dependent coefficients, ADI 3/4-point upwinding on non-square patches) */
 } pd_status;
 
 /* SchemeConfig::BCType  proj/include/patchdyn/scheme_config.hpp:21-23 */

@@ -193,3 +193,26 @@ def test_segmented_run_trips_at_the_runs_step(restated, gpu):
         for s in range(n):
             U, st = E.run(U, 1, t0=s * dt, bnd=bt[s:s + 1], raise_on_instability=False)
             assert st.failed_step == 0
+
+
+# ---------------------------------------------------------------------------
+# config 5: every (patch shape, K) combination of the sweep, whole-field runs
+# against the restated oracle at 2^12 patches (the sweep's smallest size; the
+# larger sizes are checked per row by bench.py --sweep: parity_rel)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("K", [10, 50, 200])
+@pytest.mark.parametrize("nodes", [8, 16, 32])
+def test_config5_points_full_field_vs_oracle(nodes, K, restated, gpu):
+    base, _ = configs.load("c5_sweep")
+    P = Problem(configs.sweep_desc(base, 12, nodes, K))
+    ed = P.engine_desc()
+    U0 = P.initial_field()
+    n = 3
+    st, Uo, _ = restated.run(ed, U0, n)
+    assert st == abi.PD_OK
+    F = Engine.from_problem(P, mode=FAST)
+    assert F.mode == FAST
+    Uf, sf = F.run(U0, n)
+    assert sf.steps_done == n and rel(Uf, Uo) < TOL
+    Ux, _ = Engine.from_problem(P, mode=EXACT).run(U0, n)
+    assert np.array_equal(Ux, Uo)
