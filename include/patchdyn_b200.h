@@ -66,7 +66,9 @@ typedef enum pd_status {
     PD_MACRO_PATCH_ERROR = 13,     /* MacroPatchError      errors.hpp:50 */
     PD_VALIDATION_ERROR = 15,      /* ValidationError      errors.hpp:56 */
     PD_CUDA_ERROR = 100,           /* device failure (no reference analogue) */
-    PD_UNSUPPORTED = 101           /* feature outside the device path (general sources, time-dependent coefficients, ADI 3/4-point upwinding on non-square patches) */
+    PD_UNSUPPORTED = 101           /* feature outside the device path (ADI 3/4-point upwinding on non-square
+                                      patches; a general source or time-dependent tables outside the
+                                      sampled entries) */
 } pd_status;
 
 /* SchemeConfig::BCType  proj/include/patchdyn/scheme_config.hpp:21-23 */
@@ -78,7 +80,10 @@ enum { PD_EDGE_E = 0, PD_EDGE_W = 1, PD_EDGE_N = 2, PD_EDGE_S = 3 };
 /* SchemeConfig::Quadrature  scheme_config.hpp:25-26 */
 enum { PD_QUAD_TRAPEZOID = 0, PD_QUAD_SIMPSON = 1 };
 /* source structure  microsim.hpp:58-64 */
-enum { PD_SOURCE_ZERO = 0, PD_SOURCE_SEPARABLE = 1 };
+enum { PD_SOURCE_ZERO = 0, PD_SOURCE_SEPARABLE = 1,
+       /* general f(x, y, t) (microsim.cpp:278-280): supplied per micro step through the
+        * sampled entries below; the other step entries return PD_UNSUPPORTED */
+       PD_SOURCE_GENERAL = 2 };
 /* Micro-solver (SchemeConfig::Solver, scheme_config.hpp:19-20; NOTE the C
  * values differ from the reference's enum order so that a zero-initialised
  * descriptor selects the explicit scheme of the BASELINE configs) and the ADI
@@ -283,6 +288,23 @@ pd_status pd_engine_set_linear(pd_engine* e, const double* row_w_host);
 pd_status pd_engine_set_step_kind(pd_engine* e, int32_t kind);
 int32_t pd_engine_step_kind(const pd_engine* e);
 
+/* Time-dependent coefficients and general sources (microsim.cpp:537-542,
+ * 278-280) on the device.  The reference re-samples its coefficient closures at
+ * every micro step (t_co = t_substep + s*dt) and evaluates a general source per
+ * node; closures cannot run on the GPU, so the caller samples them (as the
+ * reference does, e.g. pd_problem_sample_steps) and the device does the solve:
+ *   coeff_steps  [subs][nt][ncoeff_sets][PD_NCOEF][nx+1][ny+1] solver form, or NULL
+ *                (the engine's static table),
+ *   source_steps [subs][nt][ncoeff_sets][nx+1][ny+1] = general(node)/l, or NULL,
+ * with subs = 1 (gap-tooth step) or k+1 (projective step: substep m starts at
+ * t + m*tau).  bnd as pd_gaptooth_step ([perimeter]) / pd_projective_step
+ * ([k+2][perimeter]).  Explicit micro-solver; runs the EXACT kernel family
+ * (bit-identical to the reference).  Host buffers. */
+pd_status pd_gaptooth_step_sampled(pd_engine* e, const double* U_in, double* U_out, double t, const double* bnd,
+                                   const double* coeff_steps, const double* source_steps);
+pd_status pd_projective_step_sampled(pd_engine* e, const double* U_in, double* U_out, double t, const double* bnd,
+                                     const double* coeff_steps, const double* source_steps);
+
 /* Segmented cpi::run (cpi.cpp:134-216 split around probes / snapshots /
  * progress callbacks): the blow-up threshold is 10 x max(scale0, 1e-12) with
  * scale0 = max|U| of the RUN's initial field after refresh_boundary
@@ -307,7 +329,11 @@ enum {
     PD_PROBLEM_REF_ANNULUS = 10,     /* problems::problem2_annulus  problems.cpp:110-138 */
     PD_PROBLEM_REF_CDR = 11,         /* problems::problem1_constant(lambda)  problems.cpp:19-73 */
     PD_PROBLEM_REF_CDR_VAR = 13,     /* problems::problem1_variable(lambda)  problems.cpp:19-75 */
-    PD_PROBLEM_STEADY = 12           /* harmonic u = x + y (test_gaptooth.cpp:32-49) */
+    PD_PROBLEM_STEADY = 12,          /* harmonic u = x + y (test_gaptooth.cpp:32-49) */
+    PD_PROBLEM_PULSED_CDR = 14       /* time-dependent coefficients + a general (non-separable)
+                                        source: D(t) = eps (1 + sin(w t)/2), v(t) = vel (cos w t, 1/2),
+                                        f = sin(pi x) cos(pi y + w t), w = omega; identity map, zero Dirichlet
+                                        (exercises microsim.cpp:537-542 and 278-280) */
 };
 enum { PD_DT_GIVEN = 0, PD_DT_DIFFUSION = 1, PD_DT_METRIC = 2 };
 enum { PD_COEFF_HOST = 0, PD_COEFF_DEVICE = 1 };
@@ -367,6 +393,15 @@ pd_status pd_problem_exact(const pd_problem* p, double t, double* U_host);
 /* max |A|+|C| over all sampled nodes (the dt pin's denominator) and the
  * reference's single-direction stability number (microsim.cpp:253-262). */
 pd_status pd_problem_stability(const pd_problem* p, double* max_a_plus_c, double* ref_number);
+/* Time-dependent coefficients / general sources: the samples of one gap-tooth
+ * substep starting at t0 that PatchIntegrator::integrate takes at every micro
+ * step t0 + s*dt (sample_coeffs / sample_source, microsim.cpp:537-542,
+ * 265-281) for every coefficient set, laid out for pd_*_step_sampled:
+ * coeff_steps [nt][sets][PD_NCOEF][nx+1][ny+1], source_steps [nt][sets][nx+1][ny+1]
+ * (= general(x, y, t)/l), either NULL.  Every coefficient sample passes the
+ * explicit stability guard or PD_STABILITY_VIOLATION (microsim.cpp:253-262). */
+pd_status pd_problem_sample_substep(const pd_problem* p, double t0, double* coeff_steps_host,
+                                    double* source_steps_host);
 
 /* The device generator on its own (desc->coeff_generator must be set): the
  * table into coeffs_host [ncoeff_sets][PD_NCOEF][n1][n2] and the source's

@@ -229,6 +229,22 @@ inline Built build(const pd_problem_desc& d) {
             p.coeffs_xi_independent = true;
             break;
         }
+        case PD_PROBLEM_PULSED_CDR: { // time-dependent coefficients + a general source
+            const double eps = d.eps, vel = d.vel, om = d.omega; // om: pulsation frequency
+            p.name = "pulsed-cdr";
+            p.mapping = geometry::identity_map();
+            auto Dfn = [eps, om](double, double, double t) { return eps * (1.0 + 0.5 * std::sin(om * t)); };
+            auto vx = [vel, om](double, double, double t) { return vel * std::cos(om * t); };
+            auto vy = [vel](double, double, double) { return 0.5 * vel; };
+            auto f = [om](double x, double y, double t) { return std::sin(M_PI * x) * std::cos(M_PI * y + om * t); };
+            p.physical = geometry::cdr_coefficients(Dfn, Dfn, vx, vy, f);
+            p.initial = [](double xi, double eta) { return std::sin(M_PI * xi) * std::sin(M_PI * eta); };
+            p.bcW = p.bcE = p.bcS = p.bcN = zero2;
+            p.coeffs_time_independent = false;
+            p.source_zero = false;
+            p.source_separable = false;
+            break;
+        }
         default:
             throw ValidationError("unknown problem kind");
     }

@@ -30,7 +30,7 @@ PD_BC_NEUMANN, PD_BC_DIRICHLET, PD_BC_ROBIN = 0, 1, 2
 PD_EDGE_DIRICHLET, PD_EDGE_NEUMANN, PD_EDGE_ROBIN = 0, 1, 2
 PD_EDGE_E, PD_EDGE_W, PD_EDGE_N, PD_EDGE_S = 0, 1, 2, 3
 PD_QUAD_TRAPEZOID, PD_QUAD_SIMPSON = 0, 1
-PD_SOURCE_ZERO, PD_SOURCE_SEPARABLE = 0, 1
+PD_SOURCE_ZERO, PD_SOURCE_SEPARABLE, PD_SOURCE_GENERAL = 0, 1, 2
 PD_MODE_FAST, PD_MODE_EXACT = 0, 1
 PD_STEP_DIRECT, PD_STEP_LINEAR = 0, 1
 PD_SOLVER_EXPLICIT, PD_SOLVER_ADI = 0, 1
@@ -46,6 +46,7 @@ PD_PROBLEM_REF_ANNULUS = 10
 PD_PROBLEM_REF_CDR = 11
 PD_PROBLEM_REF_CDR_VAR = 13
 PD_PROBLEM_STEADY = 12
+PD_PROBLEM_PULSED_CDR = 14
 PD_DT_GIVEN, PD_DT_DIFFUSION, PD_DT_METRIC = 0, 1, 2
 PD_COEFF_HOST, PD_COEFF_DEVICE = 0, 1
 

@@ -24,6 +24,7 @@ KINDS = {
     "ref-cdr": abi.PD_PROBLEM_REF_CDR,
     "ref-cdr-var": abi.PD_PROBLEM_REF_CDR_VAR,
     "steady": abi.PD_PROBLEM_STEADY,
+    "pulsed-cdr": abi.PD_PROBLEM_PULSED_CDR,
 }
 BC = {"neumann": abi.PD_BC_NEUMANN, "dirichlet": abi.PD_BC_DIRICHLET, "robin": abi.PD_BC_ROBIN}
 QUAD = {"trapezoid": abi.PD_QUAD_TRAPEZOID, "simpson": abi.PD_QUAD_SIMPSON}

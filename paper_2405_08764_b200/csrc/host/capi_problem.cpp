@@ -182,6 +182,18 @@ pd_status pd_problem_exact(const pd_problem* p, double t, double* U) {
     return PD_OK;
 }
 
+pd_status pd_problem_sample_substep(const pd_problem* p, double t0, double* coeff_steps, double* source_steps) {
+    try {
+        if (!p || (!coeff_steps && !source_steps)) throw pdb200::ValidationError("null argument");
+        if (source_steps && (p->spec.source_zero || p->spec.source_separable))
+            throw pdb200::Unsupported("the problem has no general source to sample");
+        pdb200::sample_substep(p->spec, p->cfg, p->tables, t0, coeff_steps, source_steps, p->desc.threads);
+        return PD_OK;
+    } catch (const pdb200::Error& e) {
+        return static_cast<pd_status>(fail(e));
+    }
+}
+
 pd_status pd_problem_stability(const pd_problem* p, double* max_a_plus_c, double* ref_number) {
     const double dmin = std::min(p->cfg.h_xi / p->cfg.nx, p->cfg.h_eta / p->cfg.ny);
     if (max_a_plus_c) *max_a_plus_c = p->tables.max_a_plus_c;

@@ -149,10 +149,37 @@ public:
     }
     void select_default_step() const { select_step(use_fast_); }
 
+    // time-dependent coefficients or a general source: the per-micro-step
+    // sampling of PatchIntegrator::integrate (microsim.cpp:537-542, 265-281)
+    // happens here on the host and the device runs the sweeps on the samples
+    bool sampled() const {
+        return !problem_.coeffs_time_independent || (!problem_.source_zero && !problem_.source_separable);
+    }
+    // [subs][nt][sets][6][N] coefficient and [subs][nt][sets][N] source samples
+    // for the substeps starting at t, t + tau, ...
+    void sample_tables(double t, int subs, std::vector<double>& c, std::vector<double>& g) const {
+        const size_t N = static_cast<size_t>(cfg_.nx + 1) * (cfg_.ny + 1), S = tables_.desc.ncoeff_sets;
+        const size_t per_c = cfg_.nt * S * PD_NCOEF * N, per_g = cfg_.nt * S * N;
+        const bool gen = !problem_.source_zero && !problem_.source_separable;
+        c.assign(subs * per_c, 0.0);
+        g.assign(gen ? subs * per_g : 0, 0.0);
+        for (int m = 0; m < subs; ++m)
+            sample_substep(problem_, cfg_, tables_, t + m * cfg_.tau, c.data() + m * per_c,
+                           gen ? g.data() + m * per_g : nullptr);
+    }
+
 private:
     CoarseField device_step(const CoarseField& F, double t) const {
         CoarseField out{grid_, F.periodic, Field2D(F.U.n1(), F.U.n2())};
         const std::vector<double> bnd = perimeter(t + cfg_.tau);
+        if (sampled()) {
+            std::vector<double> c, g;
+            sample_tables(t, 1, c, g);
+            throw_status(pd_gaptooth_step_sampled(eng_.get(), F.U.data(), out.U.data(), t, bnd.data(), c.data(),
+                                                  g.empty() ? nullptr : g.data()),
+                         eng_.get());
+            return out;
+        }
         const std::vector<double> src = source_factors(t, 0);
         throw_status(pd_gaptooth_step(eng_.get(), F.U.data(), out.U.data(), t, bnd.data(),
                                       src.empty() ? nullptr : src.data()),
@@ -228,6 +255,14 @@ inline gaptooth::CoarseField projective_step(const gaptooth::GapToothEngine& eng
     const std::vector<double> src = engine.source_factors(t, cfg.k);
     gaptooth::CoarseField out{U.grid, U.periodic, Field2D(U.U.n1(), U.U.n2())};
     engine.select_default_step(); // cpi.cpp:65 calls engine.step
+    if (engine.sampled()) {
+        std::vector<double> c, g;
+        engine.sample_tables(t, cfg.k + 1, c, g);
+        throw_status(pd_projective_step_sampled(engine.device(), U.U.data(), out.U.data(), t, bnd.data(), c.data(),
+                                                g.empty() ? nullptr : g.data()),
+                     engine.device());
+        return out;
+    }
     throw_status(pd_projective_step(engine.device(), U.U.data(), out.U.data(), t, bnd.data(),
                                     src.empty() ? nullptr : src.data()),
                  engine.device());
@@ -277,7 +312,10 @@ inline double max_percent_error(const gaptooth::GapToothEngine& engine, const ga
 // loop stays on the device (pd_run: one launch sequence, blow-up guard on the
 // device); with probes/snapshots/exact errors it runs in segments between the
 // steps that need the field on the host.
+inline RunResult run_sampled(const gaptooth::GapToothEngine& engine, const RunOptions& opts);
+
 inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& opts = {}) {
+    if (engine.sampled()) return run_sampled(engine, opts);
     const SchemeConfig& cfg = engine.config();
     const double dt = cfg.dt();
     gaptooth::CoarseField U = engine.initial_field();
@@ -361,6 +399,63 @@ inline RunResult run(const gaptooth::GapToothEngine& engine, const RunOptions& o
             opts.progress(n + m, t1, res.max_pct_err);
     }
     throw_status(pd_engine_set_run_guard(engine.device(), 0.0, 0), engine.device());
+    res.final_field = std::move(U);
+    return res;
+}
+
+// cpi::run for time-dependent coefficients / general sources: the reference's
+// loop (cpi.cpp:134-216) with each projective step on the device over host
+// samples; guard, probes, snapshots and the exact-error metric on the host
+inline RunResult run_sampled(const gaptooth::GapToothEngine& engine, const RunOptions& opts) {
+    const SchemeConfig& cfg = engine.config();
+    const double dt = cfg.dt();
+    gaptooth::CoarseField U = engine.initial_field();
+    engine.refresh_boundary(U, 0.0);
+    double scale0 = 0.0;
+    for (double v : U.U.raw()) scale0 = std::max(scale0, std::abs(v));
+    const double blowup = 10.0 * std::max(scale0, 1e-12);
+    RunResult res;
+    std::vector<int> snap;
+    for (double ts : opts.snapshot_times) snap.push_back(std::clamp(static_cast<int>(std::lround(ts / dt)), 0, cfg.Nt));
+    auto maybe_snapshot = [&](int n, double t) {
+        for (int& s : snap)
+            if (s == n) {
+                res.snapshots.push_back(Snapshot{t, U.U.raw()});
+                s = -1;
+                break;
+            }
+    };
+    for (auto [pi, pj] : opts.probe_nodes) res.probes.push_back(ProbeSeries{pi, pj, {}});
+    maybe_snapshot(0, 0.0);
+    for (int n = 0; n < cfg.Nt; ++n) {
+        U = projective_step(engine, U, n * dt);
+        const double t1 = (n + 1) * dt;
+        res.times.push_back(t1);
+        double umax = 0.0;
+        bool finite = true;
+        for (double v : U.U.raw()) {
+            if (!std::isfinite(v)) {
+                finite = false;
+                break;
+            }
+            umax = std::max(umax, std::abs(v));
+        }
+        if (!finite || umax > blowup) {
+            std::ostringstream os;
+            os << "coarse field " << (finite ? "exceeded 10x the initial magnitude" : "became non-finite")
+               << " at macro step " << n + 1 << " (t=" << t1 << "); the projective step size is likely beyond the stable range";
+            throw MacroInstability(os.str());
+        }
+        for (auto& ps : res.probes) ps.values.push_back(U.at(ps.i, ps.j));
+        if (engine.problem().has_exact()) {
+            const double e = max_percent_error(engine, U, t1);
+            res.step_max_pct_err.push_back(e);
+            res.max_pct_err = std::max(res.max_pct_err, e);
+        }
+        maybe_snapshot(n + 1, t1);
+        if (opts.progress_every > 0 && opts.progress && (n + 1) % opts.progress_every == 0)
+            opts.progress(n + 1, t1, res.max_pct_err);
+    }
     res.final_field = std::move(U);
     return res;
 }

@@ -229,6 +229,22 @@ ProblemSpec from_desc(const pd_problem_desc& d) {
             p.coeffs_xi_independent = true;
             return p;
         }
+        case PD_PROBLEM_PULSED_CDR: { // time-dependent coefficients + general source (as oracle/ref_problems.hpp)
+            const double eps = d.eps, vel = d.vel, om = d.omega; // om: pulsation frequency
+            p.name = "pulsed-cdr";
+            p.mapping = geometry::identity_map();
+            auto Dfn = [eps, om](double, double, double t) { return eps * (1.0 + 0.5 * std::sin(om * t)); };
+            auto vx = [vel, om](double, double, double t) { return vel * std::cos(om * t); };
+            auto vy = [vel](double, double, double) { return 0.5 * vel; };
+            auto f = [om](double x, double y, double t) { return std::sin(M_PI * x) * std::cos(M_PI * y + om * t); };
+            p.physical = geometry::cdr_coefficients(Dfn, Dfn, vx, vy, f);
+            p.initial = [](double xi, double eta) { return std::sin(M_PI * xi) * std::sin(M_PI * eta); };
+            p.bcW = p.bcE = p.bcS = p.bcN = zero2;
+            p.coeffs_time_independent = false;
+            p.source_zero = false;
+            p.source_separable = false;
+            return p;
+        }
         default:
             throw ValidationError("unknown problem kind " + std::to_string(d.problem));
     }
@@ -306,10 +322,9 @@ void EngineTables::relink() {
 }
 
 EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfig& cfg, int threads, bool sample) {
-    if (!p.coeffs_time_independent)
-        throw Unsupported("time-dependent coefficients are not on the device path");
-    if (!p.source_zero && !p.source_separable)
-        throw Unsupported("general (non-separable) sources are not on the device path");
+    // time-dependent coefficients: the table is the t = 0 sample (the reference's
+    // co0_, microsim.cpp:217); the sampled step entries supply later ones.  General
+    // sources: PD_SOURCE_GENERAL, supplied per micro step the same way.
     EngineTables t;
     pd_engine_desc& d = t.desc;
     d.a = p.a;
@@ -333,7 +348,7 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
     d.robin_w1 = cfg.robin_w1;
     d.robin_w2 = cfg.robin_w2;
     d.quadrature = cfg.quadrature == cpi::SchemeConfig::Quadrature::Simpson ? PD_QUAD_SIMPSON : PD_QUAD_TRAPEZOID;
-    d.source_kind = p.source_zero ? PD_SOURCE_ZERO : PD_SOURCE_SEPARABLE;
+    d.source_kind = p.source_zero ? PD_SOURCE_ZERO : p.source_separable ? PD_SOURCE_SEPARABLE : PD_SOURCE_GENERAL;
     d.l = p.physical.l;
     d.mode = cfg.mode;
     d.solver = cfg.solver == cpi::SchemeConfig::Solver::ADI ? PD_SOLVER_ADI : PD_SOLVER_EXPLICIT;
@@ -376,7 +391,7 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
         return t;
     }
     t.coeffs.assign(static_cast<size_t>(S) * PD_NCOEF * N, 0.0);
-    if (!p.source_zero) t.source_spatial.assign(static_cast<size_t>(S) * N, 0.0);
+    if (p.source_separable) t.source_spatial.assign(static_cast<size_t>(S) * N, 0.0);
 
     // CoarseGrid::xi/eta (gaptooth.hpp:21-24) and make_micro_grid (microsim.cpp:18-24)
     const double Dxi = (p.b - p.a) / cfg.N_xi, Deta = (p.d - p.c) / cfg.N_eta;
@@ -413,7 +428,7 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
                     m_ac = std::max({m_ac, std::abs(A), std::abs(Cc)});
                     m_apc = std::max(m_apc, std::abs(A) + std::abs(Cc));
                     m_b = std::max(m_b, std::abs(B));
-                    if (!p.source_zero)
+                    if (p.source_separable)
                         t.source_spatial[static_cast<size_t>(s) * N + k] = p.source_spatial(xi, eta);
                 }
         } catch (const Error& e) {
@@ -439,6 +454,80 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
         throw MixedTermUnsupported("mixed-derivative term with Robin patch conditions is not defined");
     t.relink();
     return t;
+}
+
+// Time-dependent coefficients / general sources: the per-micro-step samples the
+// reference's PatchIntegrator takes inside integrate (sample_coeffs(t_co) and
+// sample_source(t_co), microsim.cpp:537-542, 265-281), for every coefficient
+// set, at the set's node coordinates (same arithmetic as build_tables).
+void sample_substep(const problems::ProblemSpec& p, const cpi::SchemeConfig& cfg, const EngineTables& t, double t0,
+                    double* coeff_steps, double* source_steps, int threads) {
+    const int S = t.desc.ncoeff_sets, n1 = cfg.nx + 1, n2 = cfg.ny + 1;
+    const size_t N = static_cast<size_t>(n1) * n2;
+    const double Dxi = (p.b - p.a) / cfg.N_xi, Deta = (p.d - p.c) / cfg.N_eta;
+    const double mdxi = cfg.h_xi / cfg.nx, mdeta = cfg.h_eta / cfg.ny;
+    const double l = p.physical.l, dt = cfg.tau / cfg.nt;
+    const double dmin = std::min(mdxi, mdeta);
+    // the set -> representative patch map of build_tables: row sharing never
+    // applies here (it needs time-independent coefficients and no source)
+    int err_status = 0;
+    std::string err_msg;
+#ifdef _OPENMP
+    const int nth = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 4)
+#endif
+    for (int s = 0; s < S; ++s) {
+        try {
+            const int pi = t.patch_ij[2 * s], pj = t.patch_ij[2 * s + 1];
+            const double xc = p.a + Dxi * pi, ec = p.c + Deta * pj;
+            const double xi0 = xc - 0.5 * mdxi * cfg.nx, eta0 = ec - 0.5 * mdeta * cfg.ny;
+            for (int step = 0; step < cfg.nt; ++step) {
+                const double tc = t0 + step * dt; // explicit scheme (microsim.cpp:535-537)
+                double mx = 0.0;
+                for (int i = 0; i < n1; ++i)
+                    for (int j = 0; j < n2; ++j) {
+                        const double xi = xi0 + i * mdxi, eta = eta0 + j * mdeta;
+                        const size_t k = static_cast<size_t>(i) * n2 + j;
+                        if (coeff_steps) {
+                            const geometry::TransformedCoefficients tc2 =
+                                geometry::transform_coefficients(p.mapping, p.physical, xi, eta, tc);
+                            double* o = coeff_steps + (static_cast<size_t>(step) * S + s) * PD_NCOEF * N;
+                            const double A = -tc2.a / l, Cc = -tc2.c / l;
+                            o[PD_COEF_A * N + k] = A;
+                            o[PD_COEF_B * N + k] = std::abs(tc2.b) > 1e-12 ? -tc2.b / l : 0.0;
+                            o[PD_COEF_C * N + k] = Cc;
+                            o[PD_COEF_VX * N + k] = tc2.d / l;
+                            o[PD_COEF_VY * N + k] = tc2.e / l;
+                            o[PD_COEF_W * N + k] = tc2.f / l;
+                            mx = std::max({mx, std::abs(A), std::abs(Cc)});
+                        }
+                        if (source_steps) {
+                            const geometry::PhysPoint q = p.mapping.forward(xi, eta);
+                            source_steps[(static_cast<size_t>(step) * S + s) * N + k] = p.physical.phi(q.x, q.y, tc) / l;
+                        }
+                    }
+                // the explicit guard of every sample  microsim.cpp:253-262
+                if (coeff_steps && cfg.solver == cpi::SchemeConfig::Solver::Explicit &&
+                    mx * dt / (dmin * dmin) > 0.5 + 1e-12) {
+                    std::ostringstream msg;
+                    msg << "explicit micro scheme diffusive stability number " << mx * dt / (dmin * dmin)
+                        << " exceeds 0.5 at t = " << tc;
+                    throw StabilityViolation(msg.str());
+                }
+            }
+        } catch (const Error& e) {
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+            {
+                if (!err_status) {
+                    err_status = e.status;
+                    err_msg = e.what();
+                }
+            }
+        }
+    }
+    if (err_status) throw Error(err_status, err_msg);
 }
 
 void check_stability(const EngineTables& t, const cpi::SchemeConfig& cfg) {

@@ -124,5 +124,10 @@ EngineTables build_tables(const problems::ProblemSpec& p, const cpi::SchemeConfi
                           bool sample = true);
 // PatchIntegrator's explicit guard  microsim.cpp:253-262
 void check_stability(const EngineTables& t, const cpi::SchemeConfig& cfg);
+// Per-micro-step samples of one substep from t0 (time-dependent coefficients,
+// general sources; microsim.cpp:537-542, 265-281): coeff_steps [nt][sets][6][N],
+// source_steps [nt][sets][N], either may be null.  Throws StabilityViolation.
+void sample_substep(const problems::ProblemSpec& p, const cpi::SchemeConfig& cfg, const EngineTables& t, double t0,
+                    double* coeff_steps, double* source_steps, int threads = 0);
 
 } // namespace pdb200

@@ -49,8 +49,14 @@ __device__ inline void pin_initial_x(double* u, const int* kinds, const double* 
 
 // K explicit steps on the shared tile (PatchIntegrator::integrate loop,
 // microsim.cpp:535-550).  Returns the buffer holding the result.
+// Sampled variant (time-dependent coefficients / general sources,
+// microsim.cpp:537-542 and 278-280): coef_steps / src_steps, when given, are
+// this patch's set in per-micro-step tables [nt][sets][6][N] / [nt][sets][N]
+// (stride = one step's tables); they replace coef and the source term.
 __device__ inline double* micro_loop_x(const Params& p, PatchSh& s, const EdgeSh* eg, const double* coef,
-                                       const double* src_sp, const double* src_time, bool mixed) {
+                                       const double* src_sp, const double* src_time, bool mixed,
+                                       const double* coef_steps = nullptr, size_t coef_stride = 0,
+                                       const double* src_steps = nullptr, size_t src_stride = 0) {
     const double idx2 = XDIV(1.0, XMUL(p.mdxi, p.mdxi)), idy2 = XDIV(1.0, XMUL(p.mdeta, p.mdeta));
     const double idx = XDIV(1.0, XMUL(2.0, p.mdxi)), idy = XDIV(1.0, XMUL(2.0, p.mdeta));
     const double ixy = XDIV(1.0, XMUL(XMUL(4.0, p.mdxi), p.mdeta));
@@ -58,10 +64,12 @@ __device__ inline double* micro_loop_x(const Params& p, PatchSh& s, const EdgeSh
     double* nxt = s.u1;
     for (int step = 0; step < p.nt; ++step) {
         const double ft = (src_sp && src_time) ? src_time[step] : 0.0;
+        const double* co = coef_steps ? coef_steps + coef_stride * step : coef;
+        const double* gs = src_steps ? src_steps + src_stride * step : nullptr;
         for (int t = threadIdx.x; t < p.N; t += blockDim.x) {
             const int i = t / p.n2, j = t % p.n2;
-            const double G = (src_sp && src_time) ? XMUL(__ldg(src_sp + t), ft) : 0.0;
-            nxt[t] = sweep_node_x(cur, eg, s.val, s.slope, s.gb, p.L, p.nx, p.ny, i, j, coef, p.N, G, idx2, idy2,
+            const double G = gs ? __ldg(gs + t) : (src_sp && src_time) ? XMUL(__ldg(src_sp + t), ft) : 0.0;
+            nxt[t] = sweep_node_x(cur, eg, s.val, s.slope, s.gb, p.L, p.nx, p.ny, i, j, co, p.N, G, idx2, idy2,
                                   idx, idy, ixy, p.mdt, mixed);
         }
         __syncthreads();
@@ -95,7 +103,8 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
                  const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
                  const double* __restrict__ src_sp, const double* __restrict__ src_time,
                  const int* __restrict__ fail_flag, const double* __restrict__ stencil_in = nullptr,
-                 const int* __restrict__ item_patch = nullptr, const double* __restrict__ adi_fac = nullptr) {
+                 const int* __restrict__ item_patch = nullptr, const double* __restrict__ adi_fac = nullptr,
+                 const double* __restrict__ coef_steps = nullptr, const double* __restrict__ src_steps = nullptr) {
     extern __shared__ double sm[];
     if (fail_flag && *fail_flag) return;
     // item_patch != NULL: evolve_patch of given 3x3 values (stencil_in [items][9])
@@ -138,7 +147,10 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
         res = micro_loop_adi(p, s, eg, coef, sp, src_time, xs, xs + p.N,
                              adi_fac ? adi_fac + (size_t)set * adi_factor_doubles(p) : nullptr);
     } else {
-        res = micro_loop_x(p, s, eg, coef, sp, src_time, p.mixed != 0);
+        const size_t cst = (size_t)p.nsets * PD_NCOEF * p.N, sst = (size_t)p.nsets * p.N;
+        res = micro_loop_x(p, s, eg, coef, sp, src_time, p.mixed != 0,
+                           coef_steps ? coef_steps + (size_t)set * PD_NCOEF * p.N : nullptr, cst,
+                           src_steps ? src_steps + (size_t)set * p.N : nullptr, sst);
     }
     const double avg = restrict_x(res, p.nx, p.ny, p.quad, s.row);
     if (threadIdx.x == 0) {

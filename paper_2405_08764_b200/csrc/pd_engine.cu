@@ -105,6 +105,13 @@ struct pd_engine {
     int adi_carveout = -1;              // k_fast_adi<false> shared-memory carve-out (percent), -1: default
     double guard_scale = 0.0;           // > 0: blow-up scale of a segmented run (pd_engine_set_run_guard)
     int32_t step_offset = 0;            // macro steps before this segment, for the instability message
+    // sampled path (time-dependent coefficients / general sources): device
+    // tables [k+1][nt][sets][6][N] / [k+1][nt][sets][N] of the current call, and
+    // the substep launch_step is running (set by the step drivers)
+    DevBuf<double> d_samp;
+    const double* samp_coef = nullptr;
+    const double* samp_src = nullptr;
+    int sub_m = 0;
     DevBuf<unsigned long long> d_slot, d_spread;
     DevBuf<unsigned int> d_counter;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -126,6 +133,22 @@ struct pd_engine {
 
     // ---- one gap-tooth substep F -> out (patch nodes) -------------------
     void launch_step(const double* F, double* out, int out_mode, const double* srct, const int* fail) {
+        const bool sampled = samp_coef || samp_src;
+        if (prm.source == PD_SOURCE_GENERAL && !samp_src)
+            throw Status{PD_UNSUPPORTED, "general (non-separable) source: use the sampled step entries "
+                                         "(pd_gaptooth_step_sampled / pd_projective_step_sampled)"};
+        if (sampled) { // per-micro-step tables: the EXACT family reads them from HBM each step
+            if (step_kind == PD_STEP_LINEAR || prm.solver == PD_SOLVER_ADI)
+                throw Status{PD_UNSUPPORTED, "sampled coefficient/source tables: explicit micro-solver, direct step only"};
+            const size_t per_sub_c = (size_t)prm.nt * prm.nsets * PD_NCOEF * prm.N;
+            const size_t per_sub_s = (size_t)prm.nt * prm.nsets * prm.N;
+            k_gaptooth_exact<<<prm.P, exact_threads(prm), exact_smem_bytes(prm), stream>>>(
+                prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail, nullptr, nullptr,
+                d_adi_fac.p, samp_coef ? samp_coef + per_sub_c * sub_m : nullptr,
+                samp_src ? samp_src + per_sub_s * sub_m : nullptr);
+            check_launch();
+            return;
+        }
         if (step_kind == PD_STEP_LINEAR) {
             k_linear_step<<<(prm.P + 127) / 128, 128, 0, stream>>>(prm, F, out, out_mode, d_pij.p, d_roww.p, fail);
         } else if (mode == PD_MODE_FAST && fast.adi) {
@@ -163,6 +186,7 @@ struct pd_engine {
     }
     void gaptooth_step_dev(const double* in, double* out, const double* bnd, const double* srct, const int* fail) {
         copy_through(in, out);
+        sub_m = 0;
         launch_step(in, out, OUT_FIELD, srct, fail);
         launch_refresh(out, in, bnd, fail);
     }
@@ -172,6 +196,7 @@ struct pd_engine {
         const int k = prm.k;
         copy_through(in, out);
         if (k == 0) {
+            sub_m = 0;
             launch_step(in, out, OUT_PROJECTIVE, srct, fail);
             launch_refresh(out, in, bnd ? bnd + perim : nullptr, fail);
             return;
@@ -181,6 +206,7 @@ struct pd_engine {
         for (int m = 0; m <= k; ++m) {
             double* nxt = d_chain.p + NF * m;
             copy_through(prev, nxt);
+            sub_m = m;
             launch_step(prev, nxt, OUT_FIELD, srct ? srct + (size_t)prm.nt * m : nullptr, fail);
             launch_refresh(nxt, prev, bnd ? bnd + perim * m : nullptr, fail);
             prev = nxt;
@@ -574,6 +600,57 @@ pd_status pd_gaptooth_step(pd_engine* e, const double* U_in, double* U_out, doub
         download(U_out, e->d_U.p + NF, NF * 8, e->stream);
         CUDA_TRY(cudaStreamSynchronize(e->stream));
     });
+}
+
+namespace {
+// gap-tooth (substeps = 1) or projective (substeps = k+1) step over per-micro-step
+// sampled tables (microsim.cpp:537-542, 278-280), host buffers
+pd_status sampled_step(pd_engine* e, const double* U_in, double* U_out, const double* bnd,
+                       const double* coeff_steps, const double* source_steps, bool projective) {
+    if (!e || !U_in || !U_out || (!coeff_steps && !source_steps)) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        struct Reset {
+            pd_engine* e;
+            ~Reset() { e->samp_coef = e->samp_src = nullptr; }
+        } reset{e};
+        const size_t NF = e->NF;
+        const size_t subs = projective ? (size_t)e->prm.k + 1 : 1;
+        const size_t nc = coeff_steps ? subs * e->prm.nt * e->prm.nsets * PD_NCOEF * e->prm.N : 0;
+        const size_t ns = source_steps ? subs * e->prm.nt * e->prm.nsets * e->prm.N : 0;
+        e->d_samp.alloc(nc + ns);
+        if (nc) upload(e->d_samp.p, coeff_steps, nc * 8, e->stream);
+        if (ns) upload(e->d_samp.p + nc, source_steps, ns * 8, e->stream);
+        e->samp_coef = nc ? e->d_samp.p : nullptr;
+        e->samp_src = ns ? e->d_samp.p + nc : nullptr;
+        upload(e->d_U.p, U_in, NF * 8, e->stream);
+        const double* dbnd = nullptr;
+        if (bnd) {
+            const size_t n = e->perim * (projective ? (size_t)e->prm.k + 2 : 1);
+            e->d_bnd.alloc(n);
+            upload(e->d_bnd.p, bnd, n * 8, e->stream);
+            dbnd = e->d_bnd.p;
+        }
+        CUDA_TRY(cudaMemsetAsync(e->d_fail.p, 0, 8, e->stream));
+        if (projective)
+            e->projective_dev(e->d_U.p, e->d_U.p + NF, dbnd, nullptr, nullptr);
+        else
+            e->gaptooth_step_dev(e->d_U.p, e->d_U.p + NF, dbnd, nullptr, nullptr);
+        download(U_out, e->d_U.p + NF, NF * 8, e->stream);
+        CUDA_TRY(cudaStreamSynchronize(e->stream));
+    });
+}
+} // namespace
+
+pd_status pd_gaptooth_step_sampled(pd_engine* e, const double* U_in, double* U_out, double t, const double* bnd,
+                                   const double* coeff_steps, const double* source_steps) {
+    (void)t;
+    return sampled_step(e, U_in, U_out, bnd, coeff_steps, source_steps, false);
+}
+
+pd_status pd_projective_step_sampled(pd_engine* e, const double* U_in, double* U_out, double t, const double* bnd,
+                                     const double* coeff_steps, const double* source_steps) {
+    (void)t;
+    return sampled_step(e, U_in, U_out, bnd, coeff_steps, source_steps, true);
 }
 
 pd_status pd_projective_step_device(pd_engine* e, const double* in, double* out, double t, const double* bnd,

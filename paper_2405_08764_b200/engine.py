@@ -79,6 +79,9 @@ def lib() -> C.CDLL:
     L.pd_engine_step_kind.argtypes = [vp]
     L.pd_engine_step_kind.restype = C.c_int32
     L.pd_engine_set_run_guard.argtypes = [vp, C.c_double, C.c_int32]
+    L.pd_gaptooth_step_sampled.argtypes = [vp, _dp, _dp, C.c_double, _dp, _dp, _dp]
+    L.pd_projective_step_sampled.argtypes = [vp, _dp, _dp, C.c_double, _dp, _dp, _dp]
+    L.pd_problem_sample_substep.argtypes = [vp, C.c_double, _dp, _dp]
     L.pd_engine_mixed.argtypes = [vp]
     L.pd_engine_mixed.restype = C.c_int32
     L.pd_engine_launch_count.argtypes = [vp]
@@ -102,6 +105,7 @@ def lib() -> C.CDLL:
                  "pd_projective_step", "pd_projective_step_device", "pd_run", "pd_run_device",
                  "pd_integrate_batch", "pd_lift_batch", "pd_restrict_batch", "pd_evolve_batch",
                  "pd_linear_weights", "pd_engine_set_linear", "pd_engine_set_step_kind", "pd_engine_set_run_guard",
+                 "pd_gaptooth_step_sampled", "pd_projective_step_sampled", "pd_problem_sample_substep",
                  "pd_problem_create",
                  "pd_problem_resolved", "pd_problem_engine_desc", "pd_problem_initial_field",
                  "pd_problem_boundary", "pd_problem_boundary_table", "pd_problem_exact",
@@ -186,6 +190,27 @@ class Problem:
             return None
         _check(st)
         return U
+
+    def sample_substep(self, t0, coeffs=True, source=True):
+        """Per-micro-step samples of one substep from t0 (time-dependent
+        coefficients / general sources, microsim.cpp:537-542, 265-281):
+        (coeff_steps [nt][sets][6][n1][n2] or None, source_steps [nt][sets][n1][n2] or None)."""
+        ed = self.engine_desc()
+        nt, S, n1, n2 = ed.nt, ed.ncoeff_sets, ed.nx + 1, ed.ny + 1
+        c = np.empty((nt, S, abi.PD_NCOEF, n1, n2)) if coeffs else None
+        g = np.empty((nt, S, n1, n2)) if source else None
+        _check(lib().pd_problem_sample_substep(self.h, t0, _d(c), _d(g)))
+        return c, g
+
+    def sample_projective(self, t):
+        """[k+1] substeps (substep m from t + m tau) stacked for pd_projective_step_sampled."""
+        k, tau = self.desc.k, self.desc.tau
+        ed = self.engine_desc()
+        gen = ed.source_kind == abi.PD_SOURCE_GENERAL
+        parts = [self.sample_substep(t + m * tau, coeffs=True, source=gen) for m in range(k + 1)]
+        c = np.concatenate([p[0] for p in parts])
+        g = np.concatenate([p[1] for p in parts]) if gen else None
+        return c, g
 
     def stability(self):
         a, r = C.c_double(), C.c_double()
@@ -319,6 +344,26 @@ class Engine:
     @property
     def launch_count(self) -> int:
         return int(lib().pd_engine_launch_count(self.h))
+
+    def step_sampled(self, U, t, coeff_steps=None, source_steps=None, bnd=None):
+        """step_direct with per-micro-step sampled tables (pd_gaptooth_step_sampled)."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty_like(U)
+        c = None if coeff_steps is None else np.ascontiguousarray(coeff_steps, dtype=np.float64)
+        g = None if source_steps is None else np.ascontiguousarray(source_steps, dtype=np.float64)
+        b = None if bnd is None else np.ascontiguousarray(bnd, dtype=np.float64)
+        _check(lib().pd_gaptooth_step_sampled(self.h, _d(U), _d(out), t, _d(b), _d(c), _d(g)), self.h)
+        return out
+
+    def projective_step_sampled(self, U, t, coeff_steps=None, source_steps=None, bnd=None):
+        """cpi::projective_step with per-micro-step sampled tables ([k+1][nt]...)."""
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty_like(U)
+        c = None if coeff_steps is None else np.ascontiguousarray(coeff_steps, dtype=np.float64)
+        g = None if source_steps is None else np.ascontiguousarray(source_steps, dtype=np.float64)
+        b = None if bnd is None else np.ascontiguousarray(bnd, dtype=np.float64)
+        _check(lib().pd_projective_step_sampled(self.h, _d(U), _d(out), t, _d(b), _d(c), _d(g)), self.h)
+        return out
 
     def set_run_guard(self, scale0: float = 0.0, step_offset: int = 0):
         """Segmented cpi::run: later runs use 10 x max(scale0, 1e-12) as the

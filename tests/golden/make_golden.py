@@ -29,6 +29,10 @@ ref_linear.npz      configs 1 and 3 with the reference's DEFAULT linear_cache=au
                     GapToothEngine::step takes the linear-response shortcut
                     (gaptooth.cpp:377-418); first projective step and final
                     field of the full run, by the unmodified reference.
+ref_pulsed.npz      configs/pulsed_cdr.cfg (time-dependent coefficients + a general
+                    source, k = 0 and k = 1): step_direct and 6 projective
+                    steps by the UNMODIFIED reference (per-micro-step sampling
+                    inside PatchIntegrator::integrate, microsim.cpp:537-542).
 unit_cases.npz      PatchIntegrator::integrate / lift / restrict_average cases
                     run through the reference (known answers of
                     proj/tests/test_microsim.cpp and test_gaptooth.cpp).
@@ -178,6 +182,24 @@ def c4_full(O):
     print(f"c4 full oracle run: {prob.desc.Nt} steps, {time.perf_counter() - t0:.1f} s, {O.threads} threads")
 
 
+def ref_pulsed(ref):
+    out = {}
+    for k in (0, 1):
+        d, _ = configs.load("pulsed_cdr")
+        prob = Problem(configs.copy_desc(d, k=k))
+        R = ref.engine(prob.desc)
+        U0 = R.initial_field()
+        dt = prob.desc.T / prob.desc.Nt
+        out[f"k{k}_U0"] = U0
+        out[f"k{k}_S1"] = R.step_direct(U0, 0.0)
+        U = U0
+        for n in range(6):
+            U = R.projective_step(U, n * dt)
+            out[f"k{k}_U{n + 1}"] = U
+    np.savez_compressed(OUT / "ref_pulsed.npz", **out)
+    print("ref_pulsed:", len(out), "arrays")
+
+
 def unit_cases(ref):
     """Integrate / lift / restrict through the reference (fixtures for the GPU box)."""
     rng = np.random.default_rng(99)
@@ -219,6 +241,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["linear"]:
         ref_linear(ref)
         sys.exit(0)
+    if sys.argv[1:] == ["pulsed"]:
+        ref_pulsed(ref)
+        sys.exit(0)
     if sys.argv[1:] == ["c4full"]:
         c4_full(O)
         sys.exit(0)
@@ -233,4 +258,5 @@ if __name__ == "__main__":
     annulus()
     c4(O)
     c4_full(O)
+    ref_pulsed(ref)
     unit_cases(ref)
