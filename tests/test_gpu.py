@@ -748,6 +748,63 @@ def test_sharded_device_run_equals_single_engine(name, mode, gpu):
         assert np.array_equal(U.reshape(P.shape), Uref)
 
 
+def _nccl_shard_worker(rank, world, port, name, over, mode, nsteps, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_08764_b200 import configs, sharded
+    from paper_2405_08764_b200.engine import Engine, Problem
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dev = torch.device("cuda", rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    P = Problem(configs.copy_desc(configs.load(name)[0], **over))
+    ed = P.engine_desc()
+    sl = sharded.slabs(ed.Nxi, bool(ed.periodic_xi), world)[rank]
+    E = Engine(sharded.subset_desc(ed, sl), mode)
+    runner = sharded.device_runner(E, sl, ed, dist, dev)  # bench.py --gpus N's path
+    U0 = torch.from_numpy(P.initial_field().reshape(-1).copy()).to(dev)
+    res = runner.run_deferred(U0, nsteps, P.desc.T / P.desc.Nt)
+    out[rank] = (runner.gather(res.U).cpu().numpy(), res.steps_done, res.failed_step, E.P)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,over", [("c3_annulus", {}), ("c4_shear", {"N_xi": 65, "N_eta": 33, "Nt": 10})],
+                         ids=["c3", "c4-small"])
+@pytest.mark.parametrize("mode", [EXACT, FAST], ids=["exact", "fast"])
+def test_sharded_nccl_two_gpus_equals_single_engine(name, over, mode, gpu):
+    """bench.py --gpus 2's transport: one process per GPU, NCCL point-to-point halo
+    columns on the engine's stream and the deferred device guard; bit-identical
+    to the single-engine run.  Needs two visible GPUs (skipped on one)."""
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (NCCL refuses two ranks on one device)")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    world = 2
+    P = Problem(configs.copy_desc(configs.load(name)[0], **over))
+    nsteps = min(20, P.desc.Nt)
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_nccl_shard_worker, args=(world, port, name, over, mode, nsteps, out), nprocs=world, join=True)
+        res = dict(out)
+    E = Engine.from_problem(P, mode=mode)
+    Uref, _ = E.run(P.initial_field(), nsteps)
+    assert sum(res[r][3] for r in range(world)) == E.P
+    for r in range(world):
+        U, done, failed, _ = res[r]
+        assert failed == 0 and done == nsteps
+        assert np.array_equal(U.reshape(P.shape), Uref)
+
+
 # ---------------------------------------------------------------------------
 # maximum size: the largest config-5 patch count (2^20 patches of 32x32 micro
 # nodes, 103 GB of device tables) — size-independent properties on the device,
