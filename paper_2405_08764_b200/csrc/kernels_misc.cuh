@@ -11,37 +11,50 @@ namespace pdb200::dev {
 // boundary rows/columns (+ the seam column when periodic).  One perimeter
 // entry t; returns |value written| (0 when the entry writes nothing).
 // seam_by_patches: the fused run's column-0 patches write the seam interior.
-__device__ __forceinline__ double refresh_one(const Params& p, double* __restrict__ out, const double* __restrict__ F,
-                                              const double* __restrict__ bnd, int t, bool seam_by_patches) {
+// max of a 64-bit unsigned over the warp with two 32-bit redux.sync (REDUX):
+// the high words first, then the low words among the lanes holding that maximum
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+    const unsigned hi = (unsigned)(v >> 32);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? (unsigned)v : 0u);
+    return ((unsigned long long)mhi << 32) | mlo;
+}
+
+// Generic form: get(k) returns entry k of the perimeter row (S row, N row, W
+// column, E column, as refresh_one's bnd layout); has_bnd false keeps F's values.
+template <class Get>
+__device__ __forceinline__ double refresh_gen(const Params& p, double* __restrict__ out, const double* __restrict__ F,
+                                              bool has_bnd, Get get, int t, bool seam_by_patches) {
     const int N1 = p.Nxi, N2 = p.Neta, n2 = p.NF2;
     const int rows = 2 * (N1 + 1);
-    const double* S = bnd;
-    const double* Nn = bnd ? bnd + (N1 + 1) : nullptr;
-    const double* W = bnd ? bnd + 2 * (N1 + 1) : nullptr;
-    const double* E = bnd ? W + (N2 + 1) : nullptr;
     if (t < rows) { // S/N rows; corners are owned by the column pass (W/E or seam)
         const int i = t % (N1 + 1), j = t < N1 + 1 ? 0 : N2;
         if (p.periodic ? i == N1 : (i == 0 || i == N1)) return 0.0;
         const size_t node = (size_t)i * n2 + j;
-        const double v = bnd ? (j == 0 ? S[i] : Nn[i]) : F[node];
+        const double v = has_bnd ? (j == 0 ? get(i) : get(N1 + 1 + i)) : F[node];
         out[node] = v;
         return fabs(v);
     }
     const int u = t - rows, j = u % (N2 + 1), east = u >= N2 + 1;
+    const int W0 = 2 * (N1 + 1), E0 = W0 + N2 + 1;
     if (p.periodic) {
         if (!east) return 0.0; // column 0 holds patch results (or its boundary rows)
         double v;
-        if (j == 0) v = bnd ? S[0] : F[0];
-        else if (j == N2) v = bnd ? Nn[0] : F[N2];
+        if (j == 0) v = has_bnd ? get(0) : F[0];
+        else if (j == N2) v = has_bnd ? get(N1 + 1) : F[N2];
         else if (seam_by_patches) return 0.0;
         else v = out[j]; // patch (0,j) result, written before the refresh
         out[(size_t)N1 * n2 + j] = v;
         return fabs(v);
     }
     const size_t node = (size_t)(east ? N1 : 0) * n2 + j;
-    const double v = bnd ? (east ? E[j] : W[j]) : F[node];
+    const double v = has_bnd ? get(east ? E0 + j : W0 + j) : F[node];
     out[node] = v;
     return fabs(v);
+}
+__device__ __forceinline__ double refresh_one(const Params& p, double* __restrict__ out, const double* __restrict__ F,
+                                              const double* __restrict__ bnd, int t, bool seam_by_patches) {
+    return refresh_gen(p, out, F, bnd != nullptr, [&](int k) { return bnd[k]; }, t, seam_by_patches);
 }
 
 __device__ __forceinline__ void refresh_range(const Params& p, double* __restrict__ out, const double* __restrict__ F,
@@ -140,7 +153,7 @@ __global__ void k_exact_err(Params p, const double* __restrict__ U, const double
 __global__ void __launch_bounds__(1024)
 k_linear_run_block(Params p, double* __restrict__ U, const int* __restrict__ pij, const double* __restrict__ row_w,
                    const double* __restrict__ bnd, size_t perim, int nsteps, double blowup,
-                   unsigned long long* __restrict__ slot, int* __restrict__ fail) {
+                   unsigned long long* __restrict__ slot, int* __restrict__ fail, int full_field) {
     extern __shared__ double sfld[];
     __shared__ unsigned long long wm[32];
     __shared__ int s_stop;
@@ -149,9 +162,77 @@ k_linear_run_block(Params p, double* __restrict__ U, const int* __restrict__ pij
     auto B = [&](int b) { return sfld + NF * (size_t)(1 + b); };
     const int tid = threadIdx.x, nth = blockDim.x;
     for (size_t q = tid; q < NF; q += nth) A[q] = U[q];
+    double* const s_roww = sfld + NF * (size_t)(p.k == 0 ? 2 : 3); // [Neta+1][9], read every step
+    for (int q = tid; q < (p.Neta + 1) * 9; q += nth) s_roww[q] = row_w[q];
     if (tid == 0) s_stop = 0;
     __syncthreads();
     const int k = p.k;
+    if (k == 0 && full_field) { // every BASELINE config: one block barrier per macro step
+        // The substep, the extrapolation and the boundary refresh of step n only
+        // read the field of step n-1 (cur) and write the other buffer (nxt): each
+        // thread extrapolates its own patches right after their linear step (the
+        // column-0 patches also write the periodic seam), boundary threads refresh
+        // the perimeter of nxt from the table (or keep cur's values), and every
+        // written node enters the thread's max |U| — all nodes of the field are
+        // written, so it is the guard's max over the field.  One barrier, then
+        // every warp reduces the per-warp maxima (double-buffered by step parity)
+        // and takes the same guard decision.  Same operations on the same values
+        // as the phased loop below: bit-identical results and statistics.
+        __shared__ unsigned long long wm2[2][32];
+        const int lane = tid & 31, nw = nth >> 5;
+        const int nperim = 2 * (p.Nxi + 1) + 2 * (p.Neta + 1);
+        double* cur = A;
+        double* nxt = B(0);
+        // perimeter entries go to the threads after the patches' (when there are
+        // spare threads), so a step's critical path is one of the two, not both
+        const int t_off = p.P % nth;
+        // the first patch's indices stay in registers for the whole run
+        const int i0 = tid < p.P ? pij[2 * tid] : 0, j0 = tid < p.P ? pij[2 * tid + 1] : 0;
+        for (int n = 0; n < nsteps; ++n) {
+            const double* bn = bnd ? bnd + perim * 2 * (size_t)n : nullptr;
+            unsigned long long mx = 0;
+            for (int q = tid; q < p.P; q += nth) {
+                const int i = q == tid ? i0 : pij[2 * q], j = q == tid ? j0 : pij[2 * q + 1];
+                const double* w = s_roww + 9 * j;
+                double acc = 0.0;
+#pragma unroll
+                for (int dp = -1; dp <= 1; ++dp) {
+                    int ip = i + dp;
+                    if (p.periodic) ip = ((ip % p.Nxi) + p.Nxi) % p.Nxi;
+#pragma unroll
+                    for (int dq = -1; dq <= 1; ++dq)
+                        acc = XADD(acc, XMUL(w[3 * (dp + 1) + dq + 1], cur[(size_t)ip * p.NF2 + j + dq]));
+                }
+                const size_t node = (size_t)i * p.NF2 + j;
+                const double u = cur[node];
+                const double v = XADD(u, XMUL(p.dt_macro, XDIV(XSUB(acc, u), p.tau))); // cpi.cpp:54, 74
+                nxt[node] = v;
+                if (p.periodic && i == 0) nxt[(size_t)p.Nxi * p.NF2 + j] = v; // seam U(Nxi,j) = U(0,j)
+                mx = max(mx, (unsigned long long)__double_as_longlong(fabs(v)));
+            }
+            for (int t = (tid - t_off + nth) % nth; t < nperim; t += nth)
+                mx = max(mx, (unsigned long long)__double_as_longlong(refresh_one(p, nxt, cur, bn ? bn + perim : nullptr, t, true)));
+            mx = warp_max_u64(mx);
+            if (lane == 0) wm2[n & 1][tid >> 5] = mx;
+            __syncthreads();
+            mx = warp_max_u64(lane < nw ? wm2[n & 1][lane] : 0ull);
+            const bool nonfinite = mx >= 0x7FF0000000000000ull;
+            const bool trip = nonfinite || __longlong_as_double((long long)mx) > blowup;
+            if (tid == 0) {
+                slot[n] = mx;
+                if (trip) {
+                    fail[0] = n + 1;
+                    fail[1] = nonfinite ? 1 : 0;
+                }
+            }
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+            if (trip) break; // the field after the failing step, as the phased loop leaves it
+        }
+        for (size_t q = tid; q < NF; q += nth) U[q] = cur[q];
+        return;
+    }
     const double horizon = XSUB(p.dt_macro, XMUL((double)k, p.tau)); // as projective_dev computes it
     for (int n = 0; n < nsteps; ++n) {
         const double* bn = bnd ? bnd + perim * (size_t)(k + 2) * n : nullptr;
@@ -160,7 +241,7 @@ k_linear_run_block(Params p, double* __restrict__ U, const int* __restrict__ pij
             double* dst = B(m & 1);
             for (int q = tid; q < p.P; q += nth) {
                 const int i = pij[2 * q], j = pij[2 * q + 1];
-                const double* w = row_w + (size_t)9 * j;
+                const double* w = s_roww + 9 * j;
                 double acc = 0.0;
 #pragma unroll
                 for (int dp = -1; dp <= 1; ++dp) {

@@ -720,7 +720,8 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         const int64_t l0 = e->launches;
         // linear-response steps on a field that fits in shared memory: the whole
         // loop is one single-CTA kernel (k_linear_run_block), same results
-        const size_t block_smem = (e->prm.k == 0 ? 2 : 3) * NF * 8;
+        // fields (2 or 3) + the row weights [Neta+1][9] staged next to them
+        const size_t block_smem = ((e->prm.k == 0 ? 2 : 3) * NF + (size_t)(e->prm.Neta + 1) * 9) * 8;
         const bool block_run =
             !exact && e->step_kind == PD_STEP_LINEAR && nsteps > 0 && block_smem <= kLinearBlockSmemMax;
         // direct FAST steps (k = 0, full field): the whole run is one cooperative
@@ -747,8 +748,13 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         if (fused) {
         } else if (block_run) {
             raise_dyn_smem((const void*)k_linear_run_block, block_smem);
-            k_linear_run_block<<<1, 1024, block_smem, e->stream>>>(e->prm, U, e->d_pij.p, e->d_roww.p, bnd, e->perim,
-                                                                    nsteps, blowup, e->d_slot.p, e->d_fail.p);
+            // one thread per patch up to 1024 (every warp executes the per-step
+            // reductions: idle warps would only cost issue slots on the one SM)
+            const int nperim = 2 * (e->prm.Nxi + 1) + 2 * (e->prm.Neta + 1);
+            const int lin_threads = std::min(1024, std::max(64, (std::max((int)e->prm.P, nperim) + 31) / 32 * 32));
+            k_linear_run_block<<<1, lin_threads, block_smem, e->stream>>>(e->prm, U, e->d_pij.p, e->d_roww.p, bnd, e->perim,
+                                                                    nsteps, blowup, e->d_slot.p, e->d_fail.p,
+                                                                    e->subset ? 0 : 1);
             e->check_launch();
         } else {
             double* cur = U;

@@ -1,7 +1,7 @@
 """Linear-response path (GapToothEngine::step with linear_cache) on the B200 vs the
-unmodified reference's own fast path on one host core.  Writes profiles/r01_linear_path.jsonl.
+unmodified reference's own fast path on one host core.  Writes profiles/<tag>_linear_path.jsonl.
 
-  python scripts/bench_linear.py [steps]
+  python scripts/bench_linear.py [steps] [tag]
 """
 import json, sys, time
 from pathlib import Path
@@ -41,4 +41,4 @@ for name in ["c1_diffusion", "c3_annulus", "ref_annulus_16x10"]:
         rec["ref_cores"] = 1
     out.append(rec)
     print(json.dumps(rec), flush=True)
-(ROOT / "profiles" / "r01_linear_path.jsonl").write_text("".join(json.dumps(r) + "\n" for r in out))
+(ROOT / "profiles" / f"{sys.argv[2] if len(sys.argv) > 2 else 'r02'}_linear_path.jsonl").write_text("".join(json.dumps(r) + "\n" for r in out))
