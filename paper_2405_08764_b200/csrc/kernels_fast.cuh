@@ -582,7 +582,7 @@ constexpr int kRunWarps = 4;
 __device__ __forceinline__ bool guard_trips(unsigned long long v, int step, int gw, int lane, double blowup,
                                             unsigned long long* slot, int* fail) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v = max(v, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)v, o));
+    v = warp_max_u64(v);
     if (gw == 0 && lane == 0) slot[step] = v;
     const bool nonfinite = v >= 0x7FF0000000000000ull;
     if (nonfinite || __longlong_as_double((long long)v) > blowup) {
@@ -650,7 +650,7 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
         for (int t = gw * 32 + lane; t < nperim; t += nw * 32)
             m = max(m, (unsigned long long)__double_as_longlong(refresh_one(p, out, F, bn, t, true)));
 #pragma unroll
-        for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)m, o));
+        m = warp_max_u64(m);
         if (lane == 0) atomicMax(spread + (size_t)n * kGuardSpread + gw % kGuardSpread, m);
         // the guard decision of step n-1 is taken here, one step late: its maximum
         // was loaded right after the previous barrier, so the L2 round trip hid
@@ -671,7 +671,7 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
                 em = max(em, (unsigned long long)__double_as_longlong(pct));
             }
 #pragma unroll
-            for (int o = 16; o; o >>= 1) em = max(em, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)em, o));
+            em = warp_max_u64(em);
             if (lane == 0 && em) atomicMax(err + n, em);
         }
     }

@@ -91,7 +91,7 @@ __global__ void k_guard(const double* __restrict__ U, size_t n, unsigned long lo
     unsigned long long m = 0;
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x)
         m = max(m, (unsigned long long)__double_as_longlong(fabs(U[t])));
-    for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)m, o));
+    m = warp_max_u64(m);
     __shared__ unsigned long long wm[32];
     if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -132,7 +132,7 @@ __global__ void k_exact_err(Params p, const double* __restrict__ U, const double
         const double pct = __dmul_rn(__ddiv_rn(fabs(__dsub_rn(U[node], e)), fabs(e)), 100.0);
         m = max(m, (unsigned long long)__double_as_longlong(pct));
     }
-    for (int o = 16; o; o >>= 1) m = max(m, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)m, o));
+    m = warp_max_u64(m);
     __shared__ unsigned long long wm[32];
     if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -276,7 +276,7 @@ k_linear_run_block(Params p, double* __restrict__ U, const int* __restrict__ pij
         // blow-up guard (cpi.cpp:187-202), max |U| as a non-negative bit pattern
         unsigned long long mx = 0;
         for (size_t q = tid; q < NF; q += nth) mx = max(mx, (unsigned long long)__double_as_longlong(fabs(A[q])));
-        for (int o = 16; o; o >>= 1) mx = max(mx, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
+        mx = warp_max_u64(mx);
         if ((tid & 31) == 0) wm[tid >> 5] = mx;
         __syncthreads();
         if (tid == 0) {
