@@ -10,11 +10,15 @@ micro nodes, K = 50 micro-steps, 9-point non-orthogonal CDR, FP64).
                   [--config c4_shear] [--no-cpu-baseline] [--sweep]
 
 N = 1: the device-resident single-engine loop (pd_run_device).  N > 1 is
-launched by torchrun (one process per GPU, NCCL): the workload is split into
+launched by torchrun (one process per GPU): the workload is split into
 xi-slabs of patch columns (sharded.py), every rank advances its own
-patches and exchanges one macro column with each neighbour per step (NCCL
-point-to-point on the engine's stream) plus a device-side all-reduce(max)
-guard — strong scaling, value = all patches' updates / max-over-ranks time.
+patches and its step kernel stores its two edge columns straight into the
+neighbours' field buffers (CUDA IPC mappings over NVLink/NVSwitch) and bumps
+their link counters; each rank's stream waits on its own counters before the
+next step (pd_projective_step_halo / pd_stream_wait_flag), with one
+all-reduce(max) guard per run (--exchange nccl: NCCL point-to-point halo
+columns instead) — strong scaling, value = all patches' updates /
+max-over-ranks time.
 
 --impl reference times the reference's CPU implementation of the path on this
 host's cores: for the shear-cdr workloads (configs 4/5, whose mixed term the
@@ -476,7 +480,11 @@ def run_single(args, desc):
 
 
 def run_sharded(args, desc, rank, world, local):
-    """N > 1: xi-slab strong scaling (sharded.py) with NCCL halo columns."""
+    """N > 1: xi-slab strong scaling (sharded.py).  Default exchange: the fused
+    peer-memory halo (each rank's step kernel stores its edge columns into the
+    neighbours' buffers over NVLink/NVSwitch through CUDA IPC mappings; the
+    streams wait on link counters; no NCCL in the loop).  --exchange nccl: NCCL
+    point-to-point halo columns (the baseline)."""
     import torch
     import torch.distributed as dist
 
@@ -492,10 +500,36 @@ def run_sharded(args, desc, rank, world, local):
     P, N, K = workload(r)
     sl = sharded.slabs(ed.Nxi, bool(ed.periodic_xi), world)[rank]
     eng = Engine(sharded.subset_desc(ed, sl))
-    runner = sharded.device_runner(eng, sl, ed, dist, dev)
-    U0 = torch.from_numpy(prob.initial_field().reshape(-1).copy()).to(dev)
+    # one node, one process per GPU: the neighbour rank's device is its rank
+    ndev = torch.cuda.device_count()
+    peer_ok = args.exchange == "peer" and all(nb < ndev and nb != local and torch.cuda.can_device_access_peer(local, nb)
+                                              for _, nb, _ in sharded.halo_links(sl))
+    ok = torch.tensor([1.0 if peer_ok else 0.0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    use_peer = bool(ok.item())
     dt = r.T / r.Nt
-    runner.run_deferred(U0.clone(), args.warmup, dt)
+    U0 = torch.from_numpy(prob.initial_field().reshape(-1).copy()).to(dev)
+    if use_peer:
+        run = sharded.peer_runner(eng, sl, ed.Neta, dist, dev)
+
+        def red(x):
+            t = x.detach().to(dev).clone()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.cpu()
+
+        def go(U, n, t0=0.0):
+            return sharded.run_peer([run], [U], n, dt, t0, reduce_max=red, barrier=dist.barrier)[0]
+        exchange = ("fused peer-memory halo: the step kernel stores its edge columns into the neighbours' field "
+                    "buffers (CUDA IPC over NVLink/NVSwitch) and bumps their link counters; streams wait on "
+                    "counters (cuStreamWaitValue32); one all-reduce(max) guard per run")
+    else:
+        runner = sharded.device_runner(eng, sl, ed, dist, dev)
+
+        def go(U, n, t0=0.0):
+            return runner.run_deferred(U, n, dt, t0)
+        exchange = ("NCCL point-to-point halo columns (one macro column per neighbour per step) + "
+                    "device all-reduce(max) guard, on the engine's stream")
+    go(U0.clone(), args.warmup)
     dist.barrier()
     torch.cuda.synchronize()
 
@@ -505,7 +539,7 @@ def run_sharded(args, desc, rank, world, local):
     l0 = eng.launch_count
     dist.barrier()
     torch.cuda.synchronize()
-    res = runner.run_deferred(U, args.steps, dt)
+    res = go(U, args.steps)
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
@@ -522,7 +556,7 @@ def run_sharded(args, desc, rank, world, local):
     t0 = time.perf_counter()
     for n in range(ke):
         Ud = Uh.to(dev, non_blocking=True)
-        Ud = runner.run_deferred(Ud, 1, dt, t0=n * dt).U
+        Ud = go(Ud, 1, n * dt).U
         Uh.copy_(Ud)
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
@@ -530,7 +564,7 @@ def run_sharded(args, desc, rank, world, local):
     NF = Uh.numel()
     e2e = {"value": P * N * K * ke / float(e2e_s.item()), "unit": UNIT, "h2d_bytes_per_step": NF * 8,
            "d2h_bytes_per_step": NF * 8, "steps": ke,
-           "path": "host field (pinned) -> per-rank slab step + NCCL halo exchange -> host, each step"}
+           "path": "host field (pinned) -> per-rank slab step + halo exchange -> host, each step"}
     mine = torch.tensor([eng.P], device=dev, dtype=torch.float64)
     most = mine.clone()
     dist.all_reduce(most, op=dist.ReduceOp.MAX)
@@ -541,11 +575,12 @@ def run_sharded(args, desc, rank, world, local):
                 "config": bench_config(args.config, desc, world),
                 "kernel_family": "fast" if eng.mode == abi.PD_MODE_FAST else "exact",
                 "patches_per_rank_max": int(most.item()), "steps_done": res.steps_done,
-                "failed_step": res.failed_step,
-                "exchange": "NCCL point-to-point halo columns (one macro column per neighbour per step) + "
-                            "device all-reduce(max) guard, on the engine's stream",
+                "failed_step": res.failed_step, "exchange": exchange,
                 "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
         print(json.dumps(line), flush=True)
+    if use_peer:
+        dist.barrier()
+        sharded.close_peer_runner(run)
     dist.destroy_process_group()
     return 0
 
@@ -563,6 +598,8 @@ def main():
     ap.add_argument("--sweep-max-log2", type=int, default=0)
     ap.add_argument("--sweep-nodes", default="")
     ap.add_argument("--tag", default="r02")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: fused peer-memory halo (default) or NCCL point-to-point halo columns")
     args = ap.parse_args()
     if args.sweep:
         return run_sweep(args)

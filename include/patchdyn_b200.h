@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define PD_ABI_VERSION 4
+#define PD_ABI_VERSION 5
 
 /* Status codes map 1:1 onto the reference exception types
  * (proj/include/patchdyn/errors.hpp:9-61). */
@@ -314,6 +314,44 @@ pd_status pd_projective_step_sampled(pd_engine* e, const double* U_in, double* U
  * names the run's step and time ("macro step n (t=...)", cpi.cpp:196-200).
  * pd_run_stats.failed_step stays relative to the call. */
 pd_status pd_engine_set_run_guard(pd_engine* e, double scale0, int32_t step_offset);
+
+/* ---------------------------------------------------------------------------
+ * Decomposed run over xi-slabs with a fused peer-memory halo exchange
+ * (DESIGN.md §6).  No reference analogue: the reference's serial
+ * patch loop (gaptooth.cpp:362-372) is split into contiguous slabs of patch
+ * columns, one engine (a patch subset) per rank/GPU.  Each rank's macro field
+ * buffers hold its own columns, the two halo columns and the boundary.
+ *
+ * pd_projective_step_halo: pd_projective_step_device (k = 0) whose step kernel
+ *   ALSO stores every result of a patch in column halo->column[l] into
+ *   halo->dst[l] (the neighbour's output buffer of this step — a peer pointer
+ *   over NVLink/NVSwitch, or a CUDA IPC mapping) at the same node index, then,
+ *   after a system-scope fence, adds 1 to *halo->flag[l] (the neighbour's
+ *   counter for this link) — one fused kernel, no separate exchange, no NCCL.
+ *   U_out is NOT pre-filled from U_in (columns the rank does not own are only
+ *   ever written by their owners); the boundary is refreshed as usual.
+ * pd_stream_wait_flag: the engine's stream waits (a stream memory operation
+ *   in the front end: no kernel spins, no host round trip) until
+ *   (int32_t)(*flag_dev - value) >= 0.  A link's counter reaches
+ *   (n+1)*(Neta-1) when the neighbour's step n has stored (and finished
+ *   reading) that column, so waiting for n*(Neta-1) on both links before step
+ *   n orders both the halo reads and the overwrite of the neighbour's buffer.
+ * pd_ipc_alloc / pd_ipc_open / pd_ipc_close / pd_device_free: device buffers
+ *   shareable across the processes of a one-process-per-GPU run
+ *   (cudaIpcGetMemHandle, 64-byte handles; opened with lazy peer access). */
+typedef struct pd_halo_out {
+    int32_t nlinks;      /* 0, 1 or 2 */
+    int32_t column[2];   /* macro column i (an edge column of this slab) */
+    double* dst[2];      /* neighbour's field buffer receiving this step's output */
+    uint32_t* flag[2];   /* neighbour's counter for this link */
+} pd_halo_out;
+pd_status pd_projective_step_halo(pd_engine* e, const double* U_in_dev, double* U_out_dev, double t,
+                                  const double* bnd_dev, const double* src_time_dev, const pd_halo_out* halo);
+pd_status pd_stream_wait_flag(pd_engine* e, const uint32_t* flag_dev, uint32_t value);
+pd_status pd_ipc_alloc(size_t bytes, void** dev_ptr, unsigned char handle_out[64]);
+pd_status pd_ipc_open(const unsigned char handle[64], void** dev_ptr);
+pd_status pd_ipc_close(void* dev_ptr);
+pd_status pd_device_free(void* dev_ptr);
 
 /* ---------------------------------------------------------------------------
  * Host problem builder: the B200 framework's own mesh/metric setup for the

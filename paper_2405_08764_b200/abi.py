@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes as C
 
-PD_ABI_VERSION = 4
+PD_ABI_VERSION = 5
 
 # pd_status  (errors.hpp:9-61 mapping)
 PD_OK = 0
@@ -93,6 +93,14 @@ class ProblemDesc(C.Structure):
         ("threads", C.c_int32),
         ("solver", C.c_int32), ("upwind_order", C.c_int32), ("upwind_r", C.c_double),
         ("coeff_gen", C.c_int32),
+    ]
+
+
+class HaloOut(C.Structure):
+    """pd_halo_out: the fused peer-memory halo links of one decomposed step."""
+    _fields_ = [
+        ("nlinks", C.c_int32), ("column", C.c_int32 * 2),
+        ("dst", C.c_void_p * 2), ("flag", C.c_void_p * 2),
     ]
 
 

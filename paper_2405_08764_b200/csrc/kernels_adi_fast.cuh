@@ -373,8 +373,11 @@ k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int
         const size_t node = (size_t)__ldg(nbr + 9 * patch + 4);
         if (out_mode == 0) {
             out[node] = part;
+            halo_store(p, node, part);
         } else if (out_mode == 1) {
-            out[node] = __fma_rn(p.dt_macro, __ddiv_rn(__dsub_rn(part, v[4]), p.tau), v[4]); // cpi.cpp:54, 74
+            const double w = __fma_rn(p.dt_macro, __ddiv_rn(__dsub_rn(part, v[4]), p.tau), v[4]); // cpi.cpp:54, 74
+            out[node] = w;
+            halo_store(p, node, w);
         } else {
             out[patch] = part;
         }

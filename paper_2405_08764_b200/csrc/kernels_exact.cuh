@@ -157,10 +157,13 @@ k_gaptooth_exact(Params p, const double* __restrict__ F, double* __restrict__ ou
         const size_t node = (size_t)i * p.NF2 + j;
         if (out_mode == OUT_FIELD) {
             out[node] = avg;
+            halo_store(p, node, avg);
         } else if (out_mode == OUT_PROJECTIVE) {
             const double U = F[node];
             const double Fd = XDIV(XSUB(avg, U), p.tau); // estimate_derivative  cpi.cpp:54
-            out[node] = XADD(U, XMUL(p.dt_macro, Fd));  // cpi.cpp:74 with k = 0
+            const double w = XADD(U, XMUL(p.dt_macro, Fd)); // cpi.cpp:74 with k = 0
+            out[node] = w;
+            halo_store(p, node, w); // decomposed run: fused peer-memory halo
         } else {
             out[item] = avg;
         }
@@ -191,10 +194,10 @@ __global__ void k_linear_step(Params p, const double* __restrict__ F, double* __
     const size_t node = (size_t)i * p.NF2 + j;
     if (out_mode == OUT_PROJECTIVE) {
         const double U = F[node];
-        out[node] = XADD(U, XMUL(p.dt_macro, XDIV(XSUB(acc, U), p.tau))); // cpi.cpp:54, 74 (k = 0)
-    } else {
-        out[node] = acc;
+        acc = XADD(U, XMUL(p.dt_macro, XDIV(XSUB(acc, U), p.tau))); // cpi.cpp:54, 74 (k = 0)
     }
+    out[node] = acc;
+    halo_store(p, node, acc);
 }
 
 // PatchIntegrator::integrate batched (microsim.cpp:509-552): u0/edges given.

@@ -517,6 +517,7 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
         } else {
             out[patch] = written = avg;
         }
+        if (out_mode <= 1) halo_store(p, node, written); // decomposed run: fused peer-memory halo
     }
     return fabs(written);
 #undef WT

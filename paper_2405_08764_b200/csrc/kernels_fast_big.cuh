@@ -431,9 +431,12 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
         const size_t node = (size_t)idx[4];
         if (out_mode == 0) {
             out[node] = avg;
+            halo_store(p, node, avg);
         } else if (out_mode == 1) {
             const double U = v[4];
-            out[node] = U + p.dt_macro * ((avg - U) / p.tau); // cpi.cpp:54, 74 (k = 0)
+            const double w = U + p.dt_macro * ((avg - U) / p.tau); // cpi.cpp:54, 74 (k = 0)
+            out[node] = w;
+            halo_store(p, node, w); // decomposed run: fused peer-memory halo
         } else {
             out[patch] = avg;
         }

@@ -45,7 +45,32 @@ struct Params {
     double vlag[4][3];   // Lagrange value weights at +-h/2 across each edge (E, W, N, S): edge values
     double cedge[4];     // Robin ghost coefficient cEdge = -sign 2 delta w1/w2 per edge (microsim.cpp:180)
     int pinned;          // the patch edges pin their nodes (Dirichlet, or Robin with w2 ~ 0)
+    // fused peer-memory halo of a decomposed run (pd_projective_step_halo): the
+    // results of the patches in column halo_col[l] also go to halo_dst[l] (the
+    // neighbour's buffer), each followed by a system-scope fence and +1 on
+    // *halo_flag[l]; halo_n = 0 everywhere else
+    int halo_n;
+    int halo_col[2];
+    double* halo_dst[2];
+    unsigned int* halo_flag[2];
 };
+
+// Store v (the result at macro node `node`) into the neighbours' buffers when
+// the node lies in a halo link's column, then publish it: fence.sc.sys orders
+// the (NVLink / IPC) store before the counter increment the neighbour's stream
+// waits on (pd_stream_wait_flag).  A uniform no-op when halo_n == 0.
+__device__ __forceinline__ void halo_store(const Params& p, size_t node, double v) {
+    if (!p.halo_n) return;
+    const int i = (int)(node / (size_t)p.NF2);
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+        if (l < p.halo_n && i == p.halo_col[l]) {
+            p.halo_dst[l][node] = v;
+            __threadfence_system();
+            atomicAdd_system(p.halo_flag[l], 1u);
+        }
+    }
+}
 
 // One micro edge condition in shared memory (EdgeCondition + Ghost,
 // microsim.hpp:32-37, microsim.cpp:146-150).

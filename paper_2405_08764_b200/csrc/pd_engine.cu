@@ -4,6 +4,7 @@
 // table upload, kernel selection and launch, device-resident macro loop.
 // The kernels live in kernels_exact.cuh (reference-order EXACT mode),
 // kernels_fast.cuh (register-blocked FAST mode) and kernels_misc.cuh.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1057,6 +1058,134 @@ pd_status pd_engine_set_run_guard(pd_engine* e, double scale0, int32_t step_offs
     e->guard_scale = scale0 > 0.0 ? scale0 : 0.0;
     e->step_offset = step_offset;
     return PD_OK;
+}
+
+} // extern "C"
+
+// ---------------------------------------------------------------------------
+// Decomposed run: fused peer-memory halo exchange
+// ---------------------------------------------------------------------------
+namespace {
+// cuStreamWaitValue32 through the runtime's driver entry point (the library
+// does not link libcuda; the symbol resolves on the GPU host's driver)
+using WaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32 wait_value32() {
+    static WaitValue32 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return (WaitValue32) nullptr;
+        }
+        return reinterpret_cast<WaitValue32>(f);
+    }();
+    return fn;
+}
+
+// The halo link of one call lives in the engine's Params for that call only.
+struct HaloScope {
+    Params& p;
+    HaloScope(Params& prm, const pd_halo_out& h) : p(prm) {
+        p.halo_n = h.nlinks;
+        for (int l = 0; l < 2; ++l) {
+            p.halo_col[l] = l < h.nlinks ? h.column[l] : -1;
+            p.halo_dst[l] = l < h.nlinks ? h.dst[l] : nullptr;
+            p.halo_flag[l] = l < h.nlinks ? h.flag[l] : nullptr;
+        }
+    }
+    ~HaloScope() {
+        p.halo_n = 0;
+        p.halo_col[0] = p.halo_col[1] = -1;
+        p.halo_dst[0] = p.halo_dst[1] = nullptr;
+        p.halo_flag[0] = p.halo_flag[1] = nullptr;
+    }
+};
+
+template <class F>
+pd_status guarded_free(F&& fn) {
+    try {
+        fn();
+        return PD_OK;
+    } catch (const Status& s) {
+        pdb200::set_global_error(s.msg);
+        return s.code;
+    }
+}
+} // namespace
+
+extern "C" {
+
+pd_status pd_projective_step_halo(pd_engine* e, const double* in, double* out, double t, const double* bnd,
+                                  const double* src_time, const pd_halo_out* h) {
+    (void)t;
+    if (!e || !in || !out || !h || in == out || h->nlinks < 0 || h->nlinks > 2) return PD_VALIDATION_ERROR;
+    for (int l = 0; l < h->nlinks; ++l)
+        if (!h->dst[l] || !h->flag[l] || h->column[l] < 0 || h->column[l] > e->prm.Nxi) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        if (e->prm.k != 0)
+            throw Status{PD_UNSUPPORTED, "halo-exchanging projective step: k = 0 only (one exchange per step)"};
+        if (e->step_kind == PD_STEP_DIRECT && e->prm.source == PD_SOURCE_GENERAL)
+            throw Status{PD_UNSUPPORTED, "halo-exchanging projective step: no general source"};
+        HaloScope scope(e->prm, *h);
+        // no copy-through: U_out's own columns come from the step kernel, its halo
+        // columns from the neighbours' kernels, its boundary from the refresh
+        e->sub_m = 0;
+        e->launch_step(in, out, OUT_PROJECTIVE, e->prm.source ? src_time : nullptr, nullptr);
+        e->launch_refresh(out, in, bnd ? bnd + e->perim : nullptr, nullptr);
+    });
+}
+
+pd_status pd_stream_wait_flag(pd_engine* e, const uint32_t* flag, uint32_t value) {
+    if (!e || !flag) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        const WaitValue32 fn = wait_value32();
+        if (!fn) throw Status{PD_CUDA_ERROR, "cuStreamWaitValue32 is not available from the driver"};
+        int dev = 0, flush = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        CUDA_TRY(cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, dev));
+        const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
+        const CUresult r = fn(reinterpret_cast<CUstream>(e->stream), reinterpret_cast<CUdeviceptr>(flag), value, flags);
+        if (r != CUDA_SUCCESS)
+            throw Status{PD_CUDA_ERROR, "cuStreamWaitValue32 failed (CUresult " + std::to_string((int)r) + ")"};
+    });
+}
+
+pd_status pd_ipc_alloc(size_t bytes, void** dptr, unsigned char handle[64]) {
+    if (!dptr || !handle || !bytes) return PD_VALIDATION_ERROR;
+    return guarded_free([&] {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+        void* p = nullptr;
+        CUDA_TRY(cudaMalloc(&p, bytes));
+        CUDA_TRY(cudaMemset(p, 0, bytes));
+        cudaIpcMemHandle_t h{};
+        const cudaError_t err = cudaIpcGetMemHandle(&h, p);
+        if (err != cudaSuccess) {
+            cudaFree(p);
+            throw Status{PD_CUDA_ERROR, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(err)};
+        }
+        std::memcpy(handle, &h, 64);
+        *dptr = p;
+    });
+}
+
+pd_status pd_ipc_open(const unsigned char handle[64], void** dptr) {
+    if (!dptr || !handle) return PD_VALIDATION_ERROR;
+    return guarded_free([&] {
+        cudaIpcMemHandle_t h{};
+        std::memcpy(&h, handle, 64);
+        CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+pd_status pd_ipc_close(void* dptr) {
+    if (!dptr) return PD_VALIDATION_ERROR;
+    return guarded_free([&] { CUDA_TRY(cudaIpcCloseMemHandle(dptr)); });
+}
+
+pd_status pd_device_free(void* dptr) {
+    if (!dptr) return PD_VALIDATION_ERROR;
+    return guarded_free([&] { CUDA_TRY(cudaFree(dptr)); });
 }
 
 } // extern "C"

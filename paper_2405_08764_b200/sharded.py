@@ -24,6 +24,7 @@ the restated oracle.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -313,3 +314,243 @@ def device_runner(engine, slab: Slab, ed: EngineDesc, dist, device, group=None) 
     _check(lib().pd_engine_set_stream(engine.h, stream.cuda_stream), engine.h)
     step = device_step_fn(engine, ed.k, engine.perim, device)
     return ShardedRun(slab, ed.Neta, step, dist, group=group, k=ed.k)
+
+
+# ---------------------------------------------------------------------------
+# Fused peer-memory halo exchange (pd_projective_step_halo):
+# the step kernel of each rank stores its edge columns straight into the
+# neighbours' field buffers (NVLink peer / CUDA IPC mappings) and bumps their
+# link counters; each rank's stream waits on its own counters (stream memory
+# operations) before the next step.  No NCCL, no host round trip per step.
+# ---------------------------------------------------------------------------
+FROM_LEFT, FROM_RIGHT = 0, 1  # a rank's two incoming link counters
+
+
+def halo_links(slab: Slab):
+    """Outgoing links of a rank: (column, neighbour rank, the neighbour's
+    counter side).  My last column is my right neighbour's left halo; my first
+    column is my left neighbour's right halo (gaptooth.cpp:74-104's 3x3
+    stencil reads one column on each side; periodic xi wraps)."""
+    out = []
+    if slab.right() is not None:
+        out.append((slab.i1 - 1, slab.right(), FROM_LEFT))
+    if slab.left() is not None:
+        out.append((slab.i0, slab.left(), FROM_RIGHT))
+    return out
+
+
+def incoming_sides(slab: Slab):
+    """Counters this rank waits on before each step."""
+    return [s for s, nb in ((FROM_LEFT, slab.left()), (FROM_RIGHT, slab.right())) if nb is not None]
+
+
+class _DevArray:
+    """A raw device allocation seen by torch (__cuda_array_interface__ v3)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _as_tensor(ptr: int, n: int, typestr: str, device):
+    import torch
+
+    return torch.as_tensor(_DevArray(ptr, n, typestr), device=device)
+
+
+class PeerRun:
+    """One rank of the cpi::run macro loop (cpi.cpp:175-202) over xi-slabs with
+    the fused peer-memory halo.  X[0], X[1]: this rank's ping-pong field
+    buffers; flags: its two incoming link counters (uint32); peers[rank] =
+    (X0 ptr, X1 ptr, flags ptr) of every neighbour.  reduce_max / barrier are
+    the collective hooks (torch.distributed, or the in-process driver)."""
+
+    def __init__(self, engine, slab: Slab, Neta: int, X, flags, peers, stream, mask):
+        self.e = engine
+        self.s = slab
+        self.n2 = Neta + 1
+        self.npc = Neta - 1  # patches per column: one counter increment each per step
+        self.X = X
+        self.flags = flags
+        self.stream = stream
+        self.mask = mask
+        self.steps_total = 0  # counters are cumulative over the runner's life
+        self.links = []
+        for col, nb, side in halo_links(slab):
+            x0, x1, fl = peers[nb]
+            self.links.append((col, (x0, x1), fl + 4 * side))
+        self.sides = incoming_sides(slab)
+        from .engine import _check, lib
+
+        _check(lib().pd_engine_set_stream(engine.h, stream.cuda_stream), engine.h)
+
+    def begin(self, U0):
+        """Load the run's initial field into both buffers (stream-ordered)."""
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            self.X[0].copy_(U0)
+            self.X[1].copy_(U0)
+
+    def enqueue_step(self, n: int, t: float, bnd, maxes):
+        """Step n of the current run: wait for both neighbours' step n-1, the fused
+        step (own patches + edge columns into the neighbours' buffers + counter
+        bumps), the boundary refresh, and this rank's max |U| into maxes[n]."""
+        import torch
+
+        from . import abi
+        from .engine import _check, lib
+
+        L, h = lib(), self.e.h
+        target = ((self.steps_total + n) * self.npc) & 0xFFFFFFFF
+        if n > 0 or self.steps_total > 0:
+            for side in self.sides:
+                _check(L.pd_stream_wait_flag(h, self.flags.data_ptr() + 4 * side, target), h)
+        out = (n + 1) % 2
+        halo = abi.HaloOut()
+        halo.nlinks = len(self.links)
+        for l, (col, xs, fl) in enumerate(self.links):
+            halo.column[l] = col
+            halo.dst[l] = xs[out]
+            halo.flag[l] = fl
+        b = None
+        if bnd is not None:
+            with torch.cuda.stream(self.stream):
+                b = torch.as_tensor(np.ascontiguousarray(bnd).reshape(-1)).to(self.X[0].device, non_blocking=True)
+        _check(L.pd_projective_step_halo(h, self.X[n % 2].data_ptr(), self.X[out].data_ptr(), t,
+                                         None if b is None else b.data_ptr(), None, C.byref(halo)), h)
+        with torch.cuda.stream(self.stream):
+            m = torch.where(self.mask, self.X[out].abs(), torch.zeros((), dtype=torch.float64,
+                                                                        device=self.X[0].device)).amax()
+            maxes[n] = torch.where(torch.isfinite(m), m, torch.full_like(m, float("inf")))
+        return b
+
+    def result(self, nsteps: int):
+        return self.X[nsteps % 2]
+
+
+def _peer_guard(U0, mask, reduce_max):
+    import torch
+
+    m0 = torch.where(mask, U0.abs(), torch.zeros((), dtype=U0.dtype, device=U0.device)).amax().reshape(1)
+    return 10.0 * max(float(reduce_max(m0).max().item()), 1e-12)  # cpi.cpp:142-144
+
+
+def run_peer(runners, U0s, nsteps: int, dt: float, t0: float = 0.0, bnd_table=None, reduce_max=None,
+             barrier=None) -> list[RunResult]:
+    """Drive the ranks in `runners` (all ranks of an in-process group, or this
+    process's one rank with torch.distributed hooks) through nsteps projective
+    steps.  The guard (cpi.cpp:187-202) is taken after the loop from the
+    per-step maxima (one reduction), as ShardedRun.run_deferred; on a trip the
+    run is replayed up to the failing step, so the field is the one after it."""
+    import torch
+
+    reduce_max = reduce_max or (lambda x: x)
+    barrier = barrier or (lambda: None)
+    blowup = _peer_guard(torch.stack([U0.reshape(-1) for U0 in U0s]).reshape(-1) if len(U0s) > 1 else U0s[0],
+                         torch.cat([r.mask for r in runners]) if len(runners) > 1 else runners[0].mask, reduce_max)
+
+    def loop(steps):
+        for r, U0 in zip(runners, U0s):
+            r.begin(U0)
+        for r in runners:
+            r.stream.synchronize()
+        barrier()  # every buffer holds U0 before any neighbour stores into it
+        maxes = [torch.zeros(max(steps, 1), dtype=torch.float64, device=r.X[0].device) for r in runners]
+        evs = []
+        for r in runners:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(r.stream)
+            evs.append(ev)
+        keep = []
+        for n in range(steps):
+            for r, mx in zip(runners, maxes):
+                keep.append(r.enqueue_step(n, t0 + n * dt, None if bnd_table is None else bnd_table[n], mx))
+        for r, ev in zip(runners, evs):
+            ev[1].record(r.stream)
+        for r in runners:
+            r.stream.synchronize()
+            r.steps_total += steps
+        barrier()  # no neighbour still stores into these buffers
+        ms = [ev[0].elapsed_time(ev[1]) for ev in evs]
+        allm = reduce_max(torch.stack(maxes).amax(dim=0).cpu() if len(runners) > 1 else maxes[0].cpu())
+        return allm[:steps].numpy(), ms
+
+    allm, ms = loop(nsteps)
+    trips = allm > blowup
+    if not trips.any():
+        return [RunResult(r.result(nsteps), nsteps, 0, t) for r, t in zip(runners, ms)]
+    fail = int(np.argmax(trips)) + 1
+    loop(fail)  # the field right after the failing step, as the per-step guard leaves it
+    return [RunResult(r.result(fail), fail - 1, fail, t) for r, t in zip(runners, ms)]
+
+
+def local_peer_group(engines, slab_list, Neta: int, device):
+    """All ranks of a decomposition in ONE process (one device or several with
+    peer access): each rank's buffers and counters are plain device
+    allocations, the neighbours' pointers are used directly."""
+    import torch
+
+    NF = (slab_list[0].Nxi + 1) * (Neta + 1)
+    bufs = [[torch.empty(NF, dtype=torch.float64, device=device) for _ in range(2)] for _ in slab_list]
+    flags = [torch.zeros(2, dtype=torch.int32, device=device) for _ in slab_list]
+    peers = {r: (bufs[r][0].data_ptr(), bufs[r][1].data_ptr(), flags[r].data_ptr()) for r in range(len(slab_list))}
+    out = []
+    for r, (E, sl) in enumerate(zip(engines, slab_list)):
+        mask = ShardedRun(sl, Neta, None, None).owned_mask(device)
+        out.append(PeerRun(E, sl, Neta, bufs[r], flags[r], peers, torch.cuda.Stream(device), mask))
+    return out
+
+
+def peer_runner(engine, slab: Slab, Neta: int, dist, device, group=None):
+    """This process's rank of a one-process-per-GPU decomposition: buffers and
+    counters from pd_ipc_alloc, the neighbours' opened with CUDA IPC (lazy
+    peer access: NVLink/NVSwitch stores on a B200 node)."""
+    import torch
+
+    from .engine import _check, lib
+
+    L = lib()
+    NF = (slab.Nxi + 1) * (Neta + 1)
+
+    def alloc(nbytes):
+        p, h = C.c_void_p(), C.create_string_buffer(64)
+        _check(L.pd_ipc_alloc(nbytes, C.byref(p), h))
+        return p.value, h.raw
+
+    (x0, h0), (x1, h1), (fl, hf) = alloc(NF * 8), alloc(NF * 8), alloc(64)
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, (slab.rank, h0, h1, hf), group=group)
+    peers, opened = {}, []
+    for rank, a, b, f in handles:
+        if rank == slab.rank:
+            peers[rank] = (x0, x1, fl)
+            continue
+        if rank not in {nb for _, nb, _ in halo_links(slab)}:
+            continue
+        ptrs = []
+        for hnd in (a, b, f):
+            p = C.c_void_p()
+            _check(L.pd_ipc_open(C.create_string_buffer(hnd, 64), C.byref(p)))
+            ptrs.append(p.value)
+            opened.append(p.value)
+        peers[rank] = tuple(ptrs)
+    X = [_as_tensor(x0, NF, "<f8", device), _as_tensor(x1, NF, "<f8", device)]
+    flags = _as_tensor(fl, 2, "<i4", device)
+    mask = ShardedRun(slab, Neta, None, None).owned_mask(device)
+    run = PeerRun(engine, slab, Neta, X, flags, peers, torch.cuda.Stream(device), mask)
+    run._owned = (x0, x1, fl)
+    run._opened = opened
+    return run
+
+
+def close_peer_runner(run):
+    """Unmap the neighbours' buffers and free this rank's (after a barrier)."""
+    from .engine import lib
+
+    L = lib()
+    for p in getattr(run, "_opened", []):
+        L.pd_ipc_close(C.c_void_p(p))
+    for p in getattr(run, "_owned", ()):
+        L.pd_device_free(C.c_void_p(p))
+    run._opened, run._owned = [], ()

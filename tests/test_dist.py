@@ -112,3 +112,32 @@ def test_sharded_run_equals_single_engine(name, over, world, deferred):
             assert failed == stats.failed_step and done == stats.steps_done
             if deferred:
                 assert np.array_equal(U.reshape(P.shape), Uref)
+
+
+@pytest.mark.parametrize("Nxi,periodic,world", [(19, False, 2), (19, False, 3), (128, True, 2), (128, True, 3),
+                                                (8, True, 8), (8, False, 7), (64, True, 1)])
+def test_peer_halo_links_cover_every_halo_once(Nxi, periodic, world):
+    """The fused peer-memory halo (sharded.halo_links): every halo column a rank's
+    3x3 stencils read (gaptooth.cpp:74-104, xi-wrap when periodic) is stored by
+    exactly one link from its owner, into the counter side the rank waits on."""
+    from paper_2405_08764_b200 import sharded
+
+    sls = sharded.slabs(Nxi, periodic, world)
+    owner = {i: s.rank for s in sls for i in range(s.i0, s.i1)}
+    got = {r: [] for r in range(world)}
+    for s in sls:
+        for col, nb, side in sharded.halo_links(s):
+            assert owner[col] == s.rank  # a rank only stores columns it computes
+            got[nb].append((col, side))
+    for s in sls:
+        want = []
+        if s.left() is not None:
+            want.append((((s.i0 - 1) % Nxi) if periodic else s.i0 - 1, sharded.FROM_LEFT))
+        if s.right() is not None:
+            want.append(((s.i1 % Nxi) if periodic else s.i1, sharded.FROM_RIGHT))
+        assert sorted(got[s.rank]) == sorted(want)
+        assert sorted(sharded.incoming_sides(s)) == sorted(side for _, side in want)
+        # halos that no link feeds are the global boundary columns (refresh_boundary)
+        for h in ((s.i0 - 1), s.i1):
+            if not periodic and h in (0, Nxi):
+                assert all(c != h for c, _ in got[s.rank])
