@@ -491,9 +491,17 @@ def run_sharded(args, desc, rank, world, local):
     from paper_2405_08764_b200 import sharded
     from paper_2405_08764_b200.engine import Engine, Problem
 
+    # PD_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0 over gloo, to run
+    # this code path on a one-GPU box — its timings are not scaling numbers
+    one_dev = os.environ.get("PD_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if one_dev:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     prob = Problem(desc)
     r = prob.desc
     ed = prob.engine_desc()
@@ -502,9 +510,12 @@ def run_sharded(args, desc, rank, world, local):
     eng = Engine(sharded.subset_desc(ed, sl))
     # one node, one process per GPU: the neighbour rank's device is its rank
     ndev = torch.cuda.device_count()
-    peer_ok = args.exchange == "peer" and all(nb < ndev and nb != local and torch.cuda.can_device_access_peer(local, nb)
-                                              for _, nb, _ in sharded.halo_links(sl))
-    ok = torch.tensor([1.0 if peer_ok else 0.0], device=dev)
+    peer_ok = args.exchange == "peer" and (one_dev or all(
+        nb < ndev and nb != local and torch.cuda.can_device_access_peer(local, nb) for _, nb, _ in sharded.halo_links(sl)))
+    if args.exchange == "nccl" and one_dev:
+        raise SystemExit("--exchange nccl needs one GPU per rank")
+    cdev = torch.device("cpu") if one_dev else dev  # collectives' tensors (gloo: host)
+    ok = torch.tensor([1.0 if peer_ok else 0.0], device=cdev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     use_peer = bool(ok.item())
     dt = r.T / r.Nt
@@ -513,7 +524,7 @@ def run_sharded(args, desc, rank, world, local):
         run = sharded.peer_runner(eng, sl, ed.Neta, dist, dev)
 
         def red(x):
-            t = x.detach().to(dev).clone()
+            t = x.detach().to(cdev).clone()
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return t.cpu()
 
@@ -544,7 +555,7 @@ def run_sharded(args, desc, rank, world, local):
     dist.barrier()
     clk = clocks.stop()
     launches = eng.launch_count - l0
-    t = torch.tensor([res.device_ms], device=dev, dtype=torch.float64)
+    t = torch.tensor([res.device_ms], device=cdev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = P * N * K * args.steps / (ms * 1e-3)
@@ -559,13 +570,13 @@ def run_sharded(args, desc, rank, world, local):
         Ud = go(Ud, 1, n * dt).U
         Uh.copy_(Ud)
     torch.cuda.synchronize()
-    e2e_s = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+    e2e_s = torch.tensor([time.perf_counter() - t0], device=cdev, dtype=torch.float64)
     dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     NF = Uh.numel()
     e2e = {"value": P * N * K * ke / float(e2e_s.item()), "unit": UNIT, "h2d_bytes_per_step": NF * 8,
            "d2h_bytes_per_step": NF * 8, "steps": ke,
            "path": "host field (pinned) -> per-rank slab step + halo exchange -> host, each step"}
-    mine = torch.tensor([eng.P], device=dev, dtype=torch.float64)
+    mine = torch.tensor([eng.P], device=cdev, dtype=torch.float64)
     most = mine.clone()
     dist.all_reduce(most, op=dist.ReduceOp.MAX)
     if rank == 0:
@@ -576,6 +587,8 @@ def run_sharded(args, desc, rank, world, local):
                 "kernel_family": "fast" if eng.mode == abi.PD_MODE_FAST else "exact",
                 "patches_per_rank_max": int(most.item()), "steps_done": res.steps_done,
                 "failed_step": res.failed_step, "exchange": exchange,
+                **({"one_device_test": "all ranks on cuda:0 (PD_BENCH_ONE_DEVICE): not a scaling number"}
+                   if one_dev else {}),
                 "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
         print(json.dumps(line), flush=True)
     if use_peer:

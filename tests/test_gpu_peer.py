@@ -177,3 +177,32 @@ def test_peer_halo_ipc_processes_equal_single_engine(name, over, world, gpu):
         U, done, failed = res[r]
         assert failed == 0 and done == nsteps
         assert np.array_equal(U.reshape(P.shape), Uref)
+
+
+def test_bench_multi_rank_path_runs_peer_exchange(gpu):
+    """bench.py --gpus 2 under torchrun, both ranks on GPU 0 (PD_BENCH_ONE_DEVICE,
+    gloo for the collectives): the N > 1 code path runs end to end through the
+    fused peer-memory halo and prints one line from rank 0."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, PD_BENCH_ONE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
+           "--gpus", "2", "--steps", "4", "--warmup", "3", "--config", "c3_annulus"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["steps_done"] == 4 and line["failed_step"] == 0
+    assert line["exchange"].startswith("fused peer-memory halo") and line["value"] > 0
+    assert line["gpu_launches"] > 0
