@@ -582,7 +582,6 @@ constexpr int kRunWarps = 4;
 // the warp's 32 slots, recorded in slot[step]; true when the run stops.
 __device__ __forceinline__ bool guard_trips(unsigned long long v, int step, int gw, int lane, double blowup,
                                             unsigned long long* slot, int* fail) {
-#pragma unroll
     v = warp_max_u64(v);
     if (gw == 0 && lane == 0) slot[step] = v;
     const bool nonfinite = v >= 0x7FF0000000000000ull;
@@ -650,7 +649,6 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
         const double* bn = bnd ? bnd + bnd_stride * n : nullptr;
         for (int t = gw * 32 + lane; t < nperim; t += nw * 32)
             m = max(m, (unsigned long long)__double_as_longlong(refresh_one(p, out, F, bn, t, true)));
-#pragma unroll
         m = warp_max_u64(m);
         if (lane == 0) atomicMax(spread + (size_t)n * kGuardSpread + gw % kGuardSpread, m);
         // the guard decision of step n-1 is taken here, one step late: its maximum
@@ -671,7 +669,6 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
                 const double pct = __dmul_rn(__ddiv_rn(fabs(__dsub_rn(__ldcg(out + node), e)), fabs(e)), 100.0);
                 em = max(em, (unsigned long long)__double_as_longlong(pct));
             }
-#pragma unroll
             em = warp_max_u64(em);
             if (lane == 0 && em) atomicMax(err + n, em);
         }
