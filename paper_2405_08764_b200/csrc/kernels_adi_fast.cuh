@@ -222,20 +222,20 @@ k_fast_adi(Params p, const double* __restrict__ F, double* __restrict__ out, int
             k = t < n2 ? t : t - n2;
             const double* d = p.dlag[e];
             const double* w = p.vlag[e];
-            sl = dot3(p.lagq[k][0], dot3(d[0], v[0], d[1], v[3], d[2], v[6]), p.lagq[k][1],
-                      dot3(d[0], v[1], d[1], v[4], d[2], v[7]), p.lagq[k][2], dot3(d[0], v[2], d[1], v[5], d[2], v[8]));
-            val = dot3(p.lagq[k][0], dot3(w[0], v[0], w[1], v[3], w[2], v[6]), p.lagq[k][1],
-                       dot3(w[0], v[1], w[1], v[4], w[2], v[7]), p.lagq[k][2], dot3(w[0], v[2], w[1], v[5], w[2], v[8]));
+            sl = dot3(lagq_at(p, k, 0), dot3(d[0], v[0], d[1], v[3], d[2], v[6]), lagq_at(p, k, 1),
+                      dot3(d[0], v[1], d[1], v[4], d[2], v[7]), lagq_at(p, k, 2), dot3(d[0], v[2], d[1], v[5], d[2], v[8]));
+            val = dot3(lagq_at(p, k, 0), dot3(w[0], v[0], w[1], v[3], w[2], v[6]), lagq_at(p, k, 1),
+                       dot3(w[0], v[1], w[1], v[4], w[2], v[7]), lagq_at(p, k, 2), dot3(w[0], v[2], w[1], v[5], w[2], v[8]));
         } else {
             const int u = t - 2 * n2;
             e = u < n1 ? PD_EDGE_N : PD_EDGE_S;
             k = u < n1 ? u : u - n1;
             const double* d = p.dlag[e];
             const double* w = p.vlag[e];
-            sl = dot3(p.lagp[k][0], dot3(d[0], v[0], d[1], v[1], d[2], v[2]), p.lagp[k][1],
-                      dot3(d[0], v[3], d[1], v[4], d[2], v[5]), p.lagp[k][2], dot3(d[0], v[6], d[1], v[7], d[2], v[8]));
-            val = dot3(p.lagp[k][0], dot3(w[0], v[0], w[1], v[1], w[2], v[2]), p.lagp[k][1],
-                       dot3(w[0], v[3], w[1], v[4], w[2], v[5]), p.lagp[k][2], dot3(w[0], v[6], w[1], v[7], w[2], v[8]));
+            sl = dot3(lagp_at(p, k, 0), dot3(d[0], v[0], d[1], v[1], d[2], v[2]), lagp_at(p, k, 1),
+                      dot3(d[0], v[3], d[1], v[4], d[2], v[5]), lagp_at(p, k, 2), dot3(d[0], v[6], d[1], v[7], d[2], v[8]));
+            val = dot3(lagp_at(p, k, 0), dot3(w[0], v[0], w[1], v[1], w[2], v[2]), lagp_at(p, k, 1),
+                       dot3(w[0], v[3], w[1], v[4], w[2], v[5]), lagp_at(p, k, 2), dot3(w[0], v[6], w[1], v[7], w[2], v[8]));
         }
         gb[e * L + k] = p.bc_type == PD_BC_NEUMANN ? __dmul_rn(p.gsc[e], sl) : edge_constant(p, e, val, sl);
     }

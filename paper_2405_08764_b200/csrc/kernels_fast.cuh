@@ -238,7 +238,7 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
             const double G0 = dot3(d[0], v[0], d[1], v[3], d[2], v[6]);
             const double G1 = dot3(d[0], v[1], d[1], v[4], d[2], v[7]);
             const double G2 = dot3(d[0], v[2], d[1], v[5], d[2], v[8]);
-            const double sl = dot3(p.lagq[j][0], G0, p.lagq[j][1], G1, p.lagq[j][2], G2);
+            const double sl = dot3(lagq_at(p, j, 0), G0, lagq_at(p, j, 1), G1, lagq_at(p, j, 2), G2);
             if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 sg[gs][e][j] = __dmul_rn(p.gsc[e], sl);
             } else { // Robin / Dirichlet need the edge value too (dirichlet_edge_values, gaptooth.cpp:110-130)
@@ -246,7 +246,7 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
                 const double V0 = dot3(w[0], v[0], w[1], v[3], w[2], v[6]);
                 const double V1 = dot3(w[0], v[1], w[1], v[4], w[2], v[7]);
                 const double V2 = dot3(w[0], v[2], w[1], v[5], w[2], v[8]);
-                sg[gs][e][j] = edge_constant(p, e, dot3(p.lagq[j][0], V0, p.lagq[j][1], V1, p.lagq[j][2], V2), sl);
+                sg[gs][e][j] = edge_constant(p, e, dot3(lagq_at(p, j, 0), V0, lagq_at(p, j, 1), V1, lagq_at(p, j, 2), V2), sl);
             }
         } else {
             const int u = t - 2 * n2;
@@ -255,7 +255,7 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
             const double H0 = dot3(d[0], v[0], d[1], v[1], d[2], v[2]);
             const double H1 = dot3(d[0], v[3], d[1], v[4], d[2], v[5]);
             const double H2 = dot3(d[0], v[6], d[1], v[7], d[2], v[8]);
-            const double sl = dot3(p.lagp[i][0], H0, p.lagp[i][1], H1, p.lagp[i][2], H2);
+            const double sl = dot3(lagp_at(p, i, 0), H0, lagp_at(p, i, 1), H1, lagp_at(p, i, 2), H2);
             if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 sg[gs][e][i] = __dmul_rn(p.gsc[e], sl);
             } else {
@@ -263,7 +263,7 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
                 const double V0 = dot3(w[0], v[0], w[1], v[1], w[2], v[2]);
                 const double V1 = dot3(w[0], v[3], w[1], v[4], w[2], v[5]);
                 const double V2 = dot3(w[0], v[6], w[1], v[7], w[2], v[8]);
-                sg[gs][e][i] = edge_constant(p, e, dot3(p.lagp[i][0], V0, p.lagp[i][1], V1, p.lagp[i][2], V2), sl);
+                sg[gs][e][i] = edge_constant(p, e, dot3(lagp_at(p, i, 0), V0, lagp_at(p, i, 1), V1, lagp_at(p, i, 2), V2), sl);
             }
         }
     }

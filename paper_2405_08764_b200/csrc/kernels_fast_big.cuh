@@ -155,7 +155,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const double G0 = d[0] * v[0] + d[1] * v[3] + d[2] * v[6];
             const double G1 = d[0] * v[1] + d[1] * v[4] + d[2] * v[7];
             const double G2 = d[0] * v[2] + d[1] * v[5] + d[2] * v[8];
-            const double sl = p.lagq[j][0] * G0 + p.lagq[j][1] * G1 + p.lagq[j][2] * G2;
+            const double sl = lagq_at(p, j, 0) * G0 + lagq_at(p, j, 1) * G1 + lagq_at(p, j, 2) * G2;
             if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 s_g[e][j] = p.gsc[e] * sl;
             } else {
@@ -163,7 +163,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
                 const double V0 = w[0] * v[0] + w[1] * v[3] + w[2] * v[6];
                 const double V1 = w[0] * v[1] + w[1] * v[4] + w[2] * v[7];
                 const double V2 = w[0] * v[2] + w[1] * v[5] + w[2] * v[8];
-                s_g[e][j] = edge_constant(p, e, p.lagq[j][0] * V0 + p.lagq[j][1] * V1 + p.lagq[j][2] * V2, sl);
+                s_g[e][j] = edge_constant(p, e, lagq_at(p, j, 0) * V0 + lagq_at(p, j, 1) * V1 + lagq_at(p, j, 2) * V2, sl);
             }
         } else {
             const int u = t - 2 * n2;
@@ -172,7 +172,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
             const double H0 = d[0] * v[0] + d[1] * v[1] + d[2] * v[2];
             const double H1 = d[0] * v[3] + d[1] * v[4] + d[2] * v[5];
             const double H2 = d[0] * v[6] + d[1] * v[7] + d[2] * v[8];
-            const double sl = p.lagp[i][0] * H0 + p.lagp[i][1] * H1 + p.lagp[i][2] * H2;
+            const double sl = lagp_at(p, i, 0) * H0 + lagp_at(p, i, 1) * H1 + lagp_at(p, i, 2) * H2;
             if (!Cfg::GEN || p.bc_type == PD_BC_NEUMANN) {
                 s_g[e][i] = p.gsc[e] * sl;
             } else {
@@ -180,7 +180,7 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
                 const double V0 = w[0] * v[0] + w[1] * v[1] + w[2] * v[2];
                 const double V1 = w[0] * v[3] + w[1] * v[4] + w[2] * v[5];
                 const double V2 = w[0] * v[6] + w[1] * v[7] + w[2] * v[8];
-                s_g[e][i] = edge_constant(p, e, p.lagp[i][0] * V0 + p.lagp[i][1] * V1 + p.lagp[i][2] * V2, sl);
+                s_g[e][i] = edge_constant(p, e, lagp_at(p, i, 0) * V0 + lagp_at(p, i, 1) * V1 + lagp_at(p, i, 2) * V2, sl);
             }
         }
     }

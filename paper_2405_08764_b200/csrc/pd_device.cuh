@@ -45,6 +45,10 @@ struct Params {
     double vlag[4][3];   // Lagrange value weights at +-h/2 across each edge (E, W, N, S): edge values
     double cedge[4];     // Robin ghost coefficient cEdge = -sign 2 delta w1/w2 per edge (microsim.cpp:180)
     int pinned;          // the patch edges pin their nodes (Dirichlet, or Robin with w2 ~ 0)
+    // device copy of lagq then lagp ([2][33][3]): the FAST prologues index them by
+    // lane (edge node), which through the constant bank serialises per distinct
+    // address; through L1 it is one request
+    const double* lagtab;
     // fused peer-memory halo of a decomposed run (pd_projective_step_halo): the
     // results of the patches in column halo_col[l] also go to halo_dst[l] (the
     // neighbour's buffer), each followed by a system-scope fence and +1 on
@@ -54,6 +58,10 @@ struct Params {
     double* halo_dst[2];
     unsigned int* halo_flag[2];
 };
+
+// Lagrange value weights at edge node j (E/W edges, lagq) or i (N/S, lagp)
+__device__ __forceinline__ double lagq_at(const Params& p, int j, int q) { return __ldg(p.lagtab + 3 * j + q); }
+__device__ __forceinline__ double lagp_at(const Params& p, int i, int q) { return __ldg(p.lagtab + 99 + 3 * i + q); }
 
 // Store v (the result at macro node `node`) into the neighbours' buffers when
 // the node lies in a halo link's column, then publish it: fence.sc.sys orders

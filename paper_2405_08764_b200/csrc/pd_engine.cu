@@ -97,6 +97,7 @@ struct pd_engine {
     DevBuf<int32_t> d_pij, d_nbr, d_cset, d_kinds, d_fail, d_cset_items;
     DevBuf<double> d_coeffs, d_src, d_weights, d_U, d_chain, d_bnd, d_srct, d_tmp, d_tmp2, d_rw;
     DevBuf<double> d_roww;              // linear-response row weights [Neta+1][9]
+    DevBuf<double> d_lag;               // Params::lagtab: lagq then lagp, [2][33][3]
     DevBuf<double> d_adi_fac;           // ADI static line factors [sets][2][L][L][kAdiFac] (k_adi_factor)
     DevBuf<double> d_adi_fast;          // FAST ADI folded tables (adi_fast_layout, k_adi_fast_fold)
     DevBuf<double> d_exact;             // pd_run_exact: exact-solution table [nsteps][NF] + errors [nsteps]
@@ -475,6 +476,10 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
                 upload(e->d_src.p, d.source_spatial, (size_t)d.ncoeff_sets * p.N * 8, e->stream);
             }
         }
+        e->d_lag.alloc(2 * 33 * 3);
+        upload(e->d_lag.p, &p.lagq[0][0], 33 * 3 * 8, e->stream);
+        upload(e->d_lag.p + 99, &p.lagp[0][0], 33 * 3 * 8, e->stream);
+        p.lagtab = e->d_lag.p;
         e->d_U.alloc(2 * e->NF);
         e->d_fail.alloc(4);
         e->device_bytes = Ncoef * 8 + e->pij.size() * 4 + e->nbr.size() * 4 + 2 * e->NF * 8;
