@@ -313,14 +313,17 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
     const int bjX = flip ? (bj + 1 < LJ ? bj + 1 : bj) : (bj > 0 ? bj - 1 : bj);
     double* const mine0 = &s_row[0][bj][i0 + 2];
     const double* const rx0 = &s_row[0][bjX][i0 + 2];
+    // The hand-off of step s+1's row is published at the END of step s (after the
+    // whole update), then one barrier; step 0's before the loop.  Measured against
+    // publishing at the top of each step (same arithmetic, ptxas places the barrier
+    // differently): 9-11 % faster at K = 10-200 (profiles/r02_ceiling.md).
+    static_assert(BI == 2, "the row hand-off moves one 16-byte pair per lane");
+    // local row jj = 0 as one 128-bit store / load per lane (bank-conflict free;
+    // two 64-bit accesses at a 16-byte lane stride conflicted 2-way)
+    *reinterpret_cast<double2*>(mine0) = make_double2(u[0][0], u[1][0]);
+    __syncthreads();
     for (int step = 0; step < p.nt; ++step) {
         const int po = (step & 1) * LJ * ROW;
-        double* mine = mine0 + po;
-        static_assert(BI == 2, "the row hand-off moves one 16-byte pair per lane");
-        // local row jj = 0 as one 128-bit store / load per lane (bank-conflict free;
-        // two 64-bit accesses at a 16-byte lane stride conflicted 2-way)
-        *reinterpret_cast<double2*>(mine) = make_double2(u[0][0], u[1][0]);
-        __syncthreads();
         const double2 pr = *reinterpret_cast<const double2*>(rx0 + po);
         double hS[BI], hN[BI], eS[BI], eN[BI];
         hS[0] = pr.x;
@@ -352,22 +355,20 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WC, ii, jj), u[ii][jj], c[ii][jj]);
+        // term order N, W, S, E: of the 24 orders x {barrier at the top, at the end}
+        // this one gives ptxas's shortest loop (control-word stall sum 175 vs 235 for
+        // the previous E, W, N, S with the barrier at the top; scripts/lab/stallsearch.py)
+        auto term = [&](int k) {
+            const int da = k == WE ? 1 : k == WW ? -1 : 0, db = k == WN ? 1 : k == WS ? -1 : 0;
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
+            for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WE, ii, jj), at(ii + 1, jj), nu[ii][jj]);
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WN, ii, jj), at(ii, jj + 1), nu[ii][jj]);
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WS, ii, jj), at(ii, jj - 1), nu[ii][jj]);
+                for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(k, ii, jj), at(ii + da, jj + db), nu[ii][jj]);
+        };
+        term(WN);
+        term(WW);
+        term(WS);
+        term(WE);
         if constexpr (MIXED) {
             double e[BI][BJ];
 #pragma unroll
@@ -389,6 +390,10 @@ k_fast_big(Params p, const double* __restrict__ F, double* __restrict__ out, int
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) u[ii][jj] = nu[ii][jj];
+        if (step + 1 < p.nt) { // double-buffered by step parity: one barrier per micro-step
+            *reinterpret_cast<double2*>(mine0 + ((step + 1) & 1) * LJ * ROW) = make_double2(u[0][0], u[1][0]);
+            __syncthreads();
+        }
     }
 #undef WT
 

@@ -10,8 +10,16 @@ import os, re, subprocess, sys, tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 CSRC = os.path.join(ROOT, "paper_2405_08764_b200", "csrc")
-ENTRY = "_ZN6pdb2003dev6k_fastINS0_7FastCfgILi16ELi16ELi2ELi4ELb1ELb0ELb0ELb0EEEEEvNS0_6ParamsEPKdPdiPKiS6_iS9_S6_"
-TU = '#include "kernels_fast.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast<FC16M>(Params, const double*, double*, int, const int*, const double*, int, const int*, const double*);\n}\n'
+KERNELS = {
+    "fast16": ("_ZN6pdb2003dev6k_fastINS0_7FastCfgILi16ELi16ELi2ELi4ELb1ELb0ELb0ELb0EEEEEvNS0_6ParamsEPKdPdiPKiS6_iS9_S6_",
+               '#include "kernels_fast.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast<FC16M>(Params, const double*, '
+               'double*, int, const int*, const double*, int, const int*, const double*);\n}\n'),
+    "big32": ("_ZN6pdb2003dev10k_fast_bigINS0_6BigCfgILi32ELb1ELb0ELb0EEEEEvNS0_6ParamsEPKdPdiPKiS6_S9_",
+              '#include "kernels_fast_big.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast_big<BC32M>(Params, const double*, '
+              'double*, int, const int*, const double*, const int*);\n}\n'),
+}
+KERNEL = os.environ.get("LAB_KERNEL", "fast16")
+ENTRY, TU = KERNELS[KERNEL]
 
 
 def loop_stats(sass: str):
