@@ -400,22 +400,41 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WC, ii, jj), u[ii][jj], c[ii][jj]);
+        if constexpr (MIXED) {
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
+            for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WN, ii, jj), at(ii, jj + 1), nu[ii][jj]);
+                for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WN, ii, jj), at(ii, jj + 1), nu[ii][jj]);
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
+            for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WS, ii, jj), at(ii, jj - 1), nu[ii][jj]);
+                for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WS, ii, jj), at(ii, jj - 1), nu[ii][jj]);
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
+            for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WE, ii, jj), at(ii + 1, jj), nu[ii][jj]);
+                for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WE, ii, jj), at(ii + 1, jj), nu[ii][jj]);
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
+            for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
+                for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
+        } else {
+            // 5-point tiles: the neighbour-term order ptxas schedules shortest for the
+            // single-launch run's loop (control-word stall sums, scripts/lab/stallsearch.py):
+            // 9x9 W, S, E, N (253 vs 317 for N, S, E, W), 7x7 N, E, S, W (219 vs 233)
+            auto ord = [](int q) constexpr {
+                constexpr int o9[4] = {WW, WS, WE, WN}, o7[4] = {WN, WE, WS, WW}, o0[4] = {WN, WS, WE, WW};
+                return N1 == 9 ? o9[q] : N1 == 7 ? o7[q] : o0[q];
+            };
+            auto term = [&](int k) {
+                const int da = k == WE ? 1 : k == WW ? -1 : 0, db = k == WN ? 1 : k == WS ? -1 : 0;
+#pragma unroll
+                for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+                    for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(k, ii, jj), at(ii + da, jj + db), nu[ii][jj]);
+            };
+#pragma unroll
+            for (int q = 0; q < 4; ++q) term(ord(q));
+        }
         if constexpr (MIXED) {
             // difference form: e(i,j) = u(i+1,j) - u(i-1,j) once per node, then
             // D(i,j) = e(i,j+1) - e(i,j-1); e crosses lanes only at the block's

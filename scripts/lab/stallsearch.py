@@ -17,6 +17,14 @@ KERNELS = {
     "big32": ("_ZN6pdb2003dev10k_fast_bigINS0_6BigCfgILi32ELb1ELb0ELb0EEEEEvNS0_6ParamsEPKdPdiPKiS6_S9_",
               '#include "kernels_fast_big.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast_big<BC32M>(Params, const double*, '
               'double*, int, const int*, const double*, const int*);\n}\n'),
+    "run9": ("_ZN6pdb2003dev10k_fast_runINS0_7FastCfgILi9ELi9ELi3ELi3ELb0ELb0ELb0ELb0EEEEEvNS0_6ParamsEPdS5_PKiPKdiS9_mS9_midPySA_PiS9_SA_",
+             '#include "kernels_fast.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast_run<FC9>(Params, double*, double*, '
+             'const int*, const double*, int, const double*, size_t, const double*, size_t, int, double, unsigned long long*, '
+             'unsigned long long*, int*, const double*, unsigned long long*);\n}\n'),
+    "run7": ("_ZN6pdb2003dev10k_fast_runINS0_7FastCfgILi7ELi7ELi1ELi7ELb0ELb0ELb0ELb0EEEEEvNS0_6ParamsEPdS5_PKiPKdiS9_mS9_midPySA_PiS9_SA_",
+             '#include "kernels_fast.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast_run<FC7>(Params, double*, double*, '
+             'const int*, const double*, int, const double*, size_t, const double*, size_t, int, double, unsigned long long*, '
+             'unsigned long long*, int*, const double*, unsigned long long*);\n}\n'),
 }
 KERNEL = os.environ.get("LAB_KERNEL", "fast16")
 ENTRY, TU = KERNELS[KERNEL]
@@ -30,13 +38,18 @@ def loop_stats(sass: str):
         if m:
             hi = int(re.search(r'/\* (0x[0-9a-f]+) \*/', lines[i + 1]).group(1), 16)
             ins.append((int(m.group(1), 16), m.group(2).strip(), hi))
-    best = None
+    loops = []
     for a, t, _ in ins:
         m = re.search(r'BRA(?:\.U)?\s+(?:!?U?P\d+,\s*)?0x([0-9a-f]+)', t)
         if m:
             tg = int(m.group(1), 16)
-            if tg < a and (best is None or a - tg > best[1] - best[0]):
-                best = (tg, a)
+            if tg < a:
+                loops.append((tg, a))
+    # the micro-step loop: the shortest backward branch whose body holds >= 20 DFMA
+    def ndfma(lo, hi):
+        return sum(1 for a, t, _ in ins if lo <= a <= hi and 'DFMA' in t)
+    cand = [l for l in loops if ndfma(*l) >= 20]
+    best = min(cand, key=lambda l: l[1] - l[0])
     body = [x for x in ins if best[0] <= x[0] <= best[1]]
     stall = sum((h >> 41) & 0xF for _, _, h in body)
     reads = hits = 0
