@@ -370,7 +370,7 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
     // (measured: scripts/ubench/ubench2.cu).  A lane on a
     // patch edge receives some other finite value for the missing side; the
     // boundary fold-in above has zeroed every weight that would read it.
-    for (int step = 0; step < p.nt; ++step) {
+    auto micro_step = [&](int step) {
         double hN[BI], hS[BI];
 #pragma unroll
         for (int ii = 0; ii < BI; ++ii) {
@@ -418,12 +418,17 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
 #pragma unroll
                 for (int jj = 0; jj < BJ; ++jj) nu[ii][jj] = fma(WT(WW, ii, jj), at(ii - 1, jj), nu[ii][jj]);
         } else {
-            // 5-point tiles: the neighbour-term order ptxas schedules shortest for the
-            // single-launch run's loop (control-word stall sums, scripts/lab/stallsearch.py):
-            // 9x9 W, S, E, N (253 vs 317 for N, S, E, W), 7x7 N, E, S, W (219 vs 233)
+            // 5-point tiles: the neighbour-term order of the fastest single-launch run
+            // measured (candidates from the control-word stall sums of
+            // scripts/lab/stallsearch.py, then timed): 9x9 W, S, E, N; 7x7 N, E, S, W
             auto ord = [](int q) constexpr {
+#ifdef PD_LAB_O0 // scripts/lab/stallsearch.py override
+                constexpr int ol[4] = {PD_LAB_O0, PD_LAB_O1, PD_LAB_O2, PD_LAB_O3};
+                return ol[q];
+#else
                 constexpr int o9[4] = {WW, WS, WE, WN}, o7[4] = {WN, WE, WS, WW}, o0[4] = {WN, WS, WE, WW};
                 return N1 == 9 ? o9[q] : N1 == 7 ? o7[q] : o0[q];
+#endif
             };
             auto term = [&](int k) {
                 const int da = k == WE ? 1 : k == WW ? -1 : 0, db = k == WN ? 1 : k == WS ? -1 : 0;
@@ -470,6 +475,16 @@ __device__ __forceinline__ double patch_body(const Params& p, double (&w)[2 * Cf
         for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) u[ii][jj] = nu[ii][jj];
+    };
+    if constexpr (!MIXED) {
+        // 5-point tiles (configs 1-3, latency-bound single-launch runs): two micro-steps
+        // per loop trip let ptxas overlap one step's tail with the next one's shuffles
+        // (configs 1-3 5-7 % faster); the 9-point 16x16 loop is throughput-bound and
+        // slower unrolled (+1 %), so it keeps one step per trip
+#pragma unroll 2
+        for (int step = 0; step < p.nt; ++step) micro_step(step);
+    } else {
+        for (int step = 0; step < p.nt; ++step) micro_step(step);
     }
 
     // ---- trapezoid / Simpson restriction (gaptooth.cpp:170-194) -------------
