@@ -385,9 +385,11 @@ class PeerRun:
         _check(lib().pd_engine_set_stream(engine.h, stream.cuda_stream), engine.h)
 
     def begin(self, U0):
-        """Load the run's initial field into both buffers (stream-ordered)."""
+        """Load the run's initial field into both buffers (stream-ordered after
+        whatever produced U0 on the caller's current stream, e.g. an async H2D)."""
         import torch
 
+        self.stream.wait_stream(torch.cuda.current_stream(self.X[0].device))
         with torch.cuda.stream(self.stream):
             self.X[0].copy_(U0)
             self.X[1].copy_(U0)

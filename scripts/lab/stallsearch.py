@@ -17,6 +17,9 @@ KERNELS = {
     "big32": ("_ZN6pdb2003dev10k_fast_bigINS0_6BigCfgILi32ELb1ELb0ELb0EEEEEvNS0_6ParamsEPKdPdiPKiS6_S9_",
               '#include "kernels_fast_big.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast_big<BC32M>(Params, const double*, '
               'double*, int, const int*, const double*, const int*);\n}\n'),
+    "fast8": ("_ZN6pdb2003dev6k_fastINS0_7FastCfgILi8ELi8ELi2ELi4ELb1ELb0ELb0ELb0EEEEEvNS0_6ParamsEPKdPdiPKiS6_iS9_S6_",
+              '#include "kernels_fast.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast<FC8M>(Params, const double*, '
+              'double*, int, const int*, const double*, int, const int*, const double*);\n}\n'),
     "run9": ("_ZN6pdb2003dev10k_fast_runINS0_7FastCfgILi9ELi9ELi3ELi3ELb0ELb0ELb0ELb0EEEEEvNS0_6ParamsEPdS5_PKiPKdiS9_mS9_midPySA_PiS9_SA_",
              '#include "kernels_fast.cuh"\nnamespace pdb200::dev {\ntemplate __global__ void k_fast_run<FC9>(Params, double*, double*, '
              'const int*, const double*, int, const double*, size_t, const double*, size_t, int, double, unsigned long long*, '
