@@ -25,6 +25,7 @@ the restated oracle.
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -470,7 +471,14 @@ def run_peer(runners, U0s, nsteps: int, dt: float, t0: float = 0.0, bnd_table=No
                 keep.append(r.enqueue_step(n, t0 + n * dt, None if bnd_table is None else bnd_table[n], mx))
         for r, ev in zip(runners, evs):
             ev[1].record(r.stream)
-        for r in runners:
+        # bounded wait: a counter that never arrives (a peer that died, a broken
+        # mapping) would leave a stream waiting forever; fail loudly instead
+        deadline = time.monotonic() + max(120.0, 0.5 * steps)
+        for r, ev in zip(runners, evs):
+            while not ev[1].query():
+                if time.monotonic() > deadline:
+                    raise RuntimeError(f"rank {r.s.rank}: peer halo exchange stalled (link counters not reached)")
+                time.sleep(1e-4)
             r.stream.synchronize()
             r.steps_total += steps
         barrier()  # no neighbour still stores into these buffers
