@@ -478,7 +478,7 @@ def run_peer(runners, U0s, nsteps: int, dt: float, t0: float = 0.0, bnd_table=No
             while not ev[1].query():
                 if time.monotonic() > deadline:
                     raise RuntimeError(f"rank {r.s.rank}: peer halo exchange stalled (link counters not reached)")
-                time.sleep(1e-4)
+                time.sleep(2e-5)
             r.stream.synchronize()
             r.steps_total += steps
         barrier()  # no neighbour still stores into these buffers
