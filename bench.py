@@ -520,8 +520,23 @@ def run_sharded(args, desc, rank, world, local):
     use_peer = bool(ok.item())
     dt = r.T / r.Nt
     U0 = torch.from_numpy(prob.initial_field().reshape(-1).copy()).to(dev)
+    run = None
     if use_peer:
-        run = sharded.peer_runner(eng, sl, ed.Neta, dist, dev)
+        # the IPC mappings are the one step that can fail on a node (no P2P path):
+        # agree across ranks and fall back to the NCCL exchange rather than abort
+        try:
+            run = sharded.peer_runner(eng, sl, ed.Neta, dist, dev)
+            ok_ipc = 1.0
+        except Exception as x:  # noqa: BLE001 - reported, then the NCCL transport runs
+            print(f"rank {rank}: peer-memory halo unavailable ({x}); using NCCL", file=sys.stderr, flush=True)
+            ok_ipc = 0.0
+        flag = torch.tensor([ok_ipc], device=cdev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if flag.item() < 1.0:
+            if run is not None:
+                sharded.close_peer_runner(run)
+            run, use_peer = None, False
+    if use_peer:
 
         def red(x):
             t = x.detach().to(cdev).clone()
