@@ -395,7 +395,7 @@ class PeerRun:
             self.X[0].copy_(U0)
             self.X[1].copy_(U0)
 
-    def enqueue_step(self, n: int, t: float, bnd, maxes):
+    def enqueue_step(self, n: int, t: float, bnd, maxes, src=None):
         """Step n of the current run: wait for both neighbours' step n-1, the fused
         step (own patches + edge columns into the neighbours' buffers + counter
         bumps), the boundary refresh, and this rank's max |U| into maxes[n]."""
@@ -416,17 +416,20 @@ class PeerRun:
             halo.column[l] = col
             halo.dst[l] = xs[out]
             halo.flag[l] = fl
-        b = None
-        if bnd is not None:
-            with torch.cuda.stream(self.stream):
+        b = g = None
+        with torch.cuda.stream(self.stream):
+            if bnd is not None:  # [k+2][perimeter] refresh values of this step
                 b = torch.as_tensor(np.ascontiguousarray(bnd).reshape(-1)).to(self.X[0].device, non_blocking=True)
+            if src is not None:  # [k+1][nt] separable-source time factors of this step
+                g = torch.as_tensor(np.ascontiguousarray(src).reshape(-1)).to(self.X[0].device, non_blocking=True)
         _check(L.pd_projective_step_halo(h, self.X[n % 2].data_ptr(), self.X[out].data_ptr(), t,
-                                         None if b is None else b.data_ptr(), None, C.byref(halo)), h)
+                                         None if b is None else b.data_ptr(), None if g is None else g.data_ptr(),
+                                         C.byref(halo)), h)
         with torch.cuda.stream(self.stream):
             m = torch.where(self.mask, self.X[out].abs(), torch.zeros((), dtype=torch.float64,
                                                                         device=self.X[0].device)).amax()
             maxes[n] = torch.where(torch.isfinite(m), m, torch.full_like(m, float("inf")))
-        return b
+        return b, g
 
     def result(self, nsteps: int):
         return self.X[nsteps % 2]
@@ -440,7 +443,7 @@ def _peer_guard(U0, mask, reduce_max):
 
 
 def run_peer(runners, U0s, nsteps: int, dt: float, t0: float = 0.0, bnd_table=None, reduce_max=None,
-             barrier=None) -> list[RunResult]:
+             barrier=None, src_table=None) -> list[RunResult]:
     """Drive the ranks in `runners` (all ranks of an in-process group, or this
     process's one rank with torch.distributed hooks) through nsteps projective
     steps.  The guard (cpi.cpp:187-202) is taken after the loop from the
@@ -468,7 +471,8 @@ def run_peer(runners, U0s, nsteps: int, dt: float, t0: float = 0.0, bnd_table=No
         keep = []
         for n in range(steps):
             for r, mx in zip(runners, maxes):
-                keep.append(r.enqueue_step(n, t0 + n * dt, None if bnd_table is None else bnd_table[n], mx))
+                keep.append(r.enqueue_step(n, t0 + n * dt, None if bnd_table is None else bnd_table[n], mx,
+                                           None if src_table is None else src_table[n]))
         for r, ev in zip(runners, evs):
             ev[1].record(r.stream)
         # bounded wait: a counter that never arrives (a peer that died, a broken

@@ -206,3 +206,45 @@ def test_bench_multi_rank_path_runs_peer_exchange(gpu):
     assert line["n_gpus"] == 2 and line["steps_done"] == 4 and line["failed_step"] == 0
     assert line["exchange"].startswith("fused peer-memory halo") and line["value"] > 0
     assert line["gpu_launches"] > 0
+
+
+def _peer_vs_single(P, mode, world, nsteps, bnd=None, src=None, linear=False):
+    import torch
+
+    ed = P.engine_desc()
+    periodic = bool(ed.periodic_xi)
+    sls = sharded.slabs(ed.Nxi, periodic, world)
+    dev = torch.device("cuda", 0)
+    E = Engine.from_problem(P, mode=mode)
+    engines = [Engine(sharded.subset_desc(ed, sl), mode) for sl in sls]
+    if linear:  # the full engine's row weights (gaptooth.cpp:377-394) on every slab
+        w = E.set_linear()
+        for Es in engines:
+            Es.set_linear(w)
+    runners = sharded.local_peer_group(engines, sls, ed.Neta, dev)
+    U0 = P.initial_field()
+    Ut = torch.from_numpy(U0.reshape(-1).copy()).to(dev)
+    res = sharded.run_peer(runners, [Ut] * world, nsteps, P.desc.T / P.desc.Nt, 0.0, bnd, src_table=src)
+    full = assemble([r.U.cpu().numpy() for r in res], sls, P.shape, periodic)
+    Uref, st = E.run(U0, nsteps, bnd=bnd, src_time=src)
+    assert all(r.failed_step == 0 and r.steps_done == nsteps for r in res)
+    return full, Uref
+
+
+@pytest.mark.parametrize("mode", [EXACT, FAST], ids=["exact", "fast"])
+def test_peer_halo_adi_with_source(mode, gpu):
+    """The fused halo store in the ADI kernels (EXACT and FAST families) and the
+    per-step separable-source factors (problem1, the reference's Table-1 setup)."""
+    P = Problem(configs.copy_desc(configs.load("ref_table1_cdr_const")[0]))
+    n = 6
+    full, Uref = _peer_vs_single(P, mode, 3, n, P.boundary_table(0.0, n), P.source_time(0.0, n))
+    assert np.array_equal(full, Uref)
+
+
+@pytest.mark.parametrize("name", ["c1_diffusion", "c3_annulus"])
+def test_peer_halo_linear_response_step(name, gpu):
+    """The fused halo store in the linear-response step (k_linear_step,
+    gaptooth.cpp:396-418) with the full engine's row weights on every slab."""
+    P = Problem(configs.load(name)[0])
+    full, Uref = _peer_vs_single(P, EXACT, 2, 15, linear=True)
+    assert np.array_equal(full, Uref)
