@@ -525,7 +525,7 @@ def run_sharded(args, desc, rank, world, local):
         # the IPC mappings are the one step that can fail on a node (no P2P path):
         # agree across ranks and fall back to the NCCL exchange rather than abort
         try:
-            run = sharded.peer_runner(eng, sl, ed.Neta, dist, dev)
+            run = sharded.peer_runner(eng, sl, ed.Neta, dist, dev, k=ed.k)
             ok_ipc = 1.0
         except Exception as x:  # noqa: BLE001 - reported, then the NCCL transport runs
             print(f"rank {rank}: peer-memory halo unavailable ({x}); using NCCL", file=sys.stderr, flush=True)

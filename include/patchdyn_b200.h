@@ -347,6 +347,16 @@ typedef struct pd_halo_out {
 } pd_halo_out;
 pd_status pd_projective_step_halo(pd_engine* e, const double* U_in_dev, double* U_out_dev, double t,
                                   const double* bnd_dev, const double* src_time_dev, const pd_halo_out* halo);
+/* k > 0: the projective step as its pieces, each with the same fused halo store
+ * (the neighbours' counters then advance k+2 times per projective step):
+ * substep m (0..k) of step_direct into U_out (refreshed from bnd = that substep's
+ * [perimeter] row, or kept from U_in), and the extrapolation U_out = U_k +
+ * (dt - k tau)(U_{k+1} - U_k)/tau on the engine's patch nodes (cpi.cpp:58-77),
+ * refreshed from bnd (row k+1) or kept from U_in (the step's input). */
+pd_status pd_gaptooth_substep_halo(pd_engine* e, const double* U_in_dev, double* U_out_dev, int32_t m,
+                                   const double* bnd_dev, const double* src_time_dev, const pd_halo_out* halo);
+pd_status pd_extrapolate_halo(pd_engine* e, const double* U_in_dev, const double* U_k_dev, const double* U_k1_dev,
+                              double* U_out_dev, const double* bnd_dev, const pd_halo_out* halo);
 pd_status pd_stream_wait_flag(pd_engine* e, const uint32_t* flag_dev, uint32_t value);
 pd_status pd_ipc_alloc(size_t bytes, void** dev_ptr, unsigned char handle_out[64]);
 pd_status pd_ipc_open(const unsigned char handle[64], void** dev_ptr);

@@ -77,7 +77,9 @@ __global__ void k_extrapolate(Params p, double* __restrict__ out, const double* 
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < p.P; q += gridDim.x * blockDim.x) {
         const size_t node = (size_t)pij[2 * q] * p.NF2 + pij[2 * q + 1];
         const double F = XDIV(XSUB(Uk1[node], Uk[node]), p.tau);
-        out[node] = XADD(Uk[node], XMUL(horizon, F));
+        const double v = XADD(Uk[node], XMUL(horizon, F));
+        out[node] = v;
+        halo_store(p, node, v); // decomposed run with k > 0 (pd_extrapolate_halo)
     }
 }
 

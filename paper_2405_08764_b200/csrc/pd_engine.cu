@@ -1141,6 +1141,43 @@ pd_status pd_projective_step_halo(pd_engine* e, const double* in, double* out, d
     });
 }
 
+namespace {
+pd_status check_halo(const pd_engine* e, const pd_halo_out* h) {
+    if (!h || h->nlinks < 0 || h->nlinks > 2) return PD_VALIDATION_ERROR;
+    for (int l = 0; l < h->nlinks; ++l)
+        if (!h->dst[l] || !h->flag[l] || h->column[l] < 0 || h->column[l] > e->prm.Nxi) return PD_VALIDATION_ERROR;
+    return PD_OK;
+}
+} // namespace
+
+pd_status pd_gaptooth_substep_halo(pd_engine* e, const double* in, double* out, int32_t m, const double* bnd,
+                                   const double* src_time, const pd_halo_out* h) {
+    if (!e || !in || !out || in == out || m < 0 || check_halo(e, h) != PD_OK) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        if (m > e->prm.k) throw Status{PD_VALIDATION_ERROR, "substep index beyond k"};
+        if (e->step_kind == PD_STEP_DIRECT && e->prm.source == PD_SOURCE_GENERAL)
+            throw Status{PD_UNSUPPORTED, "halo-exchanging substep: no general source"};
+        HaloScope scope(e->prm, *h);
+        e->sub_m = m; // (the sampled-table offset; plain tables ignore it)
+        e->launch_step(in, out, OUT_FIELD, e->prm.source ? src_time : nullptr, nullptr);
+        e->launch_refresh(out, in, bnd, nullptr);
+    });
+}
+
+pd_status pd_extrapolate_halo(pd_engine* e, const double* in, const double* Uk, const double* Uk1, double* out,
+                              const double* bnd, const pd_halo_out* h) {
+    if (!e || !in || !Uk || !Uk1 || !out || out == in || check_halo(e, h) != PD_OK) return PD_VALIDATION_ERROR;
+    return guarded(e, [&] {
+        if (e->prm.k < 1) throw Status{PD_VALIDATION_ERROR, "extrapolation entry is for k >= 1"};
+        HaloScope scope(e->prm, *h);
+        const double horizon = e->prm.dt_macro - e->prm.k * e->prm.tau; // cpi.cpp:67-74
+        k_extrapolate<<<(e->prm.P + 255) / 256, 256, 0, e->stream>>>(e->prm, out, Uk, Uk1, e->d_pij.p, horizon,
+                                                                   nullptr);
+        e->check_launch();
+        e->launch_refresh(out, in, bnd, nullptr);
+    });
+}
+
 pd_status pd_stream_wait_flag(pd_engine* e, const uint32_t* flag, uint32_t value) {
     if (!e || !flag) return PD_VALIDATION_ERROR;
     return guarded(e, [&] {

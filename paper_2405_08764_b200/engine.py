@@ -103,11 +103,13 @@ def lib() -> C.CDLL:
     L.pd_coeffs_generate.argtypes = [C.POINTER(EngineDesc), _dp, _dp, _dp]
     L.pd_projective_step_halo.argtypes = [vp, vp, vp, C.c_double, vp, vp, C.POINTER(abi.HaloOut)]
     L.pd_stream_wait_flag.argtypes = [vp, vp, C.c_uint32]
+    L.pd_gaptooth_substep_halo.argtypes = [vp, vp, vp, C.c_int32, vp, vp, C.POINTER(abi.HaloOut)]
+    L.pd_extrapolate_halo.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(abi.HaloOut)]
     L.pd_ipc_alloc.argtypes = [C.c_size_t, C.POINTER(vp), C.c_char_p]
     L.pd_ipc_open.argtypes = [C.c_char_p, C.POINTER(vp)]
     L.pd_ipc_close.argtypes = [vp]
     L.pd_device_free.argtypes = [vp]
-    for name in ["pd_projective_step_halo", "pd_stream_wait_flag", "pd_ipc_alloc", "pd_ipc_open", "pd_ipc_close",
+    for name in ["pd_projective_step_halo", "pd_gaptooth_substep_halo", "pd_extrapolate_halo", "pd_stream_wait_flag", "pd_ipc_alloc", "pd_ipc_open", "pd_ipc_close",
                  "pd_device_free"]:
         getattr(L, name).restype = C.c_int32
     for name in ["pd_bench_step_kernel", "pd_bench_fp64_peak", "pd_engine_create", "pd_engine_tables", "pd_engine_set_stream", "pd_gaptooth_step",

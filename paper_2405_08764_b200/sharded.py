@@ -31,7 +31,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import abi
-from .abi import EngineDesc
+from .abi import EngineDesc, perimeter_len
 
 
 @dataclass
@@ -362,24 +362,32 @@ def _as_tensor(ptr: int, n: int, typestr: str, device):
 class PeerRun:
     """One rank of the cpi::run macro loop (cpi.cpp:175-202) over xi-slabs with
     the fused peer-memory halo.  X[0], X[1]: this rank's ping-pong field
-    buffers; flags: its two incoming link counters (uint32); peers[rank] =
-    (X0 ptr, X1 ptr, flags ptr) of every neighbour.  reduce_max / barrier are
-    the collective hooks (torch.distributed, or the in-process driver)."""
+    buffers; chain: k+1 substep buffers when k > 0 (cpi.cpp:58-77 chains the
+    gap-tooth substeps); flags: its two incoming link counters (uint32);
+    peers[rank] = (X0 ptr, X1 ptr, flags ptr, chain ptrs) of every neighbour.
+    k = 0: one fused kernel per projective step (one counter advance per
+    step); k > 0: k+1 substeps and the extrapolation, each storing its edge
+    columns into the neighbours' matching buffer (k+2 advances per step)."""
 
-    def __init__(self, engine, slab: Slab, Neta: int, X, flags, peers, stream, mask):
+    def __init__(self, engine, slab: Slab, Neta: int, X, flags, peers, stream, mask, k: int = 0, chain=()):
         self.e = engine
         self.s = slab
         self.n2 = Neta + 1
-        self.npc = Neta - 1  # patches per column: one counter increment each per step
+        self.npc = Neta - 1  # patches per column: one counter increment each per piece
+        self.k = k
+        self.inc = 1 if k == 0 else k + 2  # counter advances per projective step
         self.X = X
+        self.chain = list(chain)
+        if k > 0 and len(self.chain) != k + 1:
+            raise ValueError("k > 0 needs k+1 substep buffers")
         self.flags = flags
         self.stream = stream
         self.mask = mask
         self.steps_total = 0  # counters are cumulative over the runner's life
         self.links = []
         for col, nb, side in halo_links(slab):
-            x0, x1, fl = peers[nb]
-            self.links.append((col, (x0, x1), fl + 4 * side))
+            x0, x1, fl, ch = peers[nb]
+            self.links.append((col, (x0, x1), fl + 4 * side, tuple(ch)))
         self.sides = incoming_sides(slab)
         from .engine import _check, lib
 
@@ -394,42 +402,84 @@ class PeerRun:
         with torch.cuda.stream(self.stream):
             self.X[0].copy_(U0)
             self.X[1].copy_(U0)
+            for c in self.chain:  # columns a rank never computes stay finite
+                c.copy_(U0)
+
+    def _halo(self, dst_of):
+        from . import abi
+
+        halo = abi.HaloOut()
+        halo.nlinks = len(self.links)
+        for l, (col, xs, fl, ch) in enumerate(self.links):
+            halo.column[l] = col
+            halo.dst[l] = dst_of(xs, ch)
+            halo.flag[l] = fl
+        return halo
+
+    def _wait(self, piece: int):
+        """Before piece q of the run: both neighbours have finished piece q-1."""
+        from .engine import _check, lib
+
+        if piece <= 0:
+            return
+        target = (piece * self.npc) & 0xFFFFFFFF
+        for side in self.sides:
+            _check(lib().pd_stream_wait_flag(self.e.h, self.flags.data_ptr() + 4 * side, target), self.e.h)
 
     def enqueue_step(self, n: int, t: float, bnd, maxes, src=None):
-        """Step n of the current run: wait for both neighbours' step n-1, the fused
-        step (own patches + edge columns into the neighbours' buffers + counter
-        bumps), the boundary refresh, and this rank's max |U| into maxes[n]."""
+        """Step n of the current run, all pieces at once (one rank per process)."""
+        keep = None
+        for keep in self.step_pieces(n, t, bnd, maxes, src):
+            pass
+        return keep
+
+    def step_pieces(self, n: int, t: float, bnd, maxes, src=None):
+        """Step n of the current run as a generator, one piece per next(): wait for
+        both neighbours' previous piece, then the fused step (k = 0) or one of its
+        k+2 pieces (own patches + edge columns into the neighbours' buffers +
+        counter bumps, boundary refresh); the last piece also records this rank's
+        max |U| into maxes[n].  Ranks sharing a process are advanced piece by
+        piece in turn, so every stream wait is enqueued after the work it waits
+        for (streams may share a hardware queue: a wait ahead of that work in the
+        same queue would never be satisfied)."""
         import torch
 
-        from . import abi
         from .engine import _check, lib
 
         L, h = lib(), self.e.h
-        target = ((self.steps_total + n) * self.npc) & 0xFFFFFFFF
-        if n > 0 or self.steps_total > 0:
-            for side in self.sides:
-                _check(L.pd_stream_wait_flag(h, self.flags.data_ptr() + 4 * side, target), h)
+        dev = self.X[0].device
         out = (n + 1) % 2
-        halo = abi.HaloOut()
-        halo.nlinks = len(self.links)
-        for l, (col, xs, fl) in enumerate(self.links):
-            halo.column[l] = col
-            halo.dst[l] = xs[out]
-            halo.flag[l] = fl
         b = g = None
         with torch.cuda.stream(self.stream):
             if bnd is not None:  # [k+2][perimeter] refresh values of this step
-                b = torch.as_tensor(np.ascontiguousarray(bnd).reshape(-1)).to(self.X[0].device, non_blocking=True)
+                b = torch.as_tensor(np.ascontiguousarray(bnd).reshape(-1)).to(dev, non_blocking=True)
             if src is not None:  # [k+1][nt] separable-source time factors of this step
-                g = torch.as_tensor(np.ascontiguousarray(src).reshape(-1)).to(self.X[0].device, non_blocking=True)
-        _check(L.pd_projective_step_halo(h, self.X[n % 2].data_ptr(), self.X[out].data_ptr(), t,
-                                         None if b is None else b.data_ptr(), None if g is None else g.data_ptr(),
-                                         C.byref(halo)), h)
+                g = torch.as_tensor(np.ascontiguousarray(src).reshape(-1)).to(dev, non_blocking=True)
+        ptr = lambda x, off=0: None if x is None else x.data_ptr() + 8 * off  # noqa: E731
+        first = (self.steps_total + n) * self.inc
+        if self.k == 0:
+            self._wait(first)
+            halo = self._halo(lambda xs, ch: xs[out])
+            _check(L.pd_projective_step_halo(h, self.X[n % 2].data_ptr(), self.X[out].data_ptr(), t, ptr(b), ptr(g),
+                                             C.byref(halo)), h)
+        else:
+            perim = perimeter_len(self.s.Nxi, self.n2 - 1)
+            nt = 0 if g is None else g.numel() // (self.k + 1)
+            for m in range(self.k + 1):
+                self._wait(first + m)
+                src_buf = self.X[n % 2] if m == 0 else self.chain[m - 1]
+                halo = self._halo(lambda xs, ch, m=m: ch[m])
+                _check(L.pd_gaptooth_substep_halo(h, src_buf.data_ptr(), self.chain[m].data_ptr(), m,
+                                                  ptr(b, perim * m), ptr(g, nt * m), C.byref(halo)), h)
+                yield b, g
+            halo = self._halo(lambda xs, ch: xs[out])
+            _check(L.pd_extrapolate_halo(h, self.X[n % 2].data_ptr(), self.chain[self.k - 1].data_ptr(),
+                                         self.chain[self.k].data_ptr(), self.X[out].data_ptr(),
+                                         ptr(b, perim * (self.k + 1)), C.byref(halo)), h)
         with torch.cuda.stream(self.stream):
-            m = torch.where(self.mask, self.X[out].abs(), torch.zeros((), dtype=torch.float64,
-                                                                        device=self.X[0].device)).amax()
-            maxes[n] = torch.where(torch.isfinite(m), m, torch.full_like(m, float("inf")))
-        return b, g
+            mx = torch.where(self.mask, self.X[out].abs(), torch.zeros((), dtype=torch.float64, device=dev)).amax()
+            maxes[n] = torch.where(torch.isfinite(mx), mx, torch.full_like(mx, float("inf")))
+        yield b, g
 
     def result(self, nsteps: int):
         return self.X[nsteps % 2]
@@ -470,9 +520,17 @@ def run_peer(runners, U0s, nsteps: int, dt: float, t0: float = 0.0, bnd_table=No
             evs.append(ev)
         keep = []
         for n in range(steps):
-            for r, mx in zip(runners, maxes):
-                keep.append(r.enqueue_step(n, t0 + n * dt, None if bnd_table is None else bnd_table[n], mx,
-                                           None if src_table is None else src_table[n]))
+            gens = [r.step_pieces(n, t0 + n * dt, None if bnd_table is None else bnd_table[n], mx,
+                                  None if src_table is None else src_table[n]) for r, mx in zip(runners, maxes)]
+            while gens:  # piece q of every rank before piece q+1 of any (dependency order)
+                live = []
+                for gen in gens:
+                    try:
+                        keep.append(next(gen))
+                        live.append(gen)
+                    except StopIteration:
+                        pass
+                gens = live
         for r, ev in zip(runners, evs):
             ev[1].record(r.stream)
         # bounded wait: a counter that never arrives (a peer that died, a broken
@@ -499,24 +557,27 @@ def run_peer(runners, U0s, nsteps: int, dt: float, t0: float = 0.0, bnd_table=No
     return [RunResult(r.result(fail), fail - 1, fail, t) for r, t in zip(runners, ms)]
 
 
-def local_peer_group(engines, slab_list, Neta: int, device):
+def local_peer_group(engines, slab_list, Neta: int, device, k: int = 0):
     """All ranks of a decomposition in ONE process (one device or several with
     peer access): each rank's buffers and counters are plain device
     allocations, the neighbours' pointers are used directly."""
     import torch
 
     NF = (slab_list[0].Nxi + 1) * (Neta + 1)
+    nch = k + 1 if k > 0 else 0
     bufs = [[torch.empty(NF, dtype=torch.float64, device=device) for _ in range(2)] for _ in slab_list]
+    chains = [[torch.empty(NF, dtype=torch.float64, device=device) for _ in range(nch)] for _ in slab_list]
     flags = [torch.zeros(2, dtype=torch.int32, device=device) for _ in slab_list]
-    peers = {r: (bufs[r][0].data_ptr(), bufs[r][1].data_ptr(), flags[r].data_ptr()) for r in range(len(slab_list))}
+    peers = {r: (bufs[r][0].data_ptr(), bufs[r][1].data_ptr(), flags[r].data_ptr(),
+                 tuple(c.data_ptr() for c in chains[r])) for r in range(len(slab_list))}
     out = []
     for r, (E, sl) in enumerate(zip(engines, slab_list)):
         mask = ShardedRun(sl, Neta, None, None).owned_mask(device)
-        out.append(PeerRun(E, sl, Neta, bufs[r], flags[r], peers, torch.cuda.Stream(device), mask))
+        out.append(PeerRun(E, sl, Neta, bufs[r], flags[r], peers, torch.cuda.Stream(device), mask, k, chains[r]))
     return out
 
 
-def peer_runner(engine, slab: Slab, Neta: int, dist, device, group=None):
+def peer_runner(engine, slab: Slab, Neta: int, dist, device, group=None, k: int = 0):
     """This process's rank of a one-process-per-GPU decomposition: buffers and
     counters from pd_ipc_alloc, the neighbours' opened with CUDA IPC (lazy
     peer access: NVLink/NVSwitch stores on a B200 node)."""
@@ -533,27 +594,30 @@ def peer_runner(engine, slab: Slab, Neta: int, dist, device, group=None):
         return p.value, h.raw
 
     (x0, h0), (x1, h1), (fl, hf) = alloc(NF * 8), alloc(NF * 8), alloc(64)
+    ch = [alloc(NF * 8) for _ in range(k + 1 if k > 0 else 0)]
     handles = [None] * dist.get_world_size(group)
-    dist.all_gather_object(handles, (slab.rank, h0, h1, hf), group=group)
+    dist.all_gather_object(handles, (slab.rank, h0, h1, hf, [hc for _, hc in ch]), group=group)
     peers, opened = {}, []
-    for rank, a, b, f in handles:
+
+    def open_(hnd):
+        p = C.c_void_p()
+        _check(L.pd_ipc_open(C.create_string_buffer(hnd, 64), C.byref(p)))
+        opened.append(p.value)
+        return p.value
+
+    for rank, a, b, f, hcs in handles:
         if rank == slab.rank:
-            peers[rank] = (x0, x1, fl)
+            peers[rank] = (x0, x1, fl, tuple(pc for pc, _ in ch))
             continue
         if rank not in {nb for _, nb, _ in halo_links(slab)}:
             continue
-        ptrs = []
-        for hnd in (a, b, f):
-            p = C.c_void_p()
-            _check(L.pd_ipc_open(C.create_string_buffer(hnd, 64), C.byref(p)))
-            ptrs.append(p.value)
-            opened.append(p.value)
-        peers[rank] = tuple(ptrs)
+        peers[rank] = (open_(a), open_(b), open_(f), tuple(open_(hc) for hc in hcs))
     X = [_as_tensor(x0, NF, "<f8", device), _as_tensor(x1, NF, "<f8", device)]
+    chain = [_as_tensor(pc, NF, "<f8", device) for pc, _ in ch]
     flags = _as_tensor(fl, 2, "<i4", device)
     mask = ShardedRun(slab, Neta, None, None).owned_mask(device)
-    run = PeerRun(engine, slab, Neta, X, flags, peers, torch.cuda.Stream(device), mask)
-    run._owned = (x0, x1, fl)
+    run = PeerRun(engine, slab, Neta, X, flags, peers, torch.cuda.Stream(device), mask, k, chain)
+    run._owned = (x0, x1, fl) + tuple(pc for pc, _ in ch)
     run._opened = opened
     return run
 

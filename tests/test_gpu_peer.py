@@ -132,7 +132,7 @@ def _ipc_worker(rank, world, port, name, over, mode, nsteps, out):
     sl = sharded.slabs(ed.Nxi, bool(ed.periodic_xi), world)[rank]
     dev = torch.device("cuda", 0)
     E = Engine(sharded.subset_desc(ed, sl), mode)
-    run = sharded.peer_runner(E, sl, ed.Neta, dist, dev)
+    run = sharded.peer_runner(E, sl, ed.Neta, dist, dev, k=ed.k)
 
     def red(x):
         t = x.detach().cpu().clone()
@@ -148,8 +148,9 @@ def _ipc_worker(rank, world, port, name, over, mode, nsteps, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,over,world", [("c3_annulus", {}, 2), ("c4_shear", {"N_xi": 65, "N_eta": 33, "Nt": 8}, 3)],
-                         ids=["c3-w2", "c4-small-w3"])
+@pytest.mark.parametrize("name,over,world", [("c3_annulus", {}, 2), ("c4_shear", {"N_xi": 65, "N_eta": 33, "Nt": 8}, 3),
+                                             ("c1_diffusion", {"k": 1}, 2)],
+                         ids=["c3-w2", "c4-small-w3", "c1-k1-w2"])
 def test_peer_halo_ipc_processes_equal_single_engine(name, over, world, gpu):
     import socket
 
@@ -209,6 +210,7 @@ def test_bench_multi_rank_path_runs_peer_exchange(gpu):
 
 
 def _peer_vs_single(P, mode, world, nsteps, bnd=None, src=None, linear=False):
+    """Decomposed run (in-process ranks) and the single-engine run of P."""
     import torch
 
     ed = P.engine_desc()
@@ -221,7 +223,7 @@ def _peer_vs_single(P, mode, world, nsteps, bnd=None, src=None, linear=False):
         w = E.set_linear()
         for Es in engines:
             Es.set_linear(w)
-    runners = sharded.local_peer_group(engines, sls, ed.Neta, dev)
+    runners = sharded.local_peer_group(engines, sls, ed.Neta, dev, k=ed.k)
     U0 = P.initial_field()
     Ut = torch.from_numpy(U0.reshape(-1).copy()).to(dev)
     res = sharded.run_peer(runners, [Ut] * world, nsteps, P.desc.T / P.desc.Nt, 0.0, bnd, src_table=src)
@@ -247,4 +249,20 @@ def test_peer_halo_linear_response_step(name, gpu):
     gaptooth.cpp:396-418) with the full engine's row weights on every slab."""
     P = Problem(configs.load(name)[0])
     full, Uref = _peer_vs_single(P, EXACT, 2, 15, linear=True)
+    assert np.array_equal(full, Uref)
+
+
+@pytest.mark.parametrize("name,over", [("c1_diffusion", {"k": 1}), ("c3_annulus", {"k": 2}),
+                                       ("ref_table1_cdr_const", {"problem": abi.PD_PROBLEM_REF_CDR_VAR, "k": 1})],
+                         ids=["c1-k1", "c3-k2", "adi-var-k1"])
+@pytest.mark.parametrize("mode", [EXACT, FAST], ids=["exact", "fast"])
+def test_peer_halo_k_substeps(name, over, mode, gpu):
+    """k > 0 (cpi.cpp:58-77 chains k+1 gap-tooth substeps): each substep and the
+    extrapolation store their edge columns into the neighbours' matching buffers
+    (pd_gaptooth_substep_halo / pd_extrapolate_halo), k+2 counter advances per
+    projective step; bit-identical to the single engine."""
+    P = Problem(configs.copy_desc(configs.load(name)[0], **over))
+    assert P.desc.k == over["k"]
+    n = 8
+    full, Uref = _peer_vs_single(P, mode, 3, n, P.boundary_table(0.0, n), P.source_time(0.0, n))
     assert np.array_equal(full, Uref)
