@@ -15,12 +15,20 @@ column on each side, and the global boundary) are ever current.  Per substep:
 
 Results do not depend on the decomposition: every patch value is computed from
 the same stencil values in the same arithmetic, so the sharded run equals the
-single-engine run bit for bit (tests/test_dist.py).  The exchange uses
-torch.distributed point-to-point ops — NCCL over NVLink on GPUs, gloo on CPU.
+single-engine run bit for bit (tests/test_dist.py, tests/test_gpu_peer.py).
 
-The compute is injected (``step_fn``): the product wiring (``device_step_fn``)
-runs the engine's fused projective step on device buffers; the CPU tests pass
-the restated oracle.
+Two transports:
+
+* ``PeerRun`` / ``run_peer`` (the product path, bench.py --gpus N): step 2 is
+  fused into step 1 — the step kernel stores its edge columns straight into the
+  neighbours' buffers (NVLink peer / CUDA IPC mappings) and bumps their link
+  counters, each rank's stream waits on its own counters (stream memory
+  operations), and the guard is ONE all-reduce of the per-step maxima after the
+  loop;
+* ``ShardedRun`` (the baseline, and the CPU tests): torch.distributed
+  point-to-point ops for step 2 — NCCL on GPUs, gloo on CPU; the compute is
+  injected (``step_fn``: the engine's fused projective step on device buffers,
+  or the restated oracle in the CPU tests).
 """
 from __future__ import annotations
 
