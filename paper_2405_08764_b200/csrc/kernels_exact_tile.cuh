@@ -1,0 +1,342 @@
+// EXACT-mode fused gap-tooth step on the register-blocked tile mapping.
+//
+// Same arithmetic as k_gaptooth_exact (kernels_exact.cuh): every operation an
+// explicitly rounded IEEE add / mul / div in the reference's evaluation order,
+// never contracted into FMA, so a patch evolves bit-identically to the
+// reference's CPU build (microsim.cpp:292-332, 509-552; gaptooth.cpp:110-194).
+// What changes is where the data lives: the mapping of kernels_fast.cuh.  A
+// patch of N1 x N2 micro nodes is split into BI x BJ node blocks, one block per
+// lane (LP lanes per patch, G = 32/LP patches per warp, one warp per CTA); the
+// lane keeps its nodes' state and their six solver-form coefficients in
+// REGISTERS for all K micro-steps, and neighbour values cross lanes through
+// constant-delta warp shuffles.  The shared-memory kernel it replaces re-read
+// the coefficient tables from global memory and the state from shared memory at
+// every micro-step, with one CTA barrier per step.
+//
+// Scope: the explicit micro-solver, zero source, Neumann or (unpinned) Robin
+// patch edges, the exact-fit tiles 7x7, 8x8, 9x9 and 16x16, with or without the
+// mixed term.  Everything else stays on k_gaptooth_exact (exact_tile_plan).
+#pragma once
+
+#include <cstdlib>
+
+#include "pd_device.cuh"
+#include "kernels_exact.cuh"
+
+namespace pdb200::dev {
+
+template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
+struct XTileCfg {
+    static constexpr int N1 = N1_, N2 = N2_, BI = BI_, BJ = BJ_;
+    static constexpr bool MIXED = MIXED_;
+    static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, G = 32 / LP;
+    static constexpr int N = N1 * N2, L = N1 > N2 ? N1 : N2;
+    static_assert(N1 % BI == 0 && N2 % BJ == 0, "block must tile the patch");
+    static_assert(LP <= 32, "patch must fit a warp");
+    // a lane on the W edge must not also be on the E edge (its inner node would
+    // be a ghost): at least two block columns; along eta one block column is fine
+    // when the block itself holds the inner nodes
+    static_assert(LI >= 2 && (LJ >= 2 || BJ >= 3), "edge lanes need real inner nodes");
+};
+
+// ghost value of an unpinned edge: cIn u(inner) + cEdge u(edge) + b with
+// cIn = 1 (make_ghost, microsim.cpp:160-183; explicit_sweep :314-323).
+// 1.0 * x is x for every double, so that product is not issued.
+__device__ __forceinline__ double ghost_t(double cEdge, double u_inner, double u_edge, double b) {
+    return XADD(XADD(u_inner, XMUL(cEdge, u_edge)), b);
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(32, Cfg::MIXED ? 10 : 12)
+k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
+             const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
+             const int* __restrict__ fail_flag, int nunits) {
+    constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LJ = Cfg::LJ, LP = Cfg::LP, G = Cfg::G;
+    constexpr int N1 = Cfg::N1, N2 = Cfg::N2, N = Cfg::N, L = Cfg::L;
+    constexpr int nx = N1 - 1, ny = N2 - 1;
+    constexpr bool MIXED = Cfg::MIXED;
+    __shared__ double s_st[G][9];
+    __shared__ double s_slope[G][4][L], s_val[G][4][L];
+    // ghost offsets b[k] per edge, one pad entry at each end: the step loop reads rows / columns
+    // j0 - 1 .. j0 + BJ with immediate offsets (the out-of-range ends are never selected)
+    __shared__ double s_gb[G][4][L + 2];
+    __shared__ double s_u[G][N];
+    __shared__ double s_row[G][N1];
+    if (fail_flag && *fail_flag) return;
+    const int unit = blockIdx.x;
+    if (unit >= nunits) return;
+    const int lane = threadIdx.x;
+    const int g = lane / LP, r = lane % LP;
+    const int gs = g < G ? g : 0;
+    const int patch = unit * G + g;
+    const bool valid = g < G && patch < p.P;
+    const int bi = r % LI, bj = r / LI;
+    const int i0 = bi * BI, j0 = bj * BJ;
+    const bool isW = bi == 0, isE = bi == LI - 1, isS = bj == 0, isN = bj == LJ - 1;
+
+    // ---- build_stencil (gaptooth.cpp:74-104) ----------------------------------
+    int pi = 0, pj = 0, ic = 0;
+    if (valid) {
+        pi = pij[2 * patch];
+        pj = pij[2 * patch + 1];
+        ic = pi;
+        if (p.periodic) ic = ((pi % p.Nxi) + p.Nxi) % p.Nxi;
+        for (int t = r; t < 9; t += LP) {
+            const int dp = t / 3 - 1, dq = t % 3 - 1;
+            const int ip = p.periodic ? ((ic + dp) % p.Nxi + p.Nxi) % p.Nxi : pi + dp;
+            s_st[gs][t] = F[(size_t)ip * p.NF2 + pj + dq];
+        }
+    }
+    __syncwarp();
+    const double* v = s_st[gs];
+    const double xi_c = XADD(p.a, XMUL(p.Dxi, (double)ic));
+    const double eta_c = XADD(p.c, XMUL(p.Deta, (double)pj));
+
+    // ---- edge profiles and ghost offsets (gaptooth.cpp:110-152, microsim.cpp:152-186)
+    const bool robin = p.bc_type == PD_BC_ROBIN;
+    if (valid) {
+        edge_profiles_t(v, xi_c, eta_c, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny, L, true, robin, &s_slope[gs][0][0],
+                        &s_val[gs][0][0], r, LP);
+    }
+    __syncwarp();
+    double cedge[4] = {0.0, 0.0, 0.0, 0.0}; // E, W, N, S
+    if (valid) {
+        const int kind = robin ? PD_EDGE_ROBIN : PD_EDGE_NEUMANN;
+        EdgeSh eg;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdxi, +1.0, N2, s_val[gs][PD_EDGE_E], s_slope[gs][PD_EDGE_E],
+                     &s_gb[gs][PD_EDGE_E][1], r, LP);
+        cedge[PD_EDGE_E] = eg.cEdge;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdxi, -1.0, N2, s_val[gs][PD_EDGE_W], s_slope[gs][PD_EDGE_W],
+                     &s_gb[gs][PD_EDGE_W][1], r, LP);
+        cedge[PD_EDGE_W] = eg.cEdge;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdeta, +1.0, N1, s_val[gs][PD_EDGE_N], s_slope[gs][PD_EDGE_N],
+                     &s_gb[gs][PD_EDGE_N][1], r, LP);
+        cedge[PD_EDGE_N] = eg.cEdge;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdeta, -1.0, N1, s_val[gs][PD_EDGE_S], s_slope[gs][PD_EDGE_S],
+                     &s_gb[gs][PD_EDGE_S][1], r, LP);
+        cedge[PD_EDGE_S] = eg.cEdge;
+    }
+    __syncwarp();
+    // This lane's ghost data, by role: a lane is on at most one xi edge (LI >= 2);
+    // on both eta edges only when LJ == 1, where S and N are kept apart.
+    // gbx[b + 1]: offset of the lane's xi edge at row j0 + b, b in [-1, BJ];
+    // gbs / gbn[a + 1]: offsets of the S / N edge at column i0 + a, a in [-1, BI]
+    // (read from shared memory in the step loop: registers go to the coefficients).
+    const int ex = isE ? PD_EDGE_E : PD_EDGE_W;
+    const double cEx = isE ? cedge[PD_EDGE_E] : cedge[PD_EDGE_W], cEs = cedge[PD_EDGE_S], cEn = cedge[PD_EDGE_N];
+    const double* gbx = &s_gb[gs][ex][j0];
+    const double* gbs = &s_gb[gs][PD_EDGE_S][i0];
+    const double* gbn = &s_gb[gs][PD_EDGE_N][i0];
+
+    // ---- coefficients of this lane's nodes into registers --------------------
+    double co[PD_NCOEF][BI][BJ];
+    {
+        const int set = valid ? (cset ? cset[patch] : patch) : 0;
+        const double* cf = coeffs + (size_t)set * PD_NCOEF * N;
+#pragma unroll
+        for (int c = 0; c < PD_NCOEF; ++c) {
+            if (!MIXED && c == PD_COEF_B) continue;
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii) {
+                const double* row = cf + (size_t)c * N + (i0 + ii) * N2 + j0;
+                if constexpr (BJ % 2 == 0 && N2 % 2 == 0) { // 16-byte aligned pairs
+#pragma unroll
+                    for (int jj = 0; jj < BJ; jj += 2) {
+                        const double2 t = valid ? __ldg(reinterpret_cast<const double2*>(row + jj)) : make_double2(0.0, 0.0);
+                        co[c][ii][jj] = t.x;
+                        co[c][ii][jj + 1] = t.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < BJ; ++jj) co[c][ii][jj] = valid ? __ldg(row + jj) : 0.0;
+                }
+            }
+        }
+    }
+
+    // ---- StencilPoly::center + lift (gaptooth.cpp:63-72, 154-168) ------------
+    // E[a + 1][b + 1] = value at block-relative (a, b), a in [-1, BI], b in [-1, BJ]
+    double E[BI + 2][BJ + 2];
+    {
+        const LiftConsts lc = lift_consts_x(v, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = lift_node_x(lc, p.h_xi, p.h_eta, i0 + ii, j0 + jj);
+    }
+
+    // ---- K explicit sweeps (microsim.cpp:292-332, 535-550) -------------------
+    const double idx2 = XDIV(1.0, XMUL(p.mdxi, p.mdxi)), idy2 = XDIV(1.0, XMUL(p.mdeta, p.mdeta));
+    const double idx = XDIV(1.0, XMUL(2.0, p.mdxi)), idy = XDIV(1.0, XMUL(2.0, p.mdeta));
+    const double ixy = XDIV(1.0, XMUL(XMUL(4.0, p.mdxi), p.mdeta));
+    const double dt = p.mdt;
+    constexpr int B0 = MIXED ? -1 : 0, B1 = MIXED ? BJ : BJ - 1; // rows / columns whose halo is needed
+    constexpr int A0 = MIXED ? -1 : 0, A1 = MIXED ? BI : BI - 1;
+    for (int step = 0; step < p.nt; ++step) {
+        // eta halos from lane +-LI, then xi halos (and, for the mixed term, the
+        // corners: the neighbour's eta halo) from lane +-1
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            E[ii + 1][BJ + 1] = __shfl_down_sync(0xffffffffu, E[ii + 1][1], LI);
+            E[ii + 1][0] = __shfl_up_sync(0xffffffffu, E[ii + 1][BJ], LI);
+        }
+#pragma unroll
+        for (int b = B0; b <= B1; ++b) {
+            E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
+            E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
+        }
+        // Patch edges: replace what the shuffles brought by the ghost values
+        // (explicit_sweep, microsim.cpp:314-323; at_ext_x for the mixed term's
+        // diagonal neighbours).  Every formula reads own nodes or halo entries
+        // that are real nodes for this lane, never an entry written here.
+        // S / N ghosts of the columns a in [A0, A1] inside the patch
+#pragma unroll
+        for (int a = A0; a <= A1; ++a) {
+            const bool inside = !(a == -1 && isW) && !(a == BI && isE);
+            const double gsv = ghost_t(cEs, E[a + 1][2], E[a + 1][1], gbs[a + 1]);
+            const double gnv = ghost_t(cEn, E[a + 1][BJ - 1], E[a + 1][BJ], gbn[a + 1]);
+            if (isS && inside) E[a + 1][0] = gsv;
+            if (isN && inside) E[a + 1][BJ + 1] = gnv;
+        }
+        // W / E ghosts of the rows b in [B0, B1] inside the patch (one xi role per lane)
+#pragma unroll
+        for (int b = B0; b <= B1; ++b) {
+            const bool inside = !(b == -1 && isS) && !(b == BJ && isN);
+            const double inner = isE ? E[BI - 1][b + 1] : E[2][b + 1];
+            const double edge = isE ? E[BI][b + 1] : E[1][b + 1];
+            const double gv = ghost_t(cEx, inner, edge, gbx[b + 1]);
+            if (isW && inside) E[0][b + 1] = gv;
+            if (isE && inside) E[BI + 1][b + 1] = gv;
+        }
+        if constexpr (MIXED) {
+            // patch corners: the double ghost u(ii, jj) + ox + oy (at_ext_x),
+            // branch-free: computed by every lane, kept by the corner lanes
+            const bool xedge = isW || isE;
+            {
+                const double ue = isE ? E[BI][1] : E[1][1];
+                const double ox = XADD(XMUL(cEx, ue), gbx[1]);
+                const double oy = XADD(XMUL(cEs, ue), isE ? gbs[BI] : gbs[1]);
+                const double cv = XADD(XADD(isE ? E[BI - 1][2] : E[2][2], ox), oy);
+                if (isS && isE) E[BI + 1][0] = cv;
+                if (isS && xedge && !isE) E[0][0] = cv;
+            }
+            {
+                const double ue = isE ? E[BI][BJ] : E[1][BJ];
+                const double ox = XADD(XMUL(cEx, ue), gbx[BJ]);
+                const double oy = XADD(XMUL(cEn, ue), isE ? gbn[BI] : gbn[1]);
+                const double cv = XADD(XADD(isE ? E[BI - 1][BJ - 1] : E[2][BJ - 1], ox), oy);
+                if (isN && isE) E[BI + 1][BJ + 1] = cv;
+                if (isN && xedge && !isE) E[0][BJ + 1] = cv;
+            }
+        }
+        double nu[BI][BJ];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+                const double uc = E[ii + 1][jj + 1];
+                const double uW = E[ii][jj + 1], uE = E[ii + 2][jj + 1];
+                const double uS = E[ii + 1][jj], uN = E[ii + 1][jj + 2];
+                const double uc2 = XMUL(2.0, uc);
+                const double uxx = XMUL(XADD(XSUB(uW, uc2), uE), idx2);
+                const double uyy = XMUL(XADD(XSUB(uS, uc2), uN), idy2);
+                const double ux = XMUL(XSUB(uE, uW), idx);
+                const double uy = XMUL(XSUB(uN, uS), idy);
+                double s = XMUL(co[PD_COEF_A][ii][jj], uxx);
+                if constexpr (MIXED) {
+                    const double nE = E[ii + 2][jj + 2], sE = E[ii + 2][jj], nW = E[ii][jj + 2], sW = E[ii][jj];
+                    const double uxy = XMUL(XADD(XSUB(XSUB(nE, sE), nW), sW), ixy);
+                    s = XADD(s, XMUL(co[PD_COEF_B][ii][jj], uxy));
+                }
+                s = XADD(s, XMUL(co[PD_COEF_C][ii][jj], uyy));
+                s = XSUB(s, XMUL(co[PD_COEF_VX][ii][jj], ux));
+                s = XSUB(s, XMUL(co[PD_COEF_VY][ii][jj], uy));
+                s = XSUB(s, XMUL(co[PD_COEF_W][ii][jj], uc));
+                s = XADD(s, 0.0); // + G with the zero source (microsim.cpp:329)
+                nu[ii][jj] = XADD(uc, XMUL(dt, s));
+            }
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = nu[ii][jj];
+    }
+
+    // ---- restrict_average in the reference order (gaptooth.cpp:170-194) ------
+    if (g < G) { // (lanes past the last patch of the warp hold nothing)
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) s_u[gs][(i0 + ii) * N2 + j0 + jj] = E[ii + 1][jj + 1];
+    }
+    __syncwarp();
+    if (valid) {
+        for (int i = r; i <= nx; i += LP) {
+            double rs = 0.0;
+            for (int j = 0; j <= ny; ++j) rs = XADD(rs, XMUL(quad_w(j, ny, p.quad), s_u[gs][i * N2 + j]));
+            s_row[gs][i] = rs;
+        }
+    }
+    __syncwarp();
+    if (valid && r == 0) {
+        double avg = 0.0;
+        for (int i = 0; i <= nx; ++i) avg = XADD(avg, XMUL(quad_w(i, nx, p.quad), s_row[gs][i]));
+        const size_t node = (size_t)pi * p.NF2 + pj;
+        if (out_mode == OUT_FIELD) {
+            out[node] = avg;
+            halo_store(p, node, avg);
+        } else if (out_mode == OUT_PROJECTIVE) {
+            const double U = F[node];
+            const double Fd = XDIV(XSUB(avg, U), p.tau); // estimate_derivative  cpi.cpp:54
+            const double w = XADD(U, XMUL(p.dt_macro, Fd)); // cpi.cpp:74 with k = 0
+            out[node] = w;
+            halo_store(p, node, w);
+        } else {
+            out[patch] = avg;
+        }
+    }
+}
+
+// ---- dispatch -----------------------------------------------------------------
+using XT7 = XTileCfg<7, 7, 1, 7, false>;
+using XT7M = XTileCfg<7, 7, 1, 7, true>;
+using XT8 = XTileCfg<8, 8, 2, 4, false>;
+using XT8M = XTileCfg<8, 8, 2, 4, true>;
+using XT9 = XTileCfg<9, 9, 3, 3, false>;
+using XT9M = XTileCfg<9, 9, 3, 3, true>;
+using XT16 = XTileCfg<16, 16, 2, 4, false>;
+using XT16M = XTileCfg<16, 16, 2, 4, true>;
+#define PD_XTILE_CONFIGS(X) X(0, XT7) X(1, XT7M) X(2, XT8) X(3, XT8M) X(4, XT9) X(5, XT9M) X(6, XT16) X(7, XT16M)
+
+// Tile id of the register-blocked EXACT step for these parameters, or -1: the
+// shared-memory kernel (k_gaptooth_exact) carries everything else — ADI,
+// sources, pinned (Dirichlet / degenerate Robin) edges, other patch shapes.
+// PD_EXACT_TILE=0 forces -1 (A/B runs and the equality test of the two kernels).
+inline int exact_tile_plan(const Params& p) {
+    static const bool off = [] {
+        const char* e = std::getenv("PD_EXACT_TILE");
+        return e && e[0] == '0';
+    }();
+    if (off) return -1;
+    if (p.solver != PD_SOLVER_EXPLICIT || p.source != PD_SOURCE_ZERO) return -1;
+    if (p.bc_type == PD_BC_DIRICHLET) return -1;
+    if (p.bc_type == PD_BC_ROBIN && fabs(p.w2) < 1e-300) return -1; // pinned (microsim.cpp:171-174)
+    int id = -1;
+#define PD_XMATCH(ID, CFG) \
+    if (p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
+    PD_XTILE_CONFIGS(PD_XMATCH)
+#undef PD_XMATCH
+    return id;
+}
+
+inline void launch_exact_tile(int id, const Params& p, const double* F, double* out, int out_mode, const int* pij,
+                              const int* cset, const double* coeffs, const int* fail, cudaStream_t s) {
+#define PD_XLAUNCH(ID, CFG)                                                                              \
+    if (id == ID) {                                                                                      \
+        const int nunits = (p.P + CFG::G - 1) / CFG::G;                                                  \
+        k_exact_tile<CFG><<<nunits, 32, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail, nunits); \
+    }
+    PD_XTILE_CONFIGS(PD_XLAUNCH)
+#undef PD_XLAUNCH
+}
+
+} // namespace pdb200::dev

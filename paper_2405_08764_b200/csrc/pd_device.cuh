@@ -145,13 +145,14 @@ __device__ inline double poly_x(const double* v, double xi_c, double eta_c, doub
 
 // Edge profiles (slopes and/or values), one element per thread iteration:
 // dirichlet_edge_values / neumann_edge_slopes  gaptooth.cpp:110-152.
-__device__ inline void edge_profiles_x(const double* v, double xi_c, double eta_c, double Dxi, double Deta,
+// (tid, nth): this thread's index and the thread count of the group sharing the patch
+__device__ inline void edge_profiles_t(const double* v, double xi_c, double eta_c, double Dxi, double Deta,
                                        double h_xi, double h_eta, int nx, int ny, int L, bool want_slope,
-                                       bool want_value, double* slope, double* val) {
+                                       bool want_value, double* slope, double* val, int tid, int nth) {
     const double xiE = XADD(xi_c, XMUL(0.5, h_xi)), xiW = XSUB(xi_c, XMUL(0.5, h_xi));
     const double etaN = XADD(eta_c, XMUL(0.5, h_eta)), etaS = XSUB(eta_c, XMUL(0.5, h_eta));
     const int nEW = ny + 1, total = 2 * (ny + 1) + 2 * (nx + 1);
-    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    for (int t = tid; t < total; t += nth) {
         if (t < 2 * nEW) {
             const int j = t % nEW, e = t < nEW ? PD_EDGE_E : PD_EDGE_W;
             const double eta = XADD(etaS, XDIV(XMUL(h_eta, (double)j), (double)ny));
@@ -168,36 +169,53 @@ __device__ inline void edge_profiles_x(const double* v, double xi_c, double eta_
     }
 }
 
+__device__ inline void edge_profiles_x(const double* v, double xi_c, double eta_c, double Dxi, double Deta,
+                                       double h_xi, double h_eta, int nx, int ny, int L, bool want_slope,
+                                       bool want_value, double* slope, double* val) {
+    edge_profiles_t(v, xi_c, eta_c, Dxi, Deta, h_xi, h_eta, nx, ny, L, want_slope, want_value, slope, val,
+                    (int)threadIdx.x, (int)blockDim.x);
+}
+
 // StencilPoly::center + lift  gaptooth.cpp:63-72, 154-168
+struct LiftConsts {
+    double C0, Uxi, Ueta, Uxixi, Uetaeta, Uxieta, gdxi, gdeta;
+};
+__device__ inline LiftConsts lift_consts_x(const double* v, double Dxi, double Deta, double h_xi, double h_eta,
+                                           int nx, int ny) {
+    LiftConsts c;
+    const double U = v[4];
+    c.Uxi = XDIV(XSUB(v[7], v[1]), XMUL(2.0, Dxi));
+    c.Ueta = XDIV(XSUB(v[5], v[3]), XMUL(2.0, Deta));
+    c.Uxixi = XDIV(XADD(XSUB(v[7], XMUL(2.0, v[4])), v[1]), XMUL(Dxi, Dxi));
+    c.Uetaeta = XDIV(XADD(XSUB(v[5], XMUL(2.0, v[4])), v[3]), XMUL(Deta, Deta));
+    c.Uxieta = XDIV(XADD(XSUB(XSUB(v[8], v[6]), v[2]), v[0]), XMUL(XMUL(4.0, Dxi), Deta));
+    c.C0 = XSUB(XSUB(U, XMUL(XDIV(XMUL(h_xi, h_xi), 24.0), c.Uxixi)),
+                XMUL(XDIV(XMUL(h_eta, h_eta), 24.0), c.Uetaeta));
+    c.gdxi = XDIV(h_xi, (double)nx);
+    c.gdeta = XDIV(h_eta, (double)ny);
+    return c;
+}
+__device__ inline double lift_node_x(const LiftConsts& c, double h_xi, double h_eta, int i, int j) {
+    const double X = XADD(XMUL(-0.5, h_xi), XMUL(c.gdxi, (double)i));
+    const double Y = XADD(XMUL(-0.5, h_eta), XMUL(c.gdeta, (double)j));
+    double r = XADD(c.C0, XMUL(X, c.Uxi));
+    r = XADD(r, XMUL(Y, c.Ueta));
+    r = XADD(r, XMUL(XMUL(XMUL(0.5, X), X), c.Uxixi));
+    r = XADD(r, XMUL(XMUL(X, Y), c.Uxieta));
+    r = XADD(r, XMUL(XMUL(XMUL(0.5, Y), Y), c.Uetaeta));
+    return r;
+}
 __device__ inline void lift_x(const double* v, double Dxi, double Deta, double h_xi, double h_eta, int nx,
                               int ny, double* u) {
-    const double U = v[4];
-    const double Uxi = XDIV(XSUB(v[7], v[1]), XMUL(2.0, Dxi));
-    const double Ueta = XDIV(XSUB(v[5], v[3]), XMUL(2.0, Deta));
-    const double Uxixi = XDIV(XADD(XSUB(v[7], XMUL(2.0, v[4])), v[1]), XMUL(Dxi, Dxi));
-    const double Uetaeta = XDIV(XADD(XSUB(v[5], XMUL(2.0, v[4])), v[3]), XMUL(Deta, Deta));
-    const double Uxieta = XDIV(XADD(XSUB(XSUB(v[8], v[6]), v[2]), v[0]), XMUL(XMUL(4.0, Dxi), Deta));
-    const double C0 = XSUB(XSUB(U, XMUL(XDIV(XMUL(h_xi, h_xi), 24.0), Uxixi)),
-                           XMUL(XDIV(XMUL(h_eta, h_eta), 24.0), Uetaeta));
-    const double gdxi = XDIV(h_xi, (double)nx), gdeta = XDIV(h_eta, (double)ny);
+    const LiftConsts c = lift_consts_x(v, Dxi, Deta, h_xi, h_eta, nx, ny);
     const int n2 = ny + 1, N = (nx + 1) * n2;
-    for (int t = threadIdx.x; t < N; t += blockDim.x) {
-        const int i = t / n2, j = t % n2;
-        const double X = XADD(XMUL(-0.5, h_xi), XMUL(gdxi, (double)i));
-        const double Y = XADD(XMUL(-0.5, h_eta), XMUL(gdeta, (double)j));
-        double r = XADD(C0, XMUL(X, Uxi));
-        r = XADD(r, XMUL(Y, Ueta));
-        r = XADD(r, XMUL(XMUL(XMUL(0.5, X), X), Uxixi));
-        r = XADD(r, XMUL(XMUL(X, Y), Uxieta));
-        r = XADD(r, XMUL(XMUL(XMUL(0.5, Y), Y), Uetaeta));
-        u[t] = r;
-    }
+    for (int t = threadIdx.x; t < N; t += blockDim.x) u[t] = lift_node_x(c, h_xi, h_eta, t / n2, t % n2);
 }
 
 // make_ghost  microsim.cpp:152-186, for edge e (sign +1 on E/N, -1 on W/S).
 // Scalars are computed redundantly by every thread; b[k] split across threads.
-__device__ inline void make_ghost_x(EdgeSh& g, int kind, double w1, double w2, double delta, double sign,
-                                    int len, const double* value, const double* slope, double* b) {
+__device__ inline void make_ghost_t(EdgeSh& g, int kind, double w1, double w2, double delta, double sign,
+                                    int len, const double* value, const double* slope, double* b, int tid, int nth) {
     g.kind = kind;
     g.w1 = w1;
     g.w2 = w2;
@@ -210,7 +228,7 @@ __device__ inline void make_ghost_x(EdgeSh& g, int kind, double w1, double w2, d
     }
     if (kind == PD_EDGE_NEUMANN) {
         g.cIn = 1.0;
-        for (int k = threadIdx.x; k < len; k += blockDim.x) b[k] = XMUL(XMUL(XMUL(sign, 2.0), delta), slope[k]);
+        for (int k = tid; k < len; k += nth) b[k] = XMUL(XMUL(XMUL(sign, 2.0), delta), slope[k]);
         return;
     }
     if (fabs(w2) < 1e-300) {
@@ -219,10 +237,14 @@ __device__ inline void make_ghost_x(EdgeSh& g, int kind, double w1, double w2, d
     }
     g.cIn = 1.0;
     g.cEdge = XDIV(XMUL(XMUL(XMUL(-sign, 2.0), delta), w1), w2);
-    for (int k = threadIdx.x; k < len; k += blockDim.x) {
+    for (int k = tid; k < len; k += nth) {
         const double q = XADD(XMUL(w1, value[k]), XMUL(w2, slope[k]));
         b[k] = XDIV(XMUL(XMUL(XMUL(sign, 2.0), delta), q), w2);
     }
+}
+__device__ inline void make_ghost_x(EdgeSh& g, int kind, double w1, double w2, double delta, double sign,
+                                    int len, const double* value, const double* slope, double* b) {
+    make_ghost_t(g, kind, w1, w2, delta, sign, len, value, slope, b, (int)threadIdx.x, (int)blockDim.x);
 }
 
 // pinned_value  microsim.cpp:189-192

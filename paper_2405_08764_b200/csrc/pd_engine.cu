@@ -22,6 +22,7 @@
 #include "kernels_adi.cuh"
 #include "kernels_adi_fast.cuh"
 #include "kernels_exact.cuh"
+#include "kernels_exact_tile.cuh"
 #include "kernels_fast.cuh"
 #include "kernels_fast_big.cuh"
 #include "kernels_misc.cuh"
@@ -166,6 +167,9 @@ struct pd_engine {
             launch_big(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream);
         } else if (mode == PD_MODE_FAST) {
             launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream, srct);
+        } else if (const int tile = exact_tile_plan(prm); tile >= 0) {
+            // register-blocked EXACT step (kernels_exact_tile.cuh): same arithmetic, bit-identical
+            launch_exact_tile(tile, prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, fail, stream);
         } else {
             k_gaptooth_exact<<<prm.P, exact_threads(prm), exact_smem_bytes(prm), stream>>>(
                 prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail, nullptr, nullptr,

@@ -1,0 +1,86 @@
+"""Register-blocked EXACT step (csrc/kernels_exact_tile.cuh, k_exact_tile).
+
+The tile kernel replays the reference's arithmetic (explicit_sweep,
+microsim.cpp:292-332; integrate :509-552; gaptooth.cpp:110-194) on the
+lane-per-block mapping.  It must be bit-identical to
+
+* the restated oracle (reference + mixed term) on every tile shape, with and
+  without the mixed term, Neumann and (5-point) Robin patch edges, both
+  quadratures, k = 0 and k = 1, and
+* the shared-memory kernel it replaces (k_gaptooth_exact), which a child
+  process runs with PD_EXACT_TILE=0 on the same cases.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2405_08764_b200 import abi, configs
+from paper_2405_08764_b200.engine import Engine, Problem
+
+pytestmark = pytest.mark.gpu
+EXACT = abi.PD_MODE_EXACT
+
+ROBIN = dict(bc_type=abi.PD_BC_ROBIN, robin_w1=2.0, robin_w2=1.0)
+# name -> (config, overrides, macro steps)
+CASES = {
+    "7x7-5pt": ("c1_diffusion", dict(Nt=20), 5),
+    "7x7-5pt-robin-k1": ("c1_diffusion", dict(Nt=20, k=1, **ROBIN), 4),
+    "7x7-5pt-simpson": ("c1_diffusion", dict(Nt=20, quadrature=abi.PD_QUAD_SIMPSON), 4),
+    "8x8-5pt": ("c1_diffusion", dict(nx=7, ny=7, Nt=20), 4),
+    "9x9-5pt-periodic": ("c3_annulus", dict(Nt=20), 4),
+    "9x9-5pt-cdr": ("c2_cdr_tanh", dict(N_xi=23, N_eta=23, Nt=20), 4),
+    "16x16-5pt-robin": ("c1_diffusion", dict(nx=15, ny=15, Nt=20, **ROBIN), 3),
+    "7x7-mixed": ("c4_shear", dict(nx=6, ny=6, N_xi=9, N_eta=11, nt=20, Nt=5), 4),
+    "8x8-mixed": ("c4_shear", dict(nx=7, ny=7, N_xi=11, N_eta=9, nt=20, Nt=5), 4),
+    "8x8-5pt-robin": ("c1_diffusion", dict(nx=7, ny=7, Nt=20, **ROBIN), 4),
+    "9x9-mixed-k1": ("c4_shear", dict(nx=8, ny=8, N_xi=10, N_eta=9, nt=20, Nt=5, k=1), 3),
+    "16x16-mixed": ("c4_shear", dict(N_xi=33, N_eta=17, Nt=10), 4),
+    # 17x17 nodes is not a tile: the shared-memory kernel stays in place
+    "17x17-mixed-simpson": ("c4_shear", dict(nx=16, ny=16, N_xi=9, N_eta=9, nt=20, Nt=5,
+                                             quadrature=abi.PD_QUAD_SIMPSON), 3),
+}
+
+
+def run_case(name):
+    cfg, over, n = CASES[name]
+    d, _ = configs.load(cfg)
+    P = Problem(configs.copy_desc(d, **over))
+    U0 = P.initial_field()
+    bt = P.boundary_table(0.0, n)
+    E = Engine.from_problem(P, mode=EXACT)
+    assert E.mode == EXACT
+    U, st = E.run(U0, n, bnd=bt)
+    assert st.steps_done == n
+    return P, U0, bt, n, U
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_exact_tile_bit_identical_to_oracle(name, restated, gpu):
+    P, U0, bt, n, U = run_case(name)
+    st, Uo, _ = restated.run(P.engine_desc(), U0, n, bnd=bt)
+    assert st == abi.PD_OK
+    assert np.array_equal(U, Uo)
+
+
+def test_exact_tile_equals_shared_memory_kernel(tmp_path, gpu):
+    """PD_EXACT_TILE=0 (read once per process) keeps every EXACT step on
+    k_gaptooth_exact; both kernels must produce the same bits."""
+    out = tmp_path / "smem.npz"
+    code = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import test_gpu_exact_tile as t
+np.savez(%r, **{k: t.run_case(k)[4] for k in t.CASES})
+print("ok")
+""" % (str(ROOT), str(ROOT / "tests"), str(out))
+    env = dict(os.environ, PD_EXACT_TILE="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+    ref = np.load(out)
+    for name in CASES:
+        assert np.array_equal(run_case(name)[4], ref[name]), name
