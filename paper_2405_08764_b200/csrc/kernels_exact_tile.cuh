@@ -25,6 +25,13 @@
 
 namespace pdb200::dev {
 
+// resident warps per SM the mixed-term instantiations are compiled for (8: 216 registers,
+// no spills, config 4 9.01 ms per step; 10: 168 registers with 18 local accesses per
+// micro-step, 9.61 ms)
+#ifndef PD_XT_MIXED_BLOCKS
+#define PD_XT_MIXED_BLOCKS 8
+#endif
+
 template <int N1_, int N2_, int BI_, int BJ_, bool MIXED_>
 struct XTileCfg {
     static constexpr int N1 = N1_, N2 = N2_, BI = BI_, BJ = BJ_;
@@ -46,8 +53,22 @@ __device__ __forceinline__ double ghost_t(double cEdge, double u_inner, double u
     return XADD(XADD(u_inner, XMUL(cEdge, u_edge)), b);
 }
 
+// a where (role & MASK) == WANT, else b: a selp by construction (written as a
+// conditional, the compiler turned these lane-role selections into divergent
+// branches with a warp reconvergence each — 15 % of the step loop's samples)
+enum { ROLE_W = 1, ROLE_E = 2, ROLE_S = 4, ROLE_N = 8 };
+template <int MASK, int WANT>
+__device__ __forceinline__ double pick(int role, double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %3, %4;\n\tsetp.eq.s32 p, t, %5;\n\t"
+        "selp.f64 %0, %1, %2, p;\n\t}"
+        : "=d"(r)
+        : "d"(a), "d"(b), "r"(role), "n"(MASK), "n"(WANT));
+    return r;
+}
+
 template <class Cfg>
-__global__ void __launch_bounds__(32, Cfg::MIXED ? 10 : 12)
+__global__ void __launch_bounds__(32, Cfg::MIXED ? PD_XT_MIXED_BLOCKS : 12)
 k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
              const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
              const int* __restrict__ fail_flag, int nunits) {
@@ -73,6 +94,8 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
     const int bi = r % LI, bj = r / LI;
     const int i0 = bi * BI, j0 = bj * BJ;
     const bool isW = bi == 0, isE = bi == LI - 1, isS = bj == 0, isN = bj == LJ - 1;
+    int role = (isW ? ROLE_W : 0) | (isE ? ROLE_E : 0) | (isS ? ROLE_S : 0) | (isN ? ROLE_N : 0);
+    asm volatile("mov.b32 %0, %0;" : "+r"(role)); // one live register, not re-derived from the lane id per use
 
     // ---- build_stencil (gaptooth.cpp:74-104) ----------------------------------
     int pi = 0, pj = 0, ic = 0;
@@ -189,44 +212,65 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
         // (explicit_sweep, microsim.cpp:314-323; at_ext_x for the mixed term's
         // diagonal neighbours).  Every formula reads own nodes or halo entries
         // that are real nodes for this lane, never an entry written here.
-        // S / N ghosts of the columns a in [A0, A1] inside the patch
+        // S / N ghosts of the columns a in [A0, A1] inside the patch (the halo
+        // columns a = -1 / BI only where they are not past the W / E edge)
 #pragma unroll
         for (int a = A0; a <= A1; ++a) {
-            const bool inside = !(a == -1 && isW) && !(a == BI && isE);
+            constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
             const double gsv = ghost_t(cEs, E[a + 1][2], E[a + 1][1], gbs[a + 1]);
             const double gnv = ghost_t(cEn, E[a + 1][BJ - 1], E[a + 1][BJ], gbn[a + 1]);
-            if (isS && inside) E[a + 1][0] = gsv;
-            if (isN && inside) E[a + 1][BJ + 1] = gnv;
+            if (a == -1) {
+                E[a + 1][0] = pick<S_ | W_, S_>(role, gsv, E[a + 1][0]);
+                E[a + 1][BJ + 1] = pick<N_ | W_, N_>(role, gnv, E[a + 1][BJ + 1]);
+            } else if (a == BI) {
+                E[a + 1][0] = pick<S_ | E_, S_>(role, gsv, E[a + 1][0]);
+                E[a + 1][BJ + 1] = pick<N_ | E_, N_>(role, gnv, E[a + 1][BJ + 1]);
+            } else {
+                E[a + 1][0] = pick<S_, S_>(role, gsv, E[a + 1][0]);
+                E[a + 1][BJ + 1] = pick<N_, N_>(role, gnv, E[a + 1][BJ + 1]);
+            }
         }
         // W / E ghosts of the rows b in [B0, B1] inside the patch (one xi role per lane)
 #pragma unroll
         for (int b = B0; b <= B1; ++b) {
-            const bool inside = !(b == -1 && isS) && !(b == BJ && isN);
-            const double inner = isE ? E[BI - 1][b + 1] : E[2][b + 1];
-            const double edge = isE ? E[BI][b + 1] : E[1][b + 1];
+            constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
+            const double inner = pick<E_, E_>(role, E[BI - 1][b + 1], E[2][b + 1]);
+            const double edge = pick<E_, E_>(role, E[BI][b + 1], E[1][b + 1]);
             const double gv = ghost_t(cEx, inner, edge, gbx[b + 1]);
-            if (isW && inside) E[0][b + 1] = gv;
-            if (isE && inside) E[BI + 1][b + 1] = gv;
+            if (b == -1) {
+                E[0][b + 1] = pick<W_ | S_, W_>(role, gv, E[0][b + 1]);
+                E[BI + 1][b + 1] = pick<E_ | S_, E_>(role, gv, E[BI + 1][b + 1]);
+            } else if (b == BJ) {
+                E[0][b + 1] = pick<W_ | N_, W_>(role, gv, E[0][b + 1]);
+                E[BI + 1][b + 1] = pick<E_ | N_, E_>(role, gv, E[BI + 1][b + 1]);
+            } else {
+                E[0][b + 1] = pick<W_, W_>(role, gv, E[0][b + 1]);
+                E[BI + 1][b + 1] = pick<E_, E_>(role, gv, E[BI + 1][b + 1]);
+            }
         }
         if constexpr (MIXED) {
             // patch corners: the double ghost u(ii, jj) + ox + oy (at_ext_x),
-            // branch-free: computed by every lane, kept by the corner lanes
-            const bool xedge = isW || isE;
+            // computed by every lane, kept by the corner lanes
+            constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
             {
-                const double ue = isE ? E[BI][1] : E[1][1];
+                const double ue = pick<E_, E_>(role, E[BI][1], E[1][1]);
                 const double ox = XADD(XMUL(cEx, ue), gbx[1]);
-                const double oy = XADD(XMUL(cEs, ue), isE ? gbs[BI] : gbs[1]);
-                const double cv = XADD(XADD(isE ? E[BI - 1][2] : E[2][2], ox), oy);
-                if (isS && isE) E[BI + 1][0] = cv;
-                if (isS && xedge && !isE) E[0][0] = cv;
+                const double by = pick<E_, E_>(role, gbs[BI], gbs[1]);
+                const double ui = pick<E_, E_>(role, E[BI - 1][2], E[2][2]);
+                const double oy = XADD(XMUL(cEs, ue), by);
+                const double cv = XADD(XADD(ui, ox), oy);
+                E[BI + 1][0] = pick<S_ | E_, S_ | E_>(role, cv, E[BI + 1][0]);
+                E[0][0] = pick<S_ | W_, S_ | W_>(role, cv, E[0][0]);
             }
             {
-                const double ue = isE ? E[BI][BJ] : E[1][BJ];
+                const double ue = pick<E_, E_>(role, E[BI][BJ], E[1][BJ]);
                 const double ox = XADD(XMUL(cEx, ue), gbx[BJ]);
-                const double oy = XADD(XMUL(cEn, ue), isE ? gbn[BI] : gbn[1]);
-                const double cv = XADD(XADD(isE ? E[BI - 1][BJ - 1] : E[2][BJ - 1], ox), oy);
-                if (isN && isE) E[BI + 1][BJ + 1] = cv;
-                if (isN && xedge && !isE) E[0][BJ + 1] = cv;
+                const double by = pick<E_, E_>(role, gbn[BI], gbn[1]);
+                const double ui = pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]);
+                const double oy = XADD(XMUL(cEn, ue), by);
+                const double cv = XADD(XADD(ui, ox), oy);
+                E[BI + 1][BJ + 1] = pick<N_ | E_, N_ | E_>(role, cv, E[BI + 1][BJ + 1]);
+                E[0][BJ + 1] = pick<N_ | W_, N_ | W_>(role, cv, E[0][BJ + 1]);
             }
         }
         double nu[BI][BJ];
