@@ -373,7 +373,8 @@ def roofline(eng, desc, kms, mixed, config_name):
     bytes_launch = P * (N * 8 * ncoef + 16)
     t_fp = flops_launch / (p64 * 1e12)
     t_bw = bytes_launch / (bw * 1e9)
-    traffic, traffic_src = load_traffic(config_name)
+    # the ncu summary is per kernel: EXACT-family launches have their own entry
+    traffic, traffic_src = load_traffic(config_name if eng.mode == abi.PD_MODE_FAST else config_name + "_exact")
     if t_fp >= t_bw:
         roof = {"bound": "fp64", "achieved": flops_launch / (kms * 1e-3) / 1e12, "peak": p64, "unit": "TFLOP/s"}
     else:
@@ -381,7 +382,8 @@ def roofline(eng, desc, kms, mixed, config_name):
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = traffic
     roof.update({
-        "kernel": "k_fast (fused gap-tooth substep)" if eng.mode == abi.PD_MODE_FAST else "k_gaptooth_exact",
+        "kernel": ("k_fast (fused gap-tooth substep)" if eng.mode == abi.PD_MODE_FAST
+                   else "k_exact_tile (EXACT, register-blocked)" if eng.exact_tile else "k_gaptooth_exact"),
         "kernel_ms": kms, "flops_per_update": fpu, "algorithmic_flops_per_launch": flops_launch,
         "algorithmic_bytes_per_launch": bytes_launch,
         "peak_source": f"FP64 DFMA microbenchmark measured in this run at {ghz:.3f} GHz; HBM {bw} GB/s from {bw_src}",

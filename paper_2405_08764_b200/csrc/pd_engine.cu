@@ -560,6 +560,7 @@ pd_status pd_engine_create(const pd_engine_desc* desc, pd_engine** out) {
 void pd_engine_destroy(pd_engine* e) { delete e; }
 
 int32_t pd_engine_mode(const pd_engine* e) { return e ? e->mode : -1; }
+int32_t pd_engine_exact_tile(const pd_engine* e) { return e ? (exact_tile_plan(e->prm) >= 0 ? 1 : 0) : -1; }
 int32_t pd_engine_mixed(const pd_engine* e) { return e ? e->prm.mixed : -1; }
 int64_t pd_engine_launch_count(const pd_engine* e) { return e ? e->launches : -1; }
 

@@ -56,6 +56,8 @@ def lib() -> C.CDLL:
     L.pd_engine_destroy.argtypes = [vp]
     L.pd_engine_mode.argtypes = [vp]
     L.pd_engine_mode.restype = C.c_int32
+    L.pd_engine_exact_tile.argtypes = [vp]
+    L.pd_engine_exact_tile.restype = C.c_int32
     L.pd_engine_tables.argtypes = [vp, _ip, _ip]
     L.pd_engine_device_bytes.argtypes = [vp]
     L.pd_engine_device_bytes.restype = C.c_size_t
@@ -310,6 +312,11 @@ class Engine:
     @property
     def mode(self) -> int:
         return lib().pd_engine_mode(self.h)
+
+    @property
+    def exact_tile(self) -> bool:
+        """EXACT steps of this engine run on the register-blocked tile kernel (k_exact_tile)."""
+        return lib().pd_engine_exact_tile(self.h) == 1
 
     @property
     def device_bytes(self) -> int:

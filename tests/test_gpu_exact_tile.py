@@ -53,6 +53,8 @@ def run_case(name):
     bt = P.boundary_table(0.0, n)
     E = Engine.from_problem(P, mode=EXACT)
     assert E.mode == EXACT
+    # the tile kernel is the one that runs (except in the PD_EXACT_TILE=0 child and on 17x17 nodes)
+    assert E.exact_tile == (os.environ.get("PD_EXACT_TILE") != "0" and not name.startswith("17x17"))
     U, st = E.run(U0, n, bnd=bt)
     assert st.steps_done == n
     return P, U0, bt, n, U
