@@ -157,6 +157,10 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
     const double* gbx = &s_gb[gs][ex][j0];
     const double* gbs = &s_gb[gs][PD_EDGE_S][i0];
     const double* gbn = &s_gb[gs][PD_EDGE_N][i0];
+    // LJ >= 2: a lane is on at most one eta edge too, and S / N share one ghost computation
+    constexpr bool MERGE_ETA = LJ >= 2;
+    const double cEy = isN ? cEn : cEs;
+    const double* gby = isN ? gbn : gbs;
 
     // ---- coefficients of this lane's nodes into registers --------------------
     double co[PD_NCOEF][BI][BJ];
@@ -225,8 +229,15 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
 #pragma unroll
         for (int a = A0; a <= A1; ++a) {
             constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
-            const double gsv = ghost_t(cEs, E[a + 1][2], E[a + 1][1], gbs[a + 1]);
-            const double gnv = ghost_t(cEn, E[a + 1][BJ - 1], E[a + 1][BJ], gbn[a + 1]);
+            double gsv, gnv;
+            if constexpr (MERGE_ETA) {
+                const double inner = pick<N_, N_>(role, E[a + 1][BJ - 1], E[a + 1][2]);
+                const double edge = pick<N_, N_>(role, E[a + 1][BJ], E[a + 1][1]);
+                gsv = gnv = ghost_t(cEy, inner, edge, gby[a + 1]);
+            } else {
+                gsv = ghost_t(cEs, E[a + 1][2], E[a + 1][1], gbs[a + 1]);
+                gnv = ghost_t(cEn, E[a + 1][BJ - 1], E[a + 1][BJ], gbn[a + 1]);
+            }
             if (a == -1) {
                 E[a + 1][0] = pick<S_ | W_, S_>(role, gsv, E[a + 1][0]);
                 E[a + 1][BJ + 1] = pick<N_ | W_, N_>(role, gnv, E[a + 1][BJ + 1]);
@@ -260,25 +271,41 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
             // patch corners: the double ghost u(ii, jj) + ox + oy (at_ext_x),
             // computed by every lane, kept by the corner lanes
             constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
-            {
-                const double ue = pick<E_, E_>(role, E[BI][1], E[1][1]);
-                const double ox = XADD(XMUL(cEx, ue), gbx[1]);
-                const double by = pick<E_, E_>(role, gbs[BI], gbs[1]);
-                const double ui = pick<E_, E_>(role, E[BI - 1][2], E[2][2]);
-                const double oy = XADD(XMUL(cEs, ue), by);
+            if constexpr (MERGE_ETA) { // at most one corner per lane: one computation
+                const double ue = pick<N_, N_>(role, pick<E_, E_>(role, E[BI][BJ], E[1][BJ]),
+                                               pick<E_, E_>(role, E[BI][1], E[1][1]));
+                const double ui = pick<N_, N_>(role, pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]),
+                                               pick<E_, E_>(role, E[BI - 1][2], E[2][2]));
+                const double bxc = pick<N_, N_>(role, gbx[BJ], gbx[1]);
+                const double byc = pick<E_, E_>(role, gby[BI], gby[1]);
+                const double ox = XADD(XMUL(cEx, ue), bxc);
+                const double oy = XADD(XMUL(cEy, ue), byc);
                 const double cv = XADD(XADD(ui, ox), oy);
                 E[BI + 1][0] = pick<S_ | E_, S_ | E_>(role, cv, E[BI + 1][0]);
                 E[0][0] = pick<S_ | W_, S_ | W_>(role, cv, E[0][0]);
-            }
-            {
-                const double ue = pick<E_, E_>(role, E[BI][BJ], E[1][BJ]);
-                const double ox = XADD(XMUL(cEx, ue), gbx[BJ]);
-                const double by = pick<E_, E_>(role, gbn[BI], gbn[1]);
-                const double ui = pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]);
-                const double oy = XADD(XMUL(cEn, ue), by);
-                const double cv = XADD(XADD(ui, ox), oy);
                 E[BI + 1][BJ + 1] = pick<N_ | E_, N_ | E_>(role, cv, E[BI + 1][BJ + 1]);
                 E[0][BJ + 1] = pick<N_ | W_, N_ | W_>(role, cv, E[0][BJ + 1]);
+            } else {
+                {
+                    const double ue = pick<E_, E_>(role, E[BI][1], E[1][1]);
+                    const double ox = XADD(XMUL(cEx, ue), gbx[1]);
+                    const double by = pick<E_, E_>(role, gbs[BI], gbs[1]);
+                    const double ui = pick<E_, E_>(role, E[BI - 1][2], E[2][2]);
+                    const double oy = XADD(XMUL(cEs, ue), by);
+                    const double cv = XADD(XADD(ui, ox), oy);
+                    E[BI + 1][0] = pick<S_ | E_, S_ | E_>(role, cv, E[BI + 1][0]);
+                    E[0][0] = pick<S_ | W_, S_ | W_>(role, cv, E[0][0]);
+                }
+                {
+                    const double ue = pick<E_, E_>(role, E[BI][BJ], E[1][BJ]);
+                    const double ox = XADD(XMUL(cEx, ue), gbx[BJ]);
+                    const double by = pick<E_, E_>(role, gbn[BI], gbn[1]);
+                    const double ui = pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]);
+                    const double oy = XADD(XMUL(cEn, ue), by);
+                    const double cv = XADD(XADD(ui, ox), oy);
+                    E[BI + 1][BJ + 1] = pick<N_ | E_, N_ | E_>(role, cv, E[BI + 1][BJ + 1]);
+                    E[0][BJ + 1] = pick<N_ | W_, N_ | W_>(role, cv, E[0][BJ + 1]);
+                }
             }
         }
         double nu[BI][BJ];
