@@ -14,8 +14,8 @@
 // every micro-step, with one CTA barrier per step.
 //
 // Scope: the explicit micro-solver, zero source, Neumann or (unpinned) Robin
-// patch edges, the exact-fit tiles 7x7, 8x8, 9x9 and 16x16, with or without the
-// mixed term.  Everything else stays on k_gaptooth_exact (exact_tile_plan).
+// patch edges, the exact-fit tiles 7x7, 8x8, 9x9, 16x16 (one warp per unit) and
+// 32x32 (one four-warp CTA per patch, k_exact_big), with or without the mixed term.  Everything else stays on k_gaptooth_exact (exact_tile_plan).
 #pragma once
 
 #include <cstdlib>
@@ -72,6 +72,137 @@ __device__ __forceinline__ double pick(int role, double a, double b) {
         : "=d"(r)
         : "d"(a), "d"(b), "r"(role), "n"(MASK), "n"(WANT));
     return r;
+}
+
+// One explicit sweep of a lane's BI x BJ block, halo entries of E already
+// filled from the neighbouring lanes: ghost values on the patch edges, then
+// the reference's update of every own node (explicit_sweep, microsim.cpp:304-331,
+// + the mixed term after A*uxx).  Shared by the one-warp tiles and the 32x32 CTA tile.
+template <int BI, int BJ, bool MIXED, bool MERGE_ETA>
+__device__ __forceinline__ void xt_sweep(double (&E)[BI + 2][BJ + 2], const double (&co)[PD_NCOEF][BI][BJ], int role,
+                                         double cEx, double cEs, double cEn, double cEy, const double* gbx,
+                                         const double* gbs, const double* gbn, const double* gby, double idx2,
+                                         double idy2, double idx, double idy, double ixy, double dt) {
+    constexpr int B0 = MIXED ? -1 : 0, B1 = MIXED ? BJ : BJ - 1; // rows / columns whose halo is needed
+    constexpr int A0 = MIXED ? -1 : 0, A1 = MIXED ? BI : BI - 1;
+    // Patch edges: replace what the shuffles brought by the ghost values
+    // (explicit_sweep, microsim.cpp:314-323; at_ext_x for the mixed term's
+    // diagonal neighbours).  Every formula reads own nodes or halo entries
+    // that are real nodes for this lane, never an entry written here.
+    // S / N ghosts of the columns a in [A0, A1] inside the patch (the halo
+    // columns a = -1 / BI only where they are not past the W / E edge)
+#pragma unroll
+    for (int a = A0; a <= A1; ++a) {
+        constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
+        double gsv, gnv;
+        if constexpr (MERGE_ETA) {
+            const double inner = pick<N_, N_>(role, E[a + 1][BJ - 1], E[a + 1][2]);
+            const double edge = pick<N_, N_>(role, E[a + 1][BJ], E[a + 1][1]);
+            gsv = gnv = ghost_t(cEy, inner, edge, gby[a + 1]);
+        } else {
+            gsv = ghost_t(cEs, E[a + 1][2], E[a + 1][1], gbs[a + 1]);
+            gnv = ghost_t(cEn, E[a + 1][BJ - 1], E[a + 1][BJ], gbn[a + 1]);
+        }
+        if (a == -1) {
+            E[a + 1][0] = pick<S_ | W_, S_>(role, gsv, E[a + 1][0]);
+            E[a + 1][BJ + 1] = pick<N_ | W_, N_>(role, gnv, E[a + 1][BJ + 1]);
+        } else if (a == BI) {
+            E[a + 1][0] = pick<S_ | E_, S_>(role, gsv, E[a + 1][0]);
+            E[a + 1][BJ + 1] = pick<N_ | E_, N_>(role, gnv, E[a + 1][BJ + 1]);
+        } else {
+            E[a + 1][0] = pick<S_, S_>(role, gsv, E[a + 1][0]);
+            E[a + 1][BJ + 1] = pick<N_, N_>(role, gnv, E[a + 1][BJ + 1]);
+        }
+    }
+    // W / E ghosts of the rows b in [B0, B1] inside the patch (one xi role per lane)
+#pragma unroll
+    for (int b = B0; b <= B1; ++b) {
+        constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
+        const double inner = pick<E_, E_>(role, E[BI - 1][b + 1], E[2][b + 1]);
+        const double edge = pick<E_, E_>(role, E[BI][b + 1], E[1][b + 1]);
+        const double gv = ghost_t(cEx, inner, edge, gbx[b + 1]);
+        if (b == -1) {
+            E[0][b + 1] = pick<W_ | S_, W_>(role, gv, E[0][b + 1]);
+            E[BI + 1][b + 1] = pick<E_ | S_, E_>(role, gv, E[BI + 1][b + 1]);
+        } else if (b == BJ) {
+            E[0][b + 1] = pick<W_ | N_, W_>(role, gv, E[0][b + 1]);
+            E[BI + 1][b + 1] = pick<E_ | N_, E_>(role, gv, E[BI + 1][b + 1]);
+        } else {
+            E[0][b + 1] = pick<W_, W_>(role, gv, E[0][b + 1]);
+            E[BI + 1][b + 1] = pick<E_, E_>(role, gv, E[BI + 1][b + 1]);
+        }
+    }
+    if constexpr (MIXED) {
+        // patch corners: the double ghost u(ii, jj) + ox + oy (at_ext_x),
+        // computed by every lane, kept by the corner lanes
+        constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
+        if constexpr (MERGE_ETA) { // at most one corner per lane: one computation
+            const double ue = pick<N_, N_>(role, pick<E_, E_>(role, E[BI][BJ], E[1][BJ]),
+                                           pick<E_, E_>(role, E[BI][1], E[1][1]));
+            const double ui = pick<N_, N_>(role, pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]),
+                                           pick<E_, E_>(role, E[BI - 1][2], E[2][2]));
+            const double bxc = pick<N_, N_>(role, gbx[BJ], gbx[1]);
+            const double byc = pick<E_, E_>(role, gby[BI], gby[1]);
+            const double ox = XADD(XMUL(cEx, ue), bxc);
+            const double oy = XADD(XMUL(cEy, ue), byc);
+            const double cv = XADD(XADD(ui, ox), oy);
+            E[BI + 1][0] = pick<S_ | E_, S_ | E_>(role, cv, E[BI + 1][0]);
+            E[0][0] = pick<S_ | W_, S_ | W_>(role, cv, E[0][0]);
+            E[BI + 1][BJ + 1] = pick<N_ | E_, N_ | E_>(role, cv, E[BI + 1][BJ + 1]);
+            E[0][BJ + 1] = pick<N_ | W_, N_ | W_>(role, cv, E[0][BJ + 1]);
+        } else {
+            {
+                const double ue = pick<E_, E_>(role, E[BI][1], E[1][1]);
+                const double ox = XADD(XMUL(cEx, ue), gbx[1]);
+                const double by = pick<E_, E_>(role, gbs[BI], gbs[1]);
+                const double ui = pick<E_, E_>(role, E[BI - 1][2], E[2][2]);
+                const double oy = XADD(XMUL(cEs, ue), by);
+                const double cv = XADD(XADD(ui, ox), oy);
+                E[BI + 1][0] = pick<S_ | E_, S_ | E_>(role, cv, E[BI + 1][0]);
+                E[0][0] = pick<S_ | W_, S_ | W_>(role, cv, E[0][0]);
+            }
+            {
+                const double ue = pick<E_, E_>(role, E[BI][BJ], E[1][BJ]);
+                const double ox = XADD(XMUL(cEx, ue), gbx[BJ]);
+                const double by = pick<E_, E_>(role, gbn[BI], gbn[1]);
+                const double ui = pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]);
+                const double oy = XADD(XMUL(cEn, ue), by);
+                const double cv = XADD(XADD(ui, ox), oy);
+                E[BI + 1][BJ + 1] = pick<N_ | E_, N_ | E_>(role, cv, E[BI + 1][BJ + 1]);
+                E[0][BJ + 1] = pick<N_ | W_, N_ | W_>(role, cv, E[0][BJ + 1]);
+            }
+        }
+    }
+    double nu[BI][BJ];
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+            const double uc = E[ii + 1][jj + 1];
+            const double uW = E[ii][jj + 1], uE = E[ii + 2][jj + 1];
+            const double uS = E[ii + 1][jj], uN = E[ii + 1][jj + 2];
+            const double uc2 = XMUL(2.0, uc);
+            const double uxx = XMUL(XADD(XSUB(uW, uc2), uE), idx2);
+            const double uyy = XMUL(XADD(XSUB(uS, uc2), uN), idy2);
+            const double ux = XMUL(XSUB(uE, uW), idx);
+            const double uy = XMUL(XSUB(uN, uS), idy);
+            double s = XMUL(co[PD_COEF_A][ii][jj], uxx);
+            if constexpr (MIXED) {
+                const double nE = E[ii + 2][jj + 2], sE = E[ii + 2][jj], nW = E[ii][jj + 2], sW = E[ii][jj];
+                const double uxy = XMUL(XADD(XSUB(XSUB(nE, sE), nW), sW), ixy);
+                s = XADD(s, XMUL(co[PD_COEF_B][ii][jj], uxy));
+            }
+            s = XADD(s, XMUL(co[PD_COEF_C][ii][jj], uyy));
+            s = XSUB(s, XMUL(co[PD_COEF_VX][ii][jj], ux));
+            s = XSUB(s, XMUL(co[PD_COEF_VY][ii][jj], uy));
+            s = XSUB(s, XMUL(co[PD_COEF_W][ii][jj], uc));
+            s = XADD(s, 0.0); // + G with the zero source (microsim.cpp:329)
+            nu[ii][jj] = XADD(uc, XMUL(dt, s));
+        }
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = nu[ii][jj];
 }
 
 template <class Cfg>
@@ -220,124 +351,8 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
             E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
             E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
         }
-        // Patch edges: replace what the shuffles brought by the ghost values
-        // (explicit_sweep, microsim.cpp:314-323; at_ext_x for the mixed term's
-        // diagonal neighbours).  Every formula reads own nodes or halo entries
-        // that are real nodes for this lane, never an entry written here.
-        // S / N ghosts of the columns a in [A0, A1] inside the patch (the halo
-        // columns a = -1 / BI only where they are not past the W / E edge)
-#pragma unroll
-        for (int a = A0; a <= A1; ++a) {
-            constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
-            double gsv, gnv;
-            if constexpr (MERGE_ETA) {
-                const double inner = pick<N_, N_>(role, E[a + 1][BJ - 1], E[a + 1][2]);
-                const double edge = pick<N_, N_>(role, E[a + 1][BJ], E[a + 1][1]);
-                gsv = gnv = ghost_t(cEy, inner, edge, gby[a + 1]);
-            } else {
-                gsv = ghost_t(cEs, E[a + 1][2], E[a + 1][1], gbs[a + 1]);
-                gnv = ghost_t(cEn, E[a + 1][BJ - 1], E[a + 1][BJ], gbn[a + 1]);
-            }
-            if (a == -1) {
-                E[a + 1][0] = pick<S_ | W_, S_>(role, gsv, E[a + 1][0]);
-                E[a + 1][BJ + 1] = pick<N_ | W_, N_>(role, gnv, E[a + 1][BJ + 1]);
-            } else if (a == BI) {
-                E[a + 1][0] = pick<S_ | E_, S_>(role, gsv, E[a + 1][0]);
-                E[a + 1][BJ + 1] = pick<N_ | E_, N_>(role, gnv, E[a + 1][BJ + 1]);
-            } else {
-                E[a + 1][0] = pick<S_, S_>(role, gsv, E[a + 1][0]);
-                E[a + 1][BJ + 1] = pick<N_, N_>(role, gnv, E[a + 1][BJ + 1]);
-            }
-        }
-        // W / E ghosts of the rows b in [B0, B1] inside the patch (one xi role per lane)
-#pragma unroll
-        for (int b = B0; b <= B1; ++b) {
-            constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
-            const double inner = pick<E_, E_>(role, E[BI - 1][b + 1], E[2][b + 1]);
-            const double edge = pick<E_, E_>(role, E[BI][b + 1], E[1][b + 1]);
-            const double gv = ghost_t(cEx, inner, edge, gbx[b + 1]);
-            if (b == -1) {
-                E[0][b + 1] = pick<W_ | S_, W_>(role, gv, E[0][b + 1]);
-                E[BI + 1][b + 1] = pick<E_ | S_, E_>(role, gv, E[BI + 1][b + 1]);
-            } else if (b == BJ) {
-                E[0][b + 1] = pick<W_ | N_, W_>(role, gv, E[0][b + 1]);
-                E[BI + 1][b + 1] = pick<E_ | N_, E_>(role, gv, E[BI + 1][b + 1]);
-            } else {
-                E[0][b + 1] = pick<W_, W_>(role, gv, E[0][b + 1]);
-                E[BI + 1][b + 1] = pick<E_, E_>(role, gv, E[BI + 1][b + 1]);
-            }
-        }
-        if constexpr (MIXED) {
-            // patch corners: the double ghost u(ii, jj) + ox + oy (at_ext_x),
-            // computed by every lane, kept by the corner lanes
-            constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
-            if constexpr (MERGE_ETA) { // at most one corner per lane: one computation
-                const double ue = pick<N_, N_>(role, pick<E_, E_>(role, E[BI][BJ], E[1][BJ]),
-                                               pick<E_, E_>(role, E[BI][1], E[1][1]));
-                const double ui = pick<N_, N_>(role, pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]),
-                                               pick<E_, E_>(role, E[BI - 1][2], E[2][2]));
-                const double bxc = pick<N_, N_>(role, gbx[BJ], gbx[1]);
-                const double byc = pick<E_, E_>(role, gby[BI], gby[1]);
-                const double ox = XADD(XMUL(cEx, ue), bxc);
-                const double oy = XADD(XMUL(cEy, ue), byc);
-                const double cv = XADD(XADD(ui, ox), oy);
-                E[BI + 1][0] = pick<S_ | E_, S_ | E_>(role, cv, E[BI + 1][0]);
-                E[0][0] = pick<S_ | W_, S_ | W_>(role, cv, E[0][0]);
-                E[BI + 1][BJ + 1] = pick<N_ | E_, N_ | E_>(role, cv, E[BI + 1][BJ + 1]);
-                E[0][BJ + 1] = pick<N_ | W_, N_ | W_>(role, cv, E[0][BJ + 1]);
-            } else {
-                {
-                    const double ue = pick<E_, E_>(role, E[BI][1], E[1][1]);
-                    const double ox = XADD(XMUL(cEx, ue), gbx[1]);
-                    const double by = pick<E_, E_>(role, gbs[BI], gbs[1]);
-                    const double ui = pick<E_, E_>(role, E[BI - 1][2], E[2][2]);
-                    const double oy = XADD(XMUL(cEs, ue), by);
-                    const double cv = XADD(XADD(ui, ox), oy);
-                    E[BI + 1][0] = pick<S_ | E_, S_ | E_>(role, cv, E[BI + 1][0]);
-                    E[0][0] = pick<S_ | W_, S_ | W_>(role, cv, E[0][0]);
-                }
-                {
-                    const double ue = pick<E_, E_>(role, E[BI][BJ], E[1][BJ]);
-                    const double ox = XADD(XMUL(cEx, ue), gbx[BJ]);
-                    const double by = pick<E_, E_>(role, gbn[BI], gbn[1]);
-                    const double ui = pick<E_, E_>(role, E[BI - 1][BJ - 1], E[2][BJ - 1]);
-                    const double oy = XADD(XMUL(cEn, ue), by);
-                    const double cv = XADD(XADD(ui, ox), oy);
-                    E[BI + 1][BJ + 1] = pick<N_ | E_, N_ | E_>(role, cv, E[BI + 1][BJ + 1]);
-                    E[0][BJ + 1] = pick<N_ | W_, N_ | W_>(role, cv, E[0][BJ + 1]);
-                }
-            }
-        }
-        double nu[BI][BJ];
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) {
-                const double uc = E[ii + 1][jj + 1];
-                const double uW = E[ii][jj + 1], uE = E[ii + 2][jj + 1];
-                const double uS = E[ii + 1][jj], uN = E[ii + 1][jj + 2];
-                const double uc2 = XMUL(2.0, uc);
-                const double uxx = XMUL(XADD(XSUB(uW, uc2), uE), idx2);
-                const double uyy = XMUL(XADD(XSUB(uS, uc2), uN), idy2);
-                const double ux = XMUL(XSUB(uE, uW), idx);
-                const double uy = XMUL(XSUB(uN, uS), idy);
-                double s = XMUL(co[PD_COEF_A][ii][jj], uxx);
-                if constexpr (MIXED) {
-                    const double nE = E[ii + 2][jj + 2], sE = E[ii + 2][jj], nW = E[ii][jj + 2], sW = E[ii][jj];
-                    const double uxy = XMUL(XADD(XSUB(XSUB(nE, sE), nW), sW), ixy);
-                    s = XADD(s, XMUL(co[PD_COEF_B][ii][jj], uxy));
-                }
-                s = XADD(s, XMUL(co[PD_COEF_C][ii][jj], uyy));
-                s = XSUB(s, XMUL(co[PD_COEF_VX][ii][jj], ux));
-                s = XSUB(s, XMUL(co[PD_COEF_VY][ii][jj], uy));
-                s = XSUB(s, XMUL(co[PD_COEF_W][ii][jj], uc));
-                s = XADD(s, 0.0); // + G with the zero source (microsim.cpp:329)
-                nu[ii][jj] = XADD(uc, XMUL(dt, s));
-            }
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-            for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = nu[ii][jj];
+        xt_sweep<BI, BJ, MIXED, MERGE_ETA>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2, idx, idy,
+                                          ixy, dt);
     }
 
     // ---- restrict_average in the reference order (gaptooth.cpp:170-194) ------
@@ -359,6 +374,180 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
     if (valid && r == 0) {
         double avg = 0.0;
         for (int i = 0; i <= nx; ++i) avg = XADD(avg, XMUL(quad_w(i, nx, p.quad), s_row[gs][i]));
+        const size_t node = (size_t)pi * p.NF2 + pj;
+        if (out_mode == OUT_FIELD) {
+            out[node] = avg;
+            halo_store(p, node, avg);
+        } else if (out_mode == OUT_PROJECTIVE) {
+            const double U = F[node];
+            const double Fd = XDIV(XSUB(avg, U), p.tau); // estimate_derivative  cpi.cpp:54
+            const double w = XADD(U, XMUL(p.dt_macro, Fd)); // cpi.cpp:74 with k = 0
+            out[node] = w;
+            halo_store(p, node, w);
+        } else {
+            out[patch] = avg;
+        }
+    }
+}
+
+
+// ---- 32x32 patches: one CTA of four warps per patch ----------------------------
+// The same 2x4 node blocks (16 lanes along xi, two lane rows per warp, warp w
+// holds micro rows 8w .. 8w+7).  xi neighbours and the lane rows of one warp
+// exchange by shuffles as above; the rows that face another warp are published
+// to shared memory (double-buffered by step parity, one CTA barrier per
+// micro-step) and read back by the neighbouring warp.  Arithmetic, ghost rules
+// and the pro/epilogue are those of k_exact_tile / k_gaptooth_exact.
+constexpr int kXBigWarps = 4;
+template <bool MIXED>
+__global__ void __launch_bounds__(32 * kXBigWarps, MIXED ? 2 : 3)
+k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
+            const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
+            const int* __restrict__ fail_flag) {
+    constexpr int BI = 2, BJ = 4, LI = 16, N1 = 32, N2 = 32, N = N1 * N2, L = 32, NT = 32 * kXBigWarps;
+    constexpr int nx = N1 - 1, ny = N2 - 1;
+    __shared__ double s_st[9];
+    __shared__ double s_slope[4][L], s_val[4][L];
+    __shared__ double s_gb[4][L + 2];
+    __shared__ double s_u[N];
+    __shared__ double s_row[N1];
+    // rows facing another warp: [parity][warp][0: lowest row (lane row 0, jj = 0) | 1: highest row][column + 1]
+    __shared__ double s_ex[2][kXBigWarps][2][N1 + 2];
+    if (fail_flag && *fail_flag) return;
+    const int patch = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int bi = lane & (LI - 1), bjl = lane >> 4, bj = warp * 2 + bjl;
+    const int i0 = bi * BI, j0 = bj * BJ;
+    const bool isW = bi == 0, isE = bi == LI - 1, isS = bj == 0, isN = bj == 2 * kXBigWarps - 1;
+    int role = (isW ? ROLE_W : 0) | (isE ? ROLE_E : 0) | (isS ? ROLE_S : 0) | (isN ? ROLE_N : 0);
+    asm volatile("mov.b32 %0, %0;" : "+r"(role));
+    int upper = bjl; // this lane's row block is the warp's upper one: its N side faces the next warp
+    asm volatile("mov.b32 %0, %0;" : "+r"(upper));
+
+    // ---- build_stencil (gaptooth.cpp:74-104) ----------------------------------
+    const int pi = pij[2 * patch], pj = pij[2 * patch + 1];
+    int ic = pi;
+    if (p.periodic) ic = ((pi % p.Nxi) + p.Nxi) % p.Nxi;
+    if (tid < 9) {
+        const int dp = tid / 3 - 1, dq = tid % 3 - 1;
+        const int ip = p.periodic ? ((ic + dp) % p.Nxi + p.Nxi) % p.Nxi : pi + dp;
+        s_st[tid] = F[(size_t)ip * p.NF2 + pj + dq];
+    }
+    __syncthreads();
+    const double* v = s_st;
+    const double xi_c = XADD(p.a, XMUL(p.Dxi, (double)ic));
+    const double eta_c = XADD(p.c, XMUL(p.Deta, (double)pj));
+
+    // ---- edge profiles and ghost offsets (gaptooth.cpp:110-152, microsim.cpp:152-186)
+    const bool robin = p.bc_type == PD_BC_ROBIN;
+    edge_profiles_t(v, xi_c, eta_c, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny, L, true, robin, &s_slope[0][0],
+                    &s_val[0][0], tid, NT);
+    __syncthreads();
+    double cedge[4];
+    {
+        const int kind = robin ? PD_EDGE_ROBIN : PD_EDGE_NEUMANN;
+        EdgeSh eg;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdxi, +1.0, N2, s_val[PD_EDGE_E], s_slope[PD_EDGE_E], &s_gb[PD_EDGE_E][1],
+                     tid, NT);
+        cedge[PD_EDGE_E] = eg.cEdge;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdxi, -1.0, N2, s_val[PD_EDGE_W], s_slope[PD_EDGE_W], &s_gb[PD_EDGE_W][1],
+                     tid, NT);
+        cedge[PD_EDGE_W] = eg.cEdge;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdeta, +1.0, N1, s_val[PD_EDGE_N], s_slope[PD_EDGE_N], &s_gb[PD_EDGE_N][1],
+                     tid, NT);
+        cedge[PD_EDGE_N] = eg.cEdge;
+        make_ghost_t(eg, kind, p.w1, p.w2, p.mdeta, -1.0, N1, s_val[PD_EDGE_S], s_slope[PD_EDGE_S], &s_gb[PD_EDGE_S][1],
+                     tid, NT);
+        cedge[PD_EDGE_S] = eg.cEdge;
+    }
+    __syncthreads();
+    const double cEx = isE ? cedge[PD_EDGE_E] : cedge[PD_EDGE_W], cEs = cedge[PD_EDGE_S], cEn = cedge[PD_EDGE_N];
+    const double cEy = isN ? cEn : cEs;
+    const double* gbx = &s_gb[isE ? PD_EDGE_E : PD_EDGE_W][j0];
+    const double* gbs = &s_gb[PD_EDGE_S][i0];
+    const double* gbn = &s_gb[PD_EDGE_N][i0];
+    const double* gby = isN ? gbn : gbs;
+
+    // ---- coefficients of this lane's nodes into registers --------------------
+    double co[PD_NCOEF][BI][BJ];
+    {
+        const int set = cset ? cset[patch] : patch;
+        const double* cf = coeffs + (size_t)set * PD_NCOEF * N;
+#pragma unroll
+        for (int c = 0; c < PD_NCOEF; ++c) {
+            if (!MIXED && c == PD_COEF_B) continue;
+#pragma unroll
+            for (int ii = 0; ii < BI; ++ii) {
+                const double* row = cf + (size_t)c * N + (i0 + ii) * N2 + j0;
+#pragma unroll
+                for (int jj = 0; jj < BJ; jj += 2) {
+                    const double2 t = __ldg(reinterpret_cast<const double2*>(row + jj));
+                    co[c][ii][jj] = t.x;
+                    co[c][ii][jj + 1] = t.y;
+                }
+            }
+        }
+    }
+
+    // ---- StencilPoly::center + lift (gaptooth.cpp:63-72, 154-168) ------------
+    double E[BI + 2][BJ + 2];
+    {
+        const LiftConsts lc = lift_consts_x(v, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny);
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = lift_node_x(lc, p.h_xi, p.h_eta, i0 + ii, j0 + jj);
+    }
+
+    // ---- K explicit sweeps (microsim.cpp:292-332, 535-550) -------------------
+    const double idx2 = XDIV(1.0, XMUL(p.mdxi, p.mdxi)), idy2 = XDIV(1.0, XMUL(p.mdeta, p.mdeta));
+    const double idx = XDIV(1.0, XMUL(2.0, p.mdxi)), idy = XDIV(1.0, XMUL(2.0, p.mdeta));
+    const double ixy = XDIV(1.0, XMUL(XMUL(4.0, p.mdxi), p.mdeta));
+    const double dt = p.mdt;
+    constexpr int B0 = MIXED ? -1 : 0, B1 = MIXED ? BJ : BJ - 1;
+    // the neighbouring warp's facing row: the next warp's lowest row for an upper
+    // lane row, the previous warp's highest row for a lower one (clamped at the
+    // patch's S / N ends, where the ghost values replace what is read)
+    const int nbw = bjl ? (warp + 1 < kXBigWarps ? warp + 1 : warp) : (warp > 0 ? warp - 1 : 0);
+    for (int step = 0; step < p.nt; ++step) {
+        const int par = step & 1;
+        // publish the row that faces the other warp: row jj = BJ-1 of an upper lane row, jj = 0 of a lower one
+        double* mine = &s_ex[par][warp][bjl][i0 + 1];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) mine[ii] = pick<1, 1>(upper, E[ii + 1][BJ], E[ii + 1][1]);
+        __syncthreads();
+        const double* theirs = &s_ex[par][nbw][bjl ^ 1][i0 + 1];
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii) {
+            const double x = theirs[ii];
+            const double sn = __shfl_down_sync(0xffffffffu, E[ii + 1][1], LI);  // lower lane row: its N halo
+            const double ss = __shfl_up_sync(0xffffffffu, E[ii + 1][BJ], LI);   // upper lane row: its S halo
+            E[ii + 1][BJ + 1] = pick<1, 1>(upper, x, sn);
+            E[ii + 1][0] = pick<1, 1>(upper, ss, x);
+        }
+#pragma unroll
+        for (int b = B0; b <= B1; ++b) {
+            E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
+            E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
+        }
+        xt_sweep<BI, BJ, MIXED, true>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2, idx, idy, ixy, dt);
+    }
+
+    // ---- restrict_average in the reference order (gaptooth.cpp:170-194) ------
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) s_u[(i0 + ii) * N2 + j0 + jj] = E[ii + 1][jj + 1];
+    __syncthreads();
+    for (int i = tid; i <= nx; i += NT) {
+        double rs = 0.0;
+        for (int j = 0; j <= ny; ++j) rs = XADD(rs, XMUL(quad_w(j, ny, p.quad), s_u[i * N2 + j]));
+        s_row[i] = rs;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double avg = 0.0;
+        for (int i = 0; i <= nx; ++i) avg = XADD(avg, XMUL(quad_w(i, nx, p.quad), s_row[i]));
         const size_t node = (size_t)pi * p.NF2 + pj;
         if (out_mode == OUT_FIELD) {
             out[node] = avg;
@@ -400,6 +589,7 @@ inline int exact_tile_plan(const Params& p) {
     if (p.bc_type == PD_BC_DIRICHLET) return -1;
     if (p.bc_type == PD_BC_ROBIN && fabs(p.w2) < 1e-300) return -1; // pinned (microsim.cpp:171-174)
     int id = -1;
+    if (p.n1 == 32 && p.n2 == 32) id = p.mixed ? 9 : 8; // the four-warp CTA tile (k_exact_big)
 #define PD_XMATCH(ID, CFG) \
     if (p.n1 == CFG::N1 && p.n2 == CFG::N2 && (p.mixed != 0) == CFG::MIXED) id = ID;
     PD_XTILE_CONFIGS(PD_XMATCH)
@@ -416,6 +606,8 @@ inline void launch_exact_tile(int id, const Params& p, const double* F, double* 
     }
     PD_XTILE_CONFIGS(PD_XLAUNCH)
 #undef PD_XLAUNCH
+    if (id == 8) k_exact_big<false><<<p.P, 32 * kXBigWarps, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail);
+    if (id == 9) k_exact_big<true><<<p.P, 32 * kXBigWarps, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail);
 }
 
 } // namespace pdb200::dev
