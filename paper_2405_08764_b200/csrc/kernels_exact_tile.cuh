@@ -45,6 +45,8 @@ struct XTileCfg {
     static constexpr bool MIXED = MIXED_;
     static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, G = 32 / LP;
     static constexpr int N = N1 * N2, L = N1 > N2 ? N1 : N2;
+    // resident one-warp CTAs per SM the kernel is compiled for (register budget 65536 / (32 MINB))
+    static constexpr int MINB = (MIXED || BI * BJ > 9) ? PD_XT_MIXED_BLOCKS : 12;
     static_assert(N1 % BI == 0 && N2 % BJ == 0, "block must tile the patch");
     static_assert(LP <= 32, "patch must fit a warp");
     // a lane on the W edge must not also be on the E edge (its inner node would
@@ -206,7 +208,7 @@ __device__ __forceinline__ void xt_sweep(double (&E)[BI + 2][BJ + 2], const doub
 }
 
 template <class Cfg>
-__global__ void __launch_bounds__(32, Cfg::MIXED ? PD_XT_MIXED_BLOCKS : 12)
+__global__ void __launch_bounds__(32, Cfg::MINB)
 k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
              const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
              const int* __restrict__ fail_flag, int nunits) {
@@ -573,7 +575,12 @@ using XT9 = XTileCfg<9, 9, 3, 3, false>;
 using XT9M = XTileCfg<9, 9, 3, 3, true>;
 using XT16 = XTileCfg<16, 16, 2, 4, false>;
 using XT16M = XTileCfg<16, 16, 2, 4, true>;
-#define PD_XTILE_CONFIGS(X) X(0, XT7) X(1, XT7M) X(2, XT8) X(3, XT8M) X(4, XT9) X(5, XT9M) X(6, XT16) X(7, XT16M)
+// 11x11 nodes: the reference's default micro grid (nx = ny = 10, scheme_config.hpp:17); one eta
+// column per lane, two patches per warp
+using XT11 = XTileCfg<11, 11, 1, 11, false>;
+using XT11M = XTileCfg<11, 11, 1, 11, true>;
+#define PD_XTILE_CONFIGS(X) \
+    X(0, XT7) X(1, XT7M) X(2, XT8) X(3, XT8M) X(4, XT9) X(5, XT9M) X(6, XT16) X(7, XT16M) X(10, XT11) X(11, XT11M)
 
 // Tile id of the register-blocked EXACT step for these parameters, or -1: the
 // shared-memory kernel (k_gaptooth_exact) carries everything else — ADI,

@@ -19,6 +19,10 @@ U0 = P.initial_field()
 dU = torch.from_numpy(U0.ravel()).cuda(); dS = torch.empty_like(dU)
 print('32x32 2^14 K=50 exact_tile', E.exact_tile, 'kernel ms', E.bench_step_kernel(dU.data_ptr(), dS.data_ptr(), 3))
 """
+code11 = code.replace("configs.sweep_desc(base, 14, 32, 50)", "configs.copy_desc(configs.sweep_desc(base, 16, 16, 50), nx=10, ny=10)").replace("32x32 2^14", "11x11 2^16")
+for v in ("1", "0"):
+    r = subprocess.run([sys.executable, "-c", code11], env=dict(os.environ, PD_EXACT_TILE=v), capture_output=True, text=True)
+    print(r.stdout.strip() or r.stderr[-400:])
 for v in ("1", "0"):
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PD_EXACT_TILE=v), capture_output=True, text=True)
     print(r.stdout.strip() or r.stderr[-400:])

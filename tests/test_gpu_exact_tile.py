@@ -39,6 +39,11 @@ CASES = {
     "8x8-5pt-robin": ("c1_diffusion", dict(nx=7, ny=7, Nt=20, **ROBIN), 4),
     "9x9-mixed-k1": ("c4_shear", dict(nx=8, ny=8, N_xi=10, N_eta=9, nt=20, Nt=5, k=1), 3),
     "16x16-mixed": ("c4_shear", dict(N_xi=33, N_eta=17, Nt=10), 4),
+    # 11x11 nodes: the reference's default micro grid (nx = ny = 10, scheme_config.hpp:17)
+    "11x11-5pt-robin": ("c1_diffusion", dict(nx=10, ny=10, Nt=20, **ROBIN), 4),
+    "11x11-5pt-cdr-simpson": ("c2_cdr_tanh", dict(nx=10, ny=10, N_xi=23, N_eta=23, Nt=20,
+                                                 quadrature=abi.PD_QUAD_SIMPSON), 3),
+    "11x11-mixed-k1": ("c4_shear", dict(nx=10, ny=10, N_xi=10, N_eta=12, nt=20, Nt=5, k=1), 3),
     "32x32-mixed": ("c4_shear", dict(nx=31, ny=31, N_xi=9, N_eta=11, nt=21, Nt=5), 3),
     "32x32-5pt-robin-k1": ("c1_diffusion", dict(nx=31, ny=31, Nt=20, k=1, **ROBIN), 3),
     "32x32-5pt-periodic": ("c3_annulus", dict(nx=31, ny=31, Nt=20, N_xi=16, N_eta=8), 2),
