@@ -630,7 +630,7 @@ __device__ __forceinline__ bool guard_trips(unsigned long long v, int step, int 
 }
 
 template <class Cfg>
-constexpr int run_min_blocks() { return (Cfg::MIXED || Cfg::PAD || Cfg::SRC) ? 8 : 12; }
+constexpr int run_min_blocks() { return (Cfg::MIXED || Cfg::PAD || Cfg::SRC || Cfg::NPL > 9) ? 8 : 12; }
 
 template <class Cfg>
 __global__ void __launch_bounds__(32 * kRunWarps, run_min_blocks<Cfg>() / kRunWarps)
@@ -712,7 +712,7 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
 
 // ---- instantiations --------------------------------------------------------
 // tiles: 7x7 (1x7 blocks, four patches per warp), 8x8 (2x4, four), 9x9 (3x3,
-// three), 16x16 (2x4, one); each with/without the mixed term, exact-fit or
+// three), 11x11 (1x11, two), 16x16 (2x4, one); each with/without the mixed term, exact-fit or
 // padded (PAD), Neumann-only or with Robin/Dirichlet compiled in (GEN)
 #define PD_FAST_TILE(NAME, N, BI, BJ)                                                          \
     using NAME = FastCfg<N, N, BI, BJ, false>;                                                 \
@@ -726,6 +726,7 @@ k_fast_run(Params p, double* __restrict__ UA, double* __restrict__ UB, const int
 PD_FAST_TILE(FC7, 7, 1, 7)
 PD_FAST_TILE(FC8, 8, 2, 4)
 PD_FAST_TILE(FC9, 9, 3, 3)
+PD_FAST_TILE(FC11, 11, 1, 11) // the reference's default micro grid (nx = ny = 10, scheme_config.hpp:17)
 PD_FAST_TILE(FC16, 16, 2, 4)
 #undef PD_FAST_TILE
 // separable-source variants (5-point operator): exact / padded x Neumann / general
@@ -737,6 +738,7 @@ PD_FAST_TILE(FC16, 16, 2, 4)
 PD_FAST_SRC_TILE(FC7, 7, 1, 7)
 PD_FAST_SRC_TILE(FC8, 8, 2, 4)
 PD_FAST_SRC_TILE(FC9, 9, 3, 3)
+PD_FAST_SRC_TILE(FC11, 11, 1, 11)
 PD_FAST_SRC_TILE(FC16, 16, 2, 4)
 #undef PD_FAST_SRC_TILE
 
@@ -745,8 +747,9 @@ PD_FAST_SRC_TILE(FC16, 16, 2, 4)
         X(B + 6, NAME##PG) X(B + 7, NAME##MPG)
 #define PD_FAST_SRC_IDS(X, B, NAME) X(B + 0, NAME##S) X(B + 1, NAME##SP) X(B + 2, NAME##SG) X(B + 3, NAME##SPG)
 #define PD_FAST_CONFIGS(X)                                                                                         \
-    PD_FAST_TILE_IDS(X, 0, FC7) PD_FAST_TILE_IDS(X, 8, FC8) PD_FAST_TILE_IDS(X, 16, FC9) PD_FAST_TILE_IDS(X, 24, FC16) \
-        PD_FAST_SRC_IDS(X, 32, FC7) PD_FAST_SRC_IDS(X, 36, FC8) PD_FAST_SRC_IDS(X, 40, FC9) PD_FAST_SRC_IDS(X, 44, FC16)
+    PD_FAST_TILE_IDS(X, 0, FC7) PD_FAST_TILE_IDS(X, 8, FC8) PD_FAST_TILE_IDS(X, 16, FC9) PD_FAST_TILE_IDS(X, 48, FC11) \
+        PD_FAST_TILE_IDS(X, 24, FC16) PD_FAST_SRC_IDS(X, 32, FC7) PD_FAST_SRC_IDS(X, 36, FC8) PD_FAST_SRC_IDS(X, 40, FC9) \
+        PD_FAST_SRC_IDS(X, 56, FC11) PD_FAST_SRC_IDS(X, 44, FC16)
 
 inline bool plan_fast(const Params& p, FastPlan& plan) {
     // Neumann (every BASELINE config), Robin and Dirichlet patch conditions are
@@ -757,16 +760,22 @@ inline bool plan_fast(const Params& p, FastPlan& plan) {
     if (p.quad == PD_QUAD_SIMPSON && ((p.n1 - 1) % 2 || (p.n2 - 1) % 2)) return false;
     int id = -1;
     // an exact-fit tile first (compile-time extents), else the smallest padded tile
+    // (the 11x11 tile only as an exact fit: its padded variants index their 11-node
+    // columns at run time; PD_FAST_TILE11=0 sends 11x11 to the padded 16x16 tile, for A/B runs)
+    static const bool no11 = [] {
+        const char* e = std::getenv("PD_FAST_TILE11");
+        return e && e[0] == '0';
+    }();
     const bool gen = p.bc_type != PD_BC_NEUMANN;
 #define PD_MATCH(ID, CFG)                                                                                       \
     if (id < 0 && !CFG::PAD && CFG::GEN == gen && CFG::SRC == src && p.n1 == CFG::N1 && p.n2 == CFG::N2 &&        \
-        (p.mixed != 0) == CFG::MIXED)                                                                               \
+        (p.mixed != 0) == CFG::MIXED && !(no11 && CFG::N1 == 11))                                                   \
         id = ID;
     PD_FAST_CONFIGS(PD_MATCH)
 #undef PD_MATCH
 #define PD_MATCH_PAD(ID, CFG)                                                                                   \
-    if (id < 0 && CFG::PAD && CFG::GEN == gen && CFG::SRC == src && p.n1 <= CFG::N1 && p.n2 <= CFG::N2 &&         \
-        (p.mixed != 0) == CFG::MIXED)                                                                               \
+    if (id < 0 && CFG::PAD && CFG::N1 != 11 && CFG::GEN == gen && CFG::SRC == src && p.n1 <= CFG::N1 &&           \
+        p.n2 <= CFG::N2 && (p.mixed != 0) == CFG::MIXED)                                                            \
         id = ID;
     PD_FAST_CONFIGS(PD_MATCH_PAD)
 #undef PD_MATCH_PAD
