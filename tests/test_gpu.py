@@ -851,7 +851,7 @@ def test_fast_padded_tiles_vs_oracle(nx, ny, name, restated, gpu):
 
 
 @pytest.mark.parametrize("bc", ["dirichlet", "robin", "simpson"])
-@pytest.mark.parametrize("nx,ny", [(10, 12), (20, 22)], ids=["one-warp-tile", "32x32-tile"])
+@pytest.mark.parametrize("nx,ny", [(10, 12), (20, 22), (10, 10)], ids=["one-warp-tile", "32x32-tile", "11x11-tile"])
 def test_fast_padded_tiles_patch_conditions(bc, nx, ny, restated, gpu):
     over = dict(nx=nx, ny=ny, Nt=10, **BC_CASES[bc])
     P = load("c1_diffusion", **over)

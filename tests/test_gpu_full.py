@@ -73,6 +73,10 @@ def stride_case(name):
         return Problem(configs.sweep_desc(base, 12, 16, 10))
     if name == "7x7-ragged":  # 100^2 patches: 2500 four-patch units on 1776 co-resident warps
         return load("c1_diffusion", N_xi=101, N_eta=101)
+    if name == "11x11-mixed":  # the exact-fit 1x11 tile, two patches per warp: 2048 units, strided
+        return Problem(configs.copy_desc(configs.sweep_desc(base, 12, 16, 10), nx=10, ny=10))
+    if name == "11x11-5pt":  # 45^2 patches: 1013 two-patch units (ragged), one per warp
+        return load("c1_diffusion", nx=10, ny=10, N_xi=46, N_eta=46)
     raise KeyError(name)
 
 
@@ -86,7 +90,7 @@ def host_pct_error(P, U, ex):
     return (np.abs(Ui - e)[m] / np.abs(e)[m] * 100.0).max() if m.any() else 0.0
 
 
-@pytest.mark.parametrize("case", ["8x8-2^13", "16x16-2^12", "7x7-ragged"])
+@pytest.mark.parametrize("case", ["8x8-2^13", "16x16-2^12", "7x7-ragged", "11x11-mixed", "11x11-5pt"])
 @pytest.mark.parametrize("metric", [False, True], ids=["run", "run_exact"])
 def test_fused_run_with_strided_units_equals_stepwise(case, metric, gpu):
     P = stride_case(case)
