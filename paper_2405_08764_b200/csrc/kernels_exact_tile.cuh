@@ -13,12 +13,13 @@
 // the coefficient tables from global memory and the state from shared memory at
 // every micro-step, with one CTA barrier per step.
 //
-// Scope: the explicit micro-solver, zero source, Neumann or (unpinned) Robin
-// patch edges, the exact-fit tiles 7x7, 8x8, 9x9, 16x16 (one warp per unit) and
+// Scope: the explicit micro-solver, zero source, Neumann / Robin / Dirichlet
+// patch edges (pinned edges: a second copy of the step loop), the exact-fit tiles 7x7, 8x8, 9x9, 16x16 (one warp per unit) and
 // 32x32 (one four-warp CTA per patch, k_exact_big), with or without the mixed term.  Everything else stays on k_gaptooth_exact (exact_tile_plan).
 #pragma once
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "pd_device.cuh"
 #include "kernels_exact.cuh"
@@ -80,7 +81,7 @@ __device__ __forceinline__ double pick(int role, double a, double b) {
 // filled from the neighbouring lanes: ghost values on the patch edges, then
 // the reference's update of every own node (explicit_sweep, microsim.cpp:304-331,
 // + the mixed term after A*uxx).  Shared by the one-warp tiles and the 32x32 CTA tile.
-template <int BI, int BJ, bool MIXED, bool MERGE_ETA>
+template <int BI, int BJ, bool MIXED, bool MERGE_ETA, bool PIN>
 __device__ __forceinline__ void xt_sweep(double (&E)[BI + 2][BJ + 2], const double (&co)[PD_NCOEF][BI][BJ], int role,
                                          double cEx, double cEs, double cEn, double cEy, const double* gbx,
                                          const double* gbs, const double* gbn, const double* gby, double idx2,
@@ -201,10 +202,54 @@ __device__ __forceinline__ void xt_sweep(double (&E)[BI + 2][BJ + 2], const doub
             s = XADD(s, 0.0); // + G with the zero source (microsim.cpp:329)
             nu[ii][jj] = XADD(uc, XMUL(dt, s));
         }
+    if constexpr (PIN) {
+        // pinned edges (Dirichlet, or Robin with w2 ~ 0): the edge nodes take their pinned value,
+        // first match in W, E, S, N order (explicit_sweep, microsim.cpp:306-311); the rows gb*
+        // hold pinned values instead of ghost offsets then.  Applied in reverse so W wins.
+        constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+                if (jj == BJ - 1) nu[ii][jj] = pick<N_, N_>(role, gbn[ii + 1], nu[ii][jj]);
+                if (jj == 0) nu[ii][jj] = pick<S_, S_>(role, gbs[ii + 1], nu[ii][jj]);
+                if (ii == BI - 1) nu[ii][jj] = pick<E_, E_>(role, gbx[jj + 1], nu[ii][jj]);
+                if (ii == 0) nu[ii][jj] = pick<W_, W_>(role, gbx[jj + 1], nu[ii][jj]);
+            }
+    }
 #pragma unroll
     for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
         for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = nu[ii][jj];
+}
+
+// Dirichlet edges pin their nodes from the start (integrate, microsim.cpp:521-530: W, E, S, N in
+// turn, the later edge winning at corners); val rows are the padded pinned-value rows.
+template <int BI, int BJ>
+__device__ __forceinline__ void xt_pin_initial(double (&E)[BI + 2][BJ + 2], int role, const double* gbx,
+                                               const double* gbs, const double* gbn) {
+    constexpr int W_ = ROLE_W, E_ = ROLE_E, S_ = ROLE_S, N_ = ROLE_N;
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+            double u = E[ii + 1][jj + 1];
+            if (ii == 0) u = pick<W_, W_>(role, gbx[jj + 1], u);
+            if (ii == BI - 1) u = pick<E_, E_>(role, gbx[jj + 1], u);
+            if (jj == 0) u = pick<S_, S_>(role, gbs[ii + 1], u);
+            if (jj == BJ - 1) u = pick<N_, N_>(role, gbn[ii + 1], u);
+            E[ii + 1][jj + 1] = u;
+        }
+}
+
+// Edge kind of the patch conditions (evolve_patch, gaptooth.cpp:312-353) and the pinned node
+// values of one edge (pinned_value, microsim.cpp:189-192) into its padded row.
+__device__ __forceinline__ int xt_edge_kind(const Params& p) {
+    return p.bc_type == PD_BC_DIRICHLET ? PD_EDGE_DIRICHLET : p.bc_type == PD_BC_ROBIN ? PD_EDGE_ROBIN : PD_EDGE_NEUMANN;
+}
+__device__ __forceinline__ void xt_pinned_row(const EdgeSh& g, const double* value, const double* slope, double* row,
+                                              int len, int tid, int nth) {
+    for (int k = tid; k < len; k += nth) row[k] = pinned_value_x(g, value, slope, k);
 }
 
 template <class Cfg>
@@ -256,15 +301,15 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
     const double eta_c = XADD(p.c, XMUL(p.Deta, (double)pj));
 
     // ---- edge profiles and ghost offsets (gaptooth.cpp:110-152, microsim.cpp:152-186)
-    const bool robin = p.bc_type == PD_BC_ROBIN;
+    const int kind = xt_edge_kind(p);
     if (valid) {
-        edge_profiles_t(v, xi_c, eta_c, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny, L, true, robin, &s_slope[gs][0][0],
-                        &s_val[gs][0][0], r, LP);
+        edge_profiles_t(v, xi_c, eta_c, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny, L, kind != PD_EDGE_DIRICHLET,
+                        kind != PD_EDGE_NEUMANN, &s_slope[gs][0][0], &s_val[gs][0][0], r, LP);
     }
     __syncwarp();
     double cedge[4] = {0.0, 0.0, 0.0, 0.0}; // E, W, N, S
+    bool pinned = false;
     if (valid) {
-        const int kind = robin ? PD_EDGE_ROBIN : PD_EDGE_NEUMANN;
         EdgeSh eg;
         make_ghost_t(eg, kind, p.w1, p.w2, p.mdxi, +1.0, N2, s_val[gs][PD_EDGE_E], s_slope[gs][PD_EDGE_E],
                      &s_gb[gs][PD_EDGE_E][1], r, LP);
@@ -278,7 +323,14 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
         make_ghost_t(eg, kind, p.w1, p.w2, p.mdeta, -1.0, N1, s_val[gs][PD_EDGE_S], s_slope[gs][PD_EDGE_S],
                      &s_gb[gs][PD_EDGE_S][1], r, LP);
         cedge[PD_EDGE_S] = eg.cEdge;
+        pinned = eg.pinned != 0; // all four edges share the kind: pinned together
+        if (pinned) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                xt_pinned_row(eg, s_val[gs][e], s_slope[gs][e], &s_gb[gs][e][1], e < 2 ? N2 : N1, r, LP);
+        }
     }
+    pinned = __any_sync(0xffffffffu, pinned); // warp-uniform (lanes past the last patch follow)
     __syncwarp();
     // This lane's ghost data, by role: a lane is on at most one xi edge (LI >= 2);
     // on both eta edges only when LJ == 1, where S and N are kept apart.
@@ -331,6 +383,7 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = lift_node_x(lc, p.h_xi, p.h_eta, i0 + ii, j0 + jj);
     }
+    if (kind == PD_EDGE_DIRICHLET) xt_pin_initial<BI, BJ>(E, role, gbx, gbs, gbn);
 
     // ---- K explicit sweeps (microsim.cpp:292-332, 535-550) -------------------
     const double idx2 = XDIV(1.0, XMUL(p.mdxi, p.mdxi)), idy2 = XDIV(1.0, XMUL(p.mdeta, p.mdeta));
@@ -339,23 +392,29 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
     const double dt = p.mdt;
     constexpr int B0 = MIXED ? -1 : 0, B1 = MIXED ? BJ : BJ - 1; // rows / columns whose halo is needed
     constexpr int A0 = MIXED ? -1 : 0, A1 = MIXED ? BI : BI - 1;
+    // (two copies of the loop, with and without the pinned-edge selection: a flag tested
+    // inside the one loop cost the unpinned config-4 step 6 %)
+    auto sweeps = [&](auto pin) {
 #pragma unroll(kXtUnroll)
-    for (int step = 0; step < p.nt; ++step) {
-        // eta halos from lane +-LI, then xi halos (and, for the mixed term, the
-        // corners: the neighbour's eta halo) from lane +-1
+        for (int step = 0; step < p.nt; ++step) {
+            // eta halos from lane +-LI, then xi halos (and, for the mixed term, the
+            // corners: the neighbour's eta halo) from lane +-1
 #pragma unroll
-        for (int ii = 0; ii < BI; ++ii) {
-            E[ii + 1][BJ + 1] = __shfl_down_sync(0xffffffffu, E[ii + 1][1], LI);
-            E[ii + 1][0] = __shfl_up_sync(0xffffffffu, E[ii + 1][BJ], LI);
-        }
+            for (int ii = 0; ii < BI; ++ii) {
+                E[ii + 1][BJ + 1] = __shfl_down_sync(0xffffffffu, E[ii + 1][1], LI);
+                E[ii + 1][0] = __shfl_up_sync(0xffffffffu, E[ii + 1][BJ], LI);
+            }
 #pragma unroll
-        for (int b = B0; b <= B1; ++b) {
-            E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
-            E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
+            for (int b = B0; b <= B1; ++b) {
+                E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
+                E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
+            }
+            xt_sweep<BI, BJ, MIXED, MERGE_ETA, decltype(pin)::value>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby,
+                                                                    idx2, idy2, idx, idy, ixy, dt);
         }
-        xt_sweep<BI, BJ, MIXED, MERGE_ETA>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2, idx, idy,
-                                          ixy, dt);
-    }
+    };
+    if (pinned) sweeps(std::true_type{});
+    else sweeps(std::false_type{});
 
     // ---- restrict_average in the reference order (gaptooth.cpp:170-194) ------
     if (g < G) { // (lanes past the last patch of the warp hold nothing)
@@ -441,13 +500,13 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
     const double eta_c = XADD(p.c, XMUL(p.Deta, (double)pj));
 
     // ---- edge profiles and ghost offsets (gaptooth.cpp:110-152, microsim.cpp:152-186)
-    const bool robin = p.bc_type == PD_BC_ROBIN;
-    edge_profiles_t(v, xi_c, eta_c, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny, L, true, robin, &s_slope[0][0],
-                    &s_val[0][0], tid, NT);
+    const int kind = xt_edge_kind(p);
+    edge_profiles_t(v, xi_c, eta_c, p.Dxi, p.Deta, p.h_xi, p.h_eta, nx, ny, L, kind != PD_EDGE_DIRICHLET,
+                    kind != PD_EDGE_NEUMANN, &s_slope[0][0], &s_val[0][0], tid, NT);
     __syncthreads();
     double cedge[4];
+    bool pinned;
     {
-        const int kind = robin ? PD_EDGE_ROBIN : PD_EDGE_NEUMANN;
         EdgeSh eg;
         make_ghost_t(eg, kind, p.w1, p.w2, p.mdxi, +1.0, N2, s_val[PD_EDGE_E], s_slope[PD_EDGE_E], &s_gb[PD_EDGE_E][1],
                      tid, NT);
@@ -461,6 +520,11 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
         make_ghost_t(eg, kind, p.w1, p.w2, p.mdeta, -1.0, N1, s_val[PD_EDGE_S], s_slope[PD_EDGE_S], &s_gb[PD_EDGE_S][1],
                      tid, NT);
         cedge[PD_EDGE_S] = eg.cEdge;
+        pinned = eg.pinned != 0;
+        if (pinned) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) xt_pinned_row(eg, s_val[e], s_slope[e], &s_gb[e][1], L, tid, NT);
+        }
     }
     __syncthreads();
     const double cEx = isE ? cedge[PD_EDGE_E] : cedge[PD_EDGE_W], cEs = cedge[PD_EDGE_S], cEn = cedge[PD_EDGE_N];
@@ -500,6 +564,7 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
 #pragma unroll
             for (int jj = 0; jj < BJ; ++jj) E[ii + 1][jj + 1] = lift_node_x(lc, p.h_xi, p.h_eta, i0 + ii, j0 + jj);
     }
+    if (kind == PD_EDGE_DIRICHLET) xt_pin_initial<BI, BJ>(E, role, gbx, gbs, gbn);
 
     // ---- K explicit sweeps (microsim.cpp:292-332, 535-550) -------------------
     const double idx2 = XDIV(1.0, XMUL(p.mdxi, p.mdxi)), idy2 = XDIV(1.0, XMUL(p.mdeta, p.mdeta));
@@ -511,29 +576,34 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
     // lane row, the previous warp's highest row for a lower one (clamped at the
     // patch's S / N ends, where the ghost values replace what is read)
     const int nbw = bjl ? (warp + 1 < kXBigWarps ? warp + 1 : warp) : (warp > 0 ? warp - 1 : 0);
-    for (int step = 0; step < p.nt; ++step) {
-        const int par = step & 1;
-        // publish the row that faces the other warp: row jj = BJ-1 of an upper lane row, jj = 0 of a lower one
-        double* mine = &s_ex[par][warp][bjl][i0 + 1];
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii) mine[ii] = pick<1, 1>(upper, E[ii + 1][BJ], E[ii + 1][1]);
-        __syncthreads();
-        const double* theirs = &s_ex[par][nbw][bjl ^ 1][i0 + 1];
-#pragma unroll
-        for (int ii = 0; ii < BI; ++ii) {
-            const double x = theirs[ii];
-            const double sn = __shfl_down_sync(0xffffffffu, E[ii + 1][1], LI);  // lower lane row: its N halo
-            const double ss = __shfl_up_sync(0xffffffffu, E[ii + 1][BJ], LI);   // upper lane row: its S halo
-            E[ii + 1][BJ + 1] = pick<1, 1>(upper, x, sn);
-            E[ii + 1][0] = pick<1, 1>(upper, ss, x);
+    auto sweeps = [&](auto pin) {
+        for (int step = 0; step < p.nt; ++step) {
+            const int par = step & 1;
+            // publish the row that faces the other warp: row jj = BJ-1 of an upper lane row, jj = 0 of a lower one
+            double* mine = &s_ex[par][warp][bjl][i0 + 1];
+    #pragma unroll
+            for (int ii = 0; ii < BI; ++ii) mine[ii] = pick<1, 1>(upper, E[ii + 1][BJ], E[ii + 1][1]);
+            __syncthreads();
+            const double* theirs = &s_ex[par][nbw][bjl ^ 1][i0 + 1];
+    #pragma unroll
+            for (int ii = 0; ii < BI; ++ii) {
+                const double x = theirs[ii];
+                const double sn = __shfl_down_sync(0xffffffffu, E[ii + 1][1], LI);  // lower lane row: its N halo
+                const double ss = __shfl_up_sync(0xffffffffu, E[ii + 1][BJ], LI);   // upper lane row: its S halo
+                E[ii + 1][BJ + 1] = pick<1, 1>(upper, x, sn);
+                E[ii + 1][0] = pick<1, 1>(upper, ss, x);
+            }
+    #pragma unroll
+            for (int b = B0; b <= B1; ++b) {
+                E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
+                E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
+            }
+            xt_sweep<BI, BJ, MIXED, true, decltype(pin)::value>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2,
+                                                                idx, idy, ixy, dt);
         }
-#pragma unroll
-        for (int b = B0; b <= B1; ++b) {
-            E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
-            E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
-        }
-        xt_sweep<BI, BJ, MIXED, true>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2, idx, idy, ixy, dt);
-    }
+    };
+    if (pinned) sweeps(std::true_type{});
+    else sweeps(std::false_type{});
 
     // ---- restrict_average in the reference order (gaptooth.cpp:170-194) ------
 #pragma unroll
@@ -584,7 +654,7 @@ using XT11M = XTileCfg<11, 11, 1, 11, true>;
 
 // Tile id of the register-blocked EXACT step for these parameters, or -1: the
 // shared-memory kernel (k_gaptooth_exact) carries everything else — ADI,
-// sources, pinned (Dirichlet / degenerate Robin) edges, other patch shapes.
+// sources, other patch shapes.
 // PD_EXACT_TILE=0 forces -1 (A/B runs and the equality test of the two kernels).
 inline int exact_tile_plan(const Params& p) {
     static const bool off = [] {
@@ -593,8 +663,6 @@ inline int exact_tile_plan(const Params& p) {
     }();
     if (off) return -1;
     if (p.solver != PD_SOLVER_EXPLICIT || p.source != PD_SOURCE_ZERO) return -1;
-    if (p.bc_type == PD_BC_DIRICHLET) return -1;
-    if (p.bc_type == PD_BC_ROBIN && fabs(p.w2) < 1e-300) return -1; // pinned (microsim.cpp:171-174)
     int id = -1;
     if (p.n1 == 32 && p.n2 == 32) id = p.mixed ? 9 : 8; // the four-warp CTA tile (k_exact_big)
 #define PD_XMATCH(ID, CFG) \

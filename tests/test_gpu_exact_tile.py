@@ -5,8 +5,8 @@ microsim.cpp:292-332; integrate :509-552; gaptooth.cpp:110-194) on the
 lane-per-block mapping.  It must be bit-identical to
 
 * the restated oracle (reference + mixed term) on every tile shape, with and
-  without the mixed term, Neumann and (5-point) Robin patch edges, both
-  quadratures, k = 0 and k = 1, and
+  without the mixed term, Neumann, (5-point) Robin and pinned (Dirichlet,
+  Robin with w2 = 0) patch edges, both quadratures, k = 0 and k = 1, and
 * the shared-memory kernel it replaces (k_gaptooth_exact), which a child
   process runs with PD_EXACT_TILE=0 on the same cases.
 """
@@ -25,6 +25,8 @@ pytestmark = pytest.mark.gpu
 EXACT = abi.PD_MODE_EXACT
 
 ROBIN = dict(bc_type=abi.PD_BC_ROBIN, robin_w1=2.0, robin_w2=1.0)
+DIRICHLET = dict(bc_type=abi.PD_BC_DIRICHLET)
+ROBIN_PINNED = dict(bc_type=abi.PD_BC_ROBIN, robin_w1=1.0, robin_w2=0.0)  # w2 = 0: behaves as Dirichlet
 # name -> (config, overrides, macro steps)
 CASES = {
     "7x7-5pt": ("c1_diffusion", dict(Nt=20), 5),
@@ -39,6 +41,14 @@ CASES = {
     "8x8-5pt-robin": ("c1_diffusion", dict(nx=7, ny=7, Nt=20, **ROBIN), 4),
     "9x9-mixed-k1": ("c4_shear", dict(nx=8, ny=8, N_xi=10, N_eta=9, nt=20, Nt=5, k=1), 3),
     "16x16-mixed": ("c4_shear", dict(N_xi=33, N_eta=17, Nt=10), 4),
+    # pinned edges (Dirichlet; Robin with w2 = 0): edge nodes keep their pinned values
+    "7x7-5pt-dirichlet": ("c1_diffusion", dict(Nt=20, **DIRICHLET), 5),
+    "9x9-5pt-robin-pinned-periodic": ("c3_annulus", dict(Nt=20, **ROBIN_PINNED), 3),
+    "8x8-mixed-dirichlet": ("c4_shear", dict(nx=7, ny=7, N_xi=11, N_eta=9, nt=20, Nt=5, **DIRICHLET), 4),
+    "16x16-mixed-dirichlet-k1": ("c4_shear", dict(N_xi=17, N_eta=33, Nt=10, k=1, **DIRICHLET), 3),
+    "11x11-5pt-dirichlet": ("c1_diffusion", dict(nx=10, ny=10, Nt=20, **DIRICHLET), 4),
+    "32x32-5pt-robin-pinned": ("c1_diffusion", dict(nx=31, ny=31, Nt=20, **ROBIN_PINNED), 3),
+    "32x32-mixed-dirichlet": ("c4_shear", dict(nx=31, ny=31, N_xi=9, N_eta=11, nt=21, Nt=5, **DIRICHLET), 3),
     # 11x11 nodes: the reference's default micro grid (nx = ny = 10, scheme_config.hpp:17)
     "11x11-5pt-robin": ("c1_diffusion", dict(nx=10, ny=10, Nt=20, **ROBIN), 4),
     "11x11-5pt-cdr-simpson": ("c2_cdr_tanh", dict(nx=10, ny=10, N_xi=23, N_eta=23, Nt=20,
