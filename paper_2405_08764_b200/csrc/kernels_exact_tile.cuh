@@ -13,9 +13,12 @@
 // the coefficient tables from global memory and the state from shared memory at
 // every micro-step, with one CTA barrier per step.
 //
-// Scope: the explicit micro-solver, zero source, Neumann / Robin / Dirichlet
-// patch edges (pinned edges: a second copy of the step loop), the exact-fit tiles 7x7, 8x8, 9x9, 16x16 (one warp per unit) and
-// 32x32 (one four-warp CTA per patch, k_exact_big), with or without the mixed term.  Everything else stays on k_gaptooth_exact (exact_tile_plan).
+// Scope: the explicit micro-solver with zero source and any patch condition
+// (Neumann / Robin ghosts; pinned Dirichlet or degenerate-Robin edges run a second
+// copy of the step loop), on the exact-fit tiles 7x7, 8x8, 9x9, 11x11, 16x16 (one
+// warp per unit) and 32x32 (one four-warp CTA per patch, k_exact_big), with or
+// without the mixed term.  Everything else stays on k_gaptooth_exact
+// (exact_tile_plan).
 #pragma once
 
 #include <cstdlib>
