@@ -37,10 +37,11 @@ CASES = {
     "9x9-5pt-cdr": ("c2_cdr_tanh", dict(N_xi=23, N_eta=23, Nt=20), 4),
     "16x16-5pt-robin": ("c1_diffusion", dict(nx=15, ny=15, Nt=20, **ROBIN), 3),
     "7x7-mixed": ("c4_shear", dict(nx=6, ny=6, N_xi=9, N_eta=11, nt=20, Nt=5), 4),
-    "8x8-mixed": ("c4_shear", dict(nx=7, ny=7, N_xi=11, N_eta=9, nt=20, Nt=5), 4),
+    "8x8-mixed": ("c4_shear", dict(nx=7, ny=7, N_xi=11, N_eta=9, nt=21, Nt=5), 4),  # odd nt: the unrolled loop's tail
     "8x8-5pt-robin": ("c1_diffusion", dict(nx=7, ny=7, Nt=20, **ROBIN), 4),
     "9x9-mixed-k1": ("c4_shear", dict(nx=8, ny=8, N_xi=10, N_eta=9, nt=20, Nt=5, k=1), 3),
     "16x16-mixed": ("c4_shear", dict(N_xi=33, N_eta=17, Nt=10), 4),
+    "16x16-mixed-one-micro-step": ("c4_shear", dict(N_xi=9, N_eta=9, nt=1, tau=2e-7, Nt=50), 3),
     # pinned edges (Dirichlet; Robin with w2 = 0): edge nodes keep their pinned values
     "7x7-5pt-dirichlet": ("c1_diffusion", dict(Nt=20, **DIRICHLET), 5),
     "9x9-5pt-robin-pinned-periodic": ("c3_annulus", dict(Nt=20, **ROBIN_PINNED), 3),
