@@ -310,7 +310,7 @@ def run_sweep(args):
                 d = configs.sweep_desc(base, lp, nodes, K)
                 t0 = time.perf_counter()
                 prob = Problem(d)
-                eng = Engine.from_problem(prob)
+                eng = Engine.from_problem(prob, mode=configs.MODE[args.mode])
                 build_s = time.perf_counter() - t0
                 P, N, Kk = workload(prob.desc)
                 mixed = eng.mixed
@@ -339,6 +339,7 @@ def run_sweep(args):
                 par = patch_parity(eng.step_direct(U0, 0.0), ed, idx, avg)
                 row = {"config": "c5_sweep", "log2_patches": lp, "patches": P, "micro_nodes": f"{nodes}x{nodes}", "K": K,
                        "kernel_family": "fast" if eng.mode == abi.PD_MODE_FAST else "exact",
+                       **({} if eng.mode == abi.PD_MODE_FAST else {"exact_tile": bool(eng.exact_tile)}),
                        "updates_per_s": upd / (kms * 1e-3), "step_updates_per_s": upd * steps / (st.device_ms * 1e-3),
                        "kernel_ms": kms, "ms_per_macro_step": st.device_ms / steps, "roofline_bound": bound,
                        "roofline_frac": frac, "fp64_peak_tflops": p64, "hbm_peak_gbs": bw,
