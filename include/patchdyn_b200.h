@@ -178,7 +178,7 @@ void pd_engine_destroy(pd_engine* engine);
  * shapes or features the fast kernel does not cover; never to a CPU path). */
 int32_t pd_engine_mode(const pd_engine* engine);
 /* 1 when the engine's EXACT gap-tooth step runs on the register-blocked tile kernel
- * (k_exact_tile / k_exact_big: explicit solver, zero source,
+ * (k_exact_tile / k_exact_big: explicit solver, zero or separable source,
  * 7x7/8x8/9x9/11x11/16x16/32x32 patches; same bits as the shared-memory EXACT kernel, which carries every other
  * case), 0 otherwise, -1 for NULL.  Replaces nothing in the reference: diagnostics. */
 int32_t pd_engine_exact_tile(const pd_engine* engine);

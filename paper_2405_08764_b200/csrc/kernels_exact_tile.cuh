@@ -13,12 +13,12 @@
 // the coefficient tables from global memory and the state from shared memory at
 // every micro-step, with one CTA barrier per step.
 //
-// Scope: the explicit micro-solver with zero source and any patch condition
-// (Neumann / Robin ghosts; pinned Dirichlet or degenerate-Robin edges run a second
-// copy of the step loop), on the exact-fit tiles 7x7, 8x8, 9x9, 11x11, 16x16 (one
-// warp per unit) and 32x32 (one four-warp CTA per patch, k_exact_big), with or
-// without the mixed term.  Everything else stays on k_gaptooth_exact
-// (exact_tile_plan).
+// Scope: the explicit micro-solver with zero or separable source and any patch
+// condition (Neumann / Robin ghosts; pinned Dirichlet or degenerate-Robin edges and
+// the source each run their own copy of the step loop; both together do not), on
+// the exact-fit tiles 7x7, 8x8, 9x9, 11x11, 16x16 (one warp per unit) and 32x32
+// (one four-warp CTA per patch, k_exact_big), with or without the mixed term.
+// Everything else stays on k_gaptooth_exact (exact_tile_plan).
 #pragma once
 
 #include <cstdlib>
@@ -84,11 +84,12 @@ __device__ __forceinline__ double pick(int role, double a, double b) {
 // filled from the neighbouring lanes: ghost values on the patch edges, then
 // the reference's update of every own node (explicit_sweep, microsim.cpp:304-331,
 // + the mixed term after A*uxx).  Shared by the one-warp tiles and the 32x32 CTA tile.
-template <int BI, int BJ, bool MIXED, bool MERGE_ETA, bool PIN>
+template <int BI, int BJ, bool MIXED, bool MERGE_ETA, bool PIN, bool SRC = false, int NS = 0>
 __device__ __forceinline__ void xt_sweep(double (&E)[BI + 2][BJ + 2], const double (&co)[PD_NCOEF][BI][BJ], int role,
                                          double cEx, double cEs, double cEn, double cEy, const double* gbx,
                                          const double* gbs, const double* gbn, const double* gby, double idx2,
-                                         double idy2, double idx, double idy, double ixy, double dt) {
+                                         double idy2, double idx, double idy, double ixy, double dt,
+                                         const double* spn = nullptr, double ft = 0.0) {
     constexpr int B0 = MIXED ? -1 : 0, B1 = MIXED ? BJ : BJ - 1; // rows / columns whose halo is needed
     constexpr int A0 = MIXED ? -1 : 0, A1 = MIXED ? BI : BI - 1;
     // Patch edges: replace what the shuffles brought by the ghost values
@@ -202,7 +203,11 @@ __device__ __forceinline__ void xt_sweep(double (&E)[BI + 2][BJ + 2], const doub
             s = XSUB(s, XMUL(co[PD_COEF_VX][ii][jj], ux));
             s = XSUB(s, XMUL(co[PD_COEF_VY][ii][jj], uy));
             s = XSUB(s, XMUL(co[PD_COEF_W][ii][jj], uc));
-            s = XADD(s, 0.0); // + G with the zero source (microsim.cpp:329)
+            // + G (microsim.cpp:329): zero, or the separable source spatial(node) * time(t)/l of
+            // sample_source (microsim.cpp:272-277); spn = this lane's block in the staged table
+            double G = 0.0;
+            if constexpr (SRC) G = XMUL(spn[ii * NS + jj], ft);
+            s = XADD(s, G);
             nu[ii][jj] = XADD(uc, XMUL(dt, s));
         }
     if constexpr (PIN) {
@@ -259,7 +264,8 @@ template <class Cfg>
 __global__ void __launch_bounds__(32, Cfg::MINB)
 k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
              const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
-             const int* __restrict__ fail_flag, int nunits) {
+             const int* __restrict__ fail_flag, int nunits, const double* __restrict__ src_sp,
+             const double* __restrict__ src_time) {
     constexpr int BI = Cfg::BI, BJ = Cfg::BJ, LI = Cfg::LI, LJ = Cfg::LJ, LP = Cfg::LP, G = Cfg::G;
     constexpr int N1 = Cfg::N1, N2 = Cfg::N2, N = Cfg::N, L = Cfg::L;
     constexpr int nx = N1 - 1, ny = N2 - 1;
@@ -376,6 +382,18 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
         }
     }
 
+    // separable source (microsim.cpp:272-277): this lane's spatial factors wait in the
+    // restriction tile (free until the sweeps are over), each lane reading only what it wrote
+    const bool has_src = src_sp && src_time; // without time factors g = 0, as k_gaptooth_exact
+    const double* spn = &s_u[gs][i0 * N2 + j0];
+    if (has_src && valid) {
+        const double* sp = src_sp + (size_t)(cset ? cset[patch] : patch) * N;
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) s_u[gs][(i0 + ii) * N2 + j0 + jj] = __ldg(sp + (i0 + ii) * N2 + j0 + jj);
+    }
+
     // ---- StencilPoly::center + lift (gaptooth.cpp:63-72, 154-168) ------------
     // E[a + 1][b + 1] = value at block-relative (a, b), a in [-1, BI], b in [-1, BJ]
     double E[BI + 2][BJ + 2];
@@ -397,9 +415,11 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
     constexpr int A0 = MIXED ? -1 : 0, A1 = MIXED ? BI : BI - 1;
     // (two copies of the loop, with and without the pinned-edge selection: a flag tested
     // inside the one loop cost the unpinned config-4 step 6 %)
-    auto sweeps = [&](auto pin) {
+    auto sweeps = [&](auto pin, auto src) {
 #pragma unroll(kXtUnroll)
         for (int step = 0; step < p.nt; ++step) {
+            double ft = 0.0;
+            if constexpr (decltype(src)::value) ft = __ldg(src_time + step);
             // eta halos from lane +-LI, then xi halos (and, for the mixed term, the
             // corners: the neighbour's eta halo) from lane +-1
 #pragma unroll
@@ -412,12 +432,15 @@ k_exact_tile(Params p, const double* __restrict__ F, double* __restrict__ out, i
                 E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
                 E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
             }
-            xt_sweep<BI, BJ, MIXED, MERGE_ETA, decltype(pin)::value>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby,
-                                                                    idx2, idy2, idx, idy, ixy, dt);
+            xt_sweep<BI, BJ, MIXED, MERGE_ETA, decltype(pin)::value, decltype(src)::value, N2>(
+                E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2, idx, idy, ixy, dt, spn, ft);
         }
     };
-    if (pinned) sweeps(std::true_type{});
-    else sweeps(std::false_type{});
+    // (pinned edges with a source stay on k_gaptooth_exact: exact_tile_plan)
+    if (has_src) sweeps(std::false_type{}, std::true_type{});
+    else if (pinned) sweeps(std::true_type{}, std::false_type{});
+    else sweeps(std::false_type{}, std::false_type{});
+    __syncwarp();
 
     // ---- restrict_average in the reference order (gaptooth.cpp:170-194) ------
     if (g < G) { // (lanes past the last patch of the warp hold nothing)
@@ -467,7 +490,8 @@ template <bool MIXED>
 __global__ void __launch_bounds__(32 * kXBigWarps, MIXED ? 2 : 3)
 k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, int out_mode,
             const int* __restrict__ pij, const int* __restrict__ cset, const double* __restrict__ coeffs,
-            const int* __restrict__ fail_flag) {
+            const int* __restrict__ fail_flag, const double* __restrict__ src_sp,
+            const double* __restrict__ src_time) {
     constexpr int BI = 2, BJ = 4, LI = 16, N1 = 32, N2 = 32, N = N1 * N2, L = 32, NT = 32 * kXBigWarps;
     constexpr int nx = N1 - 1, ny = N2 - 1;
     __shared__ double s_st[9];
@@ -558,6 +582,16 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
         }
     }
 
+    const bool has_src = src_sp && src_time; // separable source, staged as in k_exact_tile
+    const double* spn = &s_u[i0 * N2 + j0];
+    if (has_src) {
+        const double* sp = src_sp + (size_t)(cset ? cset[patch] : patch) * N;
+#pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) s_u[(i0 + ii) * N2 + j0 + jj] = __ldg(sp + (i0 + ii) * N2 + j0 + jj);
+    }
+
     // ---- StencilPoly::center + lift (gaptooth.cpp:63-72, 154-168) ------------
     double E[BI + 2][BJ + 2];
     {
@@ -579,9 +613,11 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
     // lane row, the previous warp's highest row for a lower one (clamped at the
     // patch's S / N ends, where the ghost values replace what is read)
     const int nbw = bjl ? (warp + 1 < kXBigWarps ? warp + 1 : warp) : (warp > 0 ? warp - 1 : 0);
-    auto sweeps = [&](auto pin) {
+    auto sweeps = [&](auto pin, auto src) {
         for (int step = 0; step < p.nt; ++step) {
             const int par = step & 1;
+            double ft = 0.0;
+            if constexpr (decltype(src)::value) ft = __ldg(src_time + step);
             // publish the row that faces the other warp: row jj = BJ-1 of an upper lane row, jj = 0 of a lower one
             double* mine = &s_ex[par][warp][bjl][i0 + 1];
     #pragma unroll
@@ -601,12 +637,14 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
                 E[BI + 1][b + 1] = __shfl_down_sync(0xffffffffu, E[1][b + 1], 1);
                 E[0][b + 1] = __shfl_up_sync(0xffffffffu, E[BI][b + 1], 1);
             }
-            xt_sweep<BI, BJ, MIXED, true, decltype(pin)::value>(E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2,
-                                                                idx, idy, ixy, dt);
+            xt_sweep<BI, BJ, MIXED, true, decltype(pin)::value, decltype(src)::value, N2>(
+                E, co, role, cEx, cEs, cEn, cEy, gbx, gbs, gbn, gby, idx2, idy2, idx, idy, ixy, dt, spn, ft);
         }
     };
-    if (pinned) sweeps(std::true_type{});
-    else sweeps(std::false_type{});
+    if (has_src) sweeps(std::false_type{}, std::true_type{});
+    else if (pinned) sweeps(std::true_type{}, std::false_type{});
+    else sweeps(std::false_type{}, std::false_type{});
+    __syncthreads();
 
     // ---- restrict_average in the reference order (gaptooth.cpp:170-194) ------
 #pragma unroll
@@ -657,7 +695,7 @@ using XT11M = XTileCfg<11, 11, 1, 11, true>;
 
 // Tile id of the register-blocked EXACT step for these parameters, or -1: the
 // shared-memory kernel (k_gaptooth_exact) carries everything else — ADI,
-// sources, other patch shapes.
+// general (sampled) sources, other patch shapes.
 // PD_EXACT_TILE=0 forces -1 (A/B runs and the equality test of the two kernels).
 inline int exact_tile_plan(const Params& p) {
     static const bool off = [] {
@@ -665,7 +703,10 @@ inline int exact_tile_plan(const Params& p) {
         return e && e[0] == '0';
     }();
     if (off) return -1;
-    if (p.solver != PD_SOLVER_EXPLICIT || p.source != PD_SOURCE_ZERO) return -1;
+    if (p.solver != PD_SOLVER_EXPLICIT) return -1;
+    if (p.source != PD_SOURCE_ZERO && p.source != PD_SOURCE_SEPARABLE) return -1;
+    const bool pins = p.bc_type == PD_BC_DIRICHLET || (p.bc_type == PD_BC_ROBIN && fabs(p.w2) < 1e-300);
+    if (p.source == PD_SOURCE_SEPARABLE && pins) return -1; // pinned edges with a source: shared-memory kernel
     int id = -1;
     if (p.n1 == 32 && p.n2 == 32) id = p.mixed ? 9 : 8; // the four-warp CTA tile (k_exact_big)
 #define PD_XMATCH(ID, CFG) \
@@ -676,16 +717,21 @@ inline int exact_tile_plan(const Params& p) {
 }
 
 inline void launch_exact_tile(int id, const Params& p, const double* F, double* out, int out_mode, const int* pij,
-                              const int* cset, const double* coeffs, const int* fail, cudaStream_t s) {
+                              const int* cset, const double* coeffs, const int* fail, cudaStream_t s,
+                              const double* src_sp, const double* src_time) {
+    if (p.source != PD_SOURCE_SEPARABLE) src_sp = nullptr;
 #define PD_XLAUNCH(ID, CFG)                                                                              \
     if (id == ID) {                                                                                      \
         const int nunits = (p.P + CFG::G - 1) / CFG::G;                                                  \
-        k_exact_tile<CFG><<<nunits, 32, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail, nunits); \
+        k_exact_tile<CFG><<<nunits, 32, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail, nunits, src_sp,  \
+                                                src_time);                                              \
     }
     PD_XTILE_CONFIGS(PD_XLAUNCH)
 #undef PD_XLAUNCH
-    if (id == 8) k_exact_big<false><<<p.P, 32 * kXBigWarps, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail);
-    if (id == 9) k_exact_big<true><<<p.P, 32 * kXBigWarps, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail);
+    if (id == 8)
+        k_exact_big<false><<<p.P, 32 * kXBigWarps, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail, src_sp, src_time);
+    if (id == 9)
+        k_exact_big<true><<<p.P, 32 * kXBigWarps, 0, s>>>(p, F, out, out_mode, pij, cset, coeffs, fail, src_sp, src_time);
 }
 
 } // namespace pdb200::dev

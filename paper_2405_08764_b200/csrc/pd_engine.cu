@@ -169,7 +169,7 @@ struct pd_engine {
             launch_fast(fast, prm, F, out, out_mode, d_nbr.p, d_weights.p, fail, stream, srct);
         } else if (const int tile = exact_tile_plan(prm); tile >= 0) {
             // register-blocked EXACT step (kernels_exact_tile.cuh): same arithmetic, bit-identical
-            launch_exact_tile(tile, prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, fail, stream);
+            launch_exact_tile(tile, prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, fail, stream, d_src.p, srct);
         } else {
             k_gaptooth_exact<<<prm.P, exact_threads(prm), exact_smem_bytes(prm), stream>>>(
                 prm, F, out, out_mode, d_pij.p, d_cset.p, d_coeffs.p, d_src.p, srct, fail, nullptr, nullptr,

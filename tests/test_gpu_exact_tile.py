@@ -6,7 +6,8 @@ lane-per-block mapping.  It must be bit-identical to
 
 * the restated oracle (reference + mixed term) on every tile shape, with and
   without the mixed term, Neumann, (5-point) Robin and pinned (Dirichlet,
-  Robin with w2 = 0) patch edges, both quadratures, k = 0 and k = 1, and
+  Robin with w2 = 0) patch edges, the separable source, both quadratures,
+  k = 0 and k = 1, and
 * the shared-memory kernel it replaces (k_gaptooth_exact), which a child
   process runs with PD_EXACT_TILE=0 on the same cases.
 """
@@ -50,6 +51,12 @@ CASES = {
     "11x11-5pt-dirichlet": ("c1_diffusion", dict(nx=10, ny=10, Nt=20, **DIRICHLET), 4),
     "32x32-5pt-robin-pinned": ("c1_diffusion", dict(nx=31, ny=31, Nt=20, **ROBIN_PINNED), 3),
     "32x32-mixed-dirichlet": ("c4_shear", dict(nx=31, ny=31, N_xi=9, N_eta=11, nt=21, Nt=5, **DIRICHLET), 3),
+    # separable source g = spatial(x, y) time(t) / l (sample_source, microsim.cpp:272-277)
+    "src-7x7": ("ref_cdr", dict(nx=6, ny=6), 3),
+    "src-9x9-k1": ("ref_cdr", dict(nx=8, ny=8, k=1), 3),
+    "src-11x11-robin": ("ref_cdr", dict(nx=10, ny=10, **ROBIN), 3),
+    "src-16x16": ("ref_cdr", dict(nx=15, ny=15, nt=1200), 2),
+    "src-32x32": ("ref_cdr", dict(nx=31, ny=31, N_xi=6, N_eta=6, nt=5000), 2),
     # 11x11 nodes: the reference's default micro grid (nx = ny = 10, scheme_config.hpp:17)
     "11x11-5pt-robin": ("c1_diffusion", dict(nx=10, ny=10, Nt=20, **ROBIN), 4),
     "11x11-5pt-cdr-simpson": ("c2_cdr_tanh", dict(nx=10, ny=10, N_xi=23, N_eta=23, Nt=20,
@@ -64,17 +71,32 @@ CASES = {
 }
 
 
-def run_case(name):
+def make_problem(name):
     cfg, over, n = CASES[name]
-    d, _ = configs.load(cfg)
-    P = Problem(configs.copy_desc(d, **over))
+    if cfg == "ref_cdr":  # the reference's CDR problem with its separable source, explicit solver
+        d = configs.default_desc()
+        d.problem = abi.PD_PROBLEM_REF_CDR
+        d.N_xi = d.N_eta = 10
+        d.Nt, d.T, d.tau = 1001, 1.0, 1e-6
+        d.nt = 500  # 2-D explicit stability: dt/d^2 = 0.2 per direction
+    else:
+        d, _ = configs.load(cfg)
+    return Problem(configs.copy_desc(d, **over)), n
+
+
+def source_time(P, n):
+    return P.source_time(0.0, n) if P.engine_desc().source_kind == abi.PD_SOURCE_SEPARABLE else None
+
+
+def run_case(name):
+    P, n = make_problem(name)
     U0 = P.initial_field()
     bt = P.boundary_table(0.0, n)
     E = Engine.from_problem(P, mode=EXACT)
     assert E.mode == EXACT
     # the tile kernel is the one that runs (except in the PD_EXACT_TILE=0 child and on 17x17 nodes)
     assert E.exact_tile == (os.environ.get("PD_EXACT_TILE") != "0" and not name.startswith("17x17"))
-    U, st = E.run(U0, n, bnd=bt)
+    U, st = E.run(U0, n, bnd=bt, src_time=source_time(P, n))
     assert st.steps_done == n
     return P, U0, bt, n, U
 
@@ -82,7 +104,7 @@ def run_case(name):
 @pytest.mark.parametrize("name", list(CASES))
 def test_exact_tile_bit_identical_to_oracle(name, restated, gpu):
     P, U0, bt, n, U = run_case(name)
-    st, Uo, _ = restated.run(P.engine_desc(), U0, n, bnd=bt)
+    st, Uo, _ = restated.run(P.engine_desc(), U0, n, bnd=bt, src_time=source_time(P, n))
     assert st == abi.PD_OK
     assert np.array_equal(U, Uo)
 
