@@ -597,6 +597,25 @@ def run_sharded(args, desc, rank, world, local):
     mine = torch.tensor([eng.P], device=cdev, dtype=torch.float64)
     most = mine.clone()
     dist.all_reduce(most, op=dist.ReduceOp.MAX)
+    roof = None
+    if rank == 0:
+        # roofline of the busiest rank's slab: its patches' algorithmic flops / bytes per macro
+        # step against the whole step's device time (the step kernel is > 99 % of it at N = 1)
+        from paper_2405_08764_b200.engine import fp64_peak
+        p64, ghz = fp64_peak(200.0)
+        bw, bw_src = peaks()
+        mixed = bool(eng.mixed)
+        Pm = int(most.item())
+        t_fp = Pm * N * K * flops_per_update(mixed) / (p64 * 1e12)
+        t_bw = Pm * (N * 8 * (6 if mixed else 5) + 16) / (bw * 1e9)
+        step_s = ms * 1e-3 / args.steps
+        roof = {"bound": "fp64" if t_fp >= t_bw else "hbm",
+                "achieved": (Pm * N * K * flops_per_update(mixed) / step_s / 1e12 if t_fp >= t_bw
+                             else Pm * (N * 8 * (6 if mixed else 5) + 16) / step_s / 1e9),
+                "peak": p64 if t_fp >= t_bw else bw, "unit": "TFLOP/s" if t_fp >= t_bw else "GB/s",
+                "frac": max(t_fp, t_bw) / step_s, "traffic": None,
+                "kernel": "per-rank fused step over the busiest slab (whole macro step timed, max over ranks)",
+                "peak_source": f"FP64 DFMA microbenchmark on rank 0 at {ghz:.3f} GHz; HBM {bw} GB/s from {bw_src}"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -607,7 +626,7 @@ def run_sharded(args, desc, rank, world, local):
                 "failed_step": res.failed_step, "exchange": exchange,
                 **({"one_device_test": "all ranks on cuda:0 (PD_BENCH_ONE_DEVICE): not a scaling number"}
                    if one_dev else {}),
-                "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
+                "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk}
         print(json.dumps(line), flush=True)
     if use_peer:
         dist.barrier()

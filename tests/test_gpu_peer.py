@@ -207,6 +207,7 @@ def test_bench_multi_rank_path_runs_peer_exchange(gpu):
     assert line["n_gpus"] == 2 and line["steps_done"] == 4 and line["failed_step"] == 0
     assert line["exchange"].startswith("fused peer-memory halo") and line["value"] > 0
     assert line["gpu_launches"] > 0
+    assert line["scaling"] == "strong" and 0.0 < line["roofline"]["frac"] < 1.0
 
 
 def _peer_vs_single(P, mode, world, nsteps, bnd=None, src=None, linear=False):
