@@ -614,6 +614,7 @@ k_exact_big(Params p, const double* __restrict__ F, double* __restrict__ out, in
     // patch's S / N ends, where the ghost values replace what is read)
     const int nbw = bjl ? (warp + 1 < kXBigWarps ? warp + 1 : warp) : (warp > 0 ? warp - 1 : 0);
     auto sweeps = [&](auto pin, auto src) {
+#pragma unroll(kXtUnroll)
         for (int step = 0; step < p.nt; ++step) {
             const int par = step & 1;
             double ft = 0.0;
