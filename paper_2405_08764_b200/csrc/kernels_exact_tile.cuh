@@ -36,6 +36,11 @@ namespace pdb200::dev {
 #define PD_XT_MIXED_BLOCKS 8
 #endif
 
+// the same for the 5-point tiles (12: 168 registers; 8: 218 registers, config 2 27.9 -> 30.0 us per launch)
+#ifndef PD_XT_PLAIN_BLOCKS
+#define PD_XT_PLAIN_BLOCKS 12
+#endif
+
 // micro-steps per loop trip: 2 lets ptxas overlap a step's tail with the next one's halo exchange
 // (config 4 9.01 -> 8.85 ms, config 2 28.3 -> 28.0 us per launch)
 #ifndef PD_XT_UNROLL
@@ -50,7 +55,7 @@ struct XTileCfg {
     static constexpr int LI = N1 / BI, LJ = N2 / BJ, LP = LI * LJ, G = 32 / LP;
     static constexpr int N = N1 * N2, L = N1 > N2 ? N1 : N2;
     // resident one-warp CTAs per SM the kernel is compiled for (register budget 65536 / (32 MINB))
-    static constexpr int MINB = (MIXED || BI * BJ > 9) ? PD_XT_MIXED_BLOCKS : 12;
+    static constexpr int MINB = (MIXED || BI * BJ > 9) ? PD_XT_MIXED_BLOCKS : PD_XT_PLAIN_BLOCKS;
     static_assert(N1 % BI == 0 && N2 % BJ == 0, "block must tile the patch");
     static_assert(LP <= 32, "patch must fit a warp");
     // a lane on the W edge must not also be on the E edge (its inner node would

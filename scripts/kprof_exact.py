@@ -11,7 +11,7 @@ if which in ('big', 'x11', 'f11'):
     base, _ = configs.load('c5_sweep')
     d = configs.sweep_desc(base, 14, 32, 50) if which == 'big' else configs.copy_desc(configs.sweep_desc(base, 16, 16, 50), nx=10, ny=10)
 else:
-    d, _ = configs.load('c4_shear' if which == 'c4' else 'c2_cdr_tanh')
+    d, _ = configs.load({'c4': 'c4_shear', 'c1': 'c1_diffusion', 'c3': 'c3_annulus'}.get(which, 'c2_cdr_tanh'))
 P = Problem(d)
 E = Engine.from_problem(P, mode=0 if which == 'f11' else 1)
 U0 = P.initial_field()
