@@ -113,6 +113,48 @@ __global__ void k_guard(const double* __restrict__ U, size_t n, unsigned long lo
     }
 }
 
+// refresh_boundary (gaptooth.cpp:296-310) and the blow-up guard (cpi.cpp:187-202) of one
+// macro step in ONE launch (the multi-launch run loop, k = 0): every thread refreshes its share
+// of the perimeter and keeps what it wrote, then scans the nodes the refresh does not own (the
+// patch nodes, written by the step kernel before this launch); together that is max |U| over the
+// refreshed field, the same slot value and decision as k_refresh followed by k_guard.
+__global__ void k_refresh_guard(Params p, double* __restrict__ out, const double* __restrict__ F,
+                                const double* __restrict__ bnd, unsigned long long* slot, unsigned int* counter,
+                                int* fail_flag, int* fail_nonfinite, int step, double blowup) {
+    if (*fail_flag) return;
+    const int stride = gridDim.x * blockDim.x, t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nperim = 2 * (p.Nxi + 1) + 2 * (p.Neta + 1);
+    unsigned long long m = 0;
+    for (int t = t0; t < nperim; t += stride)
+        m = max(m, (unsigned long long)__double_as_longlong(refresh_one(p, out, F, bnd, t, false)));
+    // nodes outside the refresh: columns i_lo .. Nxi-1, rows 1 .. Neta-1 (column 0 holds patch
+    // results when xi is periodic)
+    const int i_lo = p.periodic ? 0 : 1, ni = p.Nxi - i_lo, nj = p.Neta - 1;
+    const size_t n = (size_t)ni * nj;
+    for (size_t t = t0; t < n; t += stride) {
+        const size_t node = (size_t)(i_lo + (int)(t / nj)) * p.NF2 + 1 + (int)(t % nj);
+        m = max(m, (unsigned long long)__double_as_longlong(fabs(out[node])));
+    }
+    m = warp_max_u64(m);
+    __shared__ unsigned long long wm[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = max(m, wm[w]);
+        atomicMax(slot + step, m);
+        __threadfence();
+        const unsigned int prev = atomicAdd(counter + step, 1u);
+        if (prev == gridDim.x - 1) {
+            const unsigned long long v = atomicAdd(slot + step, 0ull);
+            const bool nonfinite = v >= 0x7FF0000000000000ull;
+            if (nonfinite || __longlong_as_double((long long)v) > blowup) {
+                *fail_nonfinite = nonfinite ? 1 : 0;
+                atomicExch(fail_flag, step + 1);
+            }
+        }
+    }
+}
+
 // ---- cpi::run's per-step exact-error metric (max_percent_error, cpi.cpp:79-94) ----
 // max over the patch nodes i in [i_lo, Nxi-1], j in [1, Neta-1] (i_lo = 0 when
 // periodic) with |exact| >= 1e-12 of |U - exact| / |exact| * 100, in the

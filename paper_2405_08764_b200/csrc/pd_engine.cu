@@ -770,11 +770,27 @@ pd_status run_device_impl(pd_engine* e, double* U, double* scratch, int32_t nste
         } else {
             double* cur = U;
             double* nxt = scratch;
+            // k = 0 on a full field: the boundary refresh and the guard share one launch
+            // (k_refresh_guard; PD_FUSED_GUARD=0 keeps k_refresh + k_guard, for A/B runs)
+            static const bool fuse_guard = [] {
+                const char* v = std::getenv("PD_FUSED_GUARD");
+                return !(v && v[0] == '0');
+            }();
+            const bool rg = fuse_guard && e->prm.k == 0 && !e->subset && !e->samp_coef && !e->samp_src;
             for (int n = 0; n < nsteps; ++n) {
-                e->projective_dev(cur, nxt, bnd ? bnd + pk * n : nullptr,
-                                  (src_time && e->prm.source) ? src_time + sk * n : nullptr, e->d_fail.p);
-                k_guard<<<gblocks, 256, 0, e->stream>>>(nxt, NF, e->d_slot.p, e->d_counter.p, e->d_fail.p,
-                                                        e->d_fail.p + 1, n, blowup);
+                const double* bn = bnd ? bnd + pk * n : nullptr;
+                const double* sn = (src_time && e->prm.source) ? src_time + sk * n : nullptr;
+                if (rg) {
+                    e->sub_m = 0;
+                    e->launch_step(cur, nxt, OUT_PROJECTIVE, sn, e->d_fail.p);
+                    k_refresh_guard<<<gblocks, 256, 0, e->stream>>>(e->prm, nxt, cur, bn ? bn + e->perim : nullptr,
+                                                                    e->d_slot.p, e->d_counter.p, e->d_fail.p,
+                                                                    e->d_fail.p + 1, n, blowup);
+                } else {
+                    e->projective_dev(cur, nxt, bn, sn, e->d_fail.p);
+                    k_guard<<<gblocks, 256, 0, e->stream>>>(nxt, NF, e->d_slot.p, e->d_counter.p, e->d_fail.p,
+                                                            e->d_fail.p + 1, n, blowup);
+                }
                 e->check_launch();
                 if (exact) {
                     k_exact_err<<<gblocks, 256, 0, e->stream>>>(e->prm, nxt, exact + NF * n,

@@ -43,8 +43,9 @@ def test_full_run_vs_reference(name, mode, gpu):
     U1 = E.projective_step(U0, 0.0, bnd=P.boundary_table(0.0, 1)[0])
     UT, stats = E.run(U0, Nt, bnd=P.boundary_table(0.0, Nt))
     assert stats.steps_done == Nt and stats.failed_step == 0
-    # FAST: the whole run is one cooperative launch (k_fast_run); EXACT: fused step + refresh + guard per step
-    assert stats.kernel_launches == (1 if mode == FAST else 3 * Nt)
+    # FAST: the whole run is one cooperative launch (k_fast_run); EXACT: the fused step and one
+    # refresh + guard launch (k_refresh_guard) per step
+    assert stats.kernel_launches == (1 if mode == FAST else 2 * Nt)
     if mode == EXACT:
         assert np.array_equal(U1, FINALS[f"{name}_U1"])
         assert np.array_equal(UT, FINALS[f"{name}_final"])
@@ -69,8 +70,8 @@ def test_run_exact_error_metric_vs_reference(name, mode, gpu):
     UT, stats, err = E.run_exact(U0, Nt, ex, bnd=bt)
     assert stats.steps_done == Nt and err.shape == (Nt,)
     # FAST: still the single-launch run (k_fast_run measures after each grid barrier);
-    # EXACT: step, refresh, guard, error per step — no host round trip either way
-    assert stats.kernel_launches == (1 if mode == FAST else 4 * Nt)
+    # EXACT: step, refresh + guard, error per step — no host round trip either way
+    assert stats.kernel_launches == (1 if mode == FAST else 3 * Nt)
     if mode == EXACT:
         assert np.array_equal(UT, FINALS[f"{name}_final"])
         assert err.max() == float(FINALS[f"{name}_maxpct"])
@@ -569,7 +570,7 @@ def test_linear_run_single_cta_and_multilaunch_vs_oracle(N, k, restated, gpu):
     assert st == 0 and np.array_equal(U, Uo)
     assert stats.umax_last == so.umax_last and stats.blowup_threshold == so.blowup_threshold
     block = (2 if k == 0 else 3) * (N + 1) ** 2 * 8 <= 220 * 1024
-    assert stats.kernel_launches == (1 if block else 20 * (3 if k == 0 else 2 * (k + 1) + 3))
+    assert stats.kernel_launches == (1 if block else 20 * (2 if k == 0 else 2 * (k + 1) + 3))
 
 
 @pytest.mark.parametrize("N", [19, 127])
